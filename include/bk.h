@@ -1,0 +1,205 @@
+/*
+ * bk.h -- C ABI of the B200-native block-Krylov hot path of arxiv 2504.02117
+ * ("vectorised DIRK time integration via block Krylov").
+ *
+ * The paper reformulates m DIRK stages x s time steps as ONE matrix equation
+ * A X = B with k = s*m columns (§2.1, eq. (matrix-fixed-point-
+ * equation)) and solves it with a vectorised block Krylov method
+ * (Algorithm 1 "solve JV = R").  The solver's time is spent in the
+ * block operator apply (BOP, §3), the k x k block inner products
+ * and the block updates.  This library exports exactly those calls.
+ *
+ * Conventions (all entry points):
+ *  - Values are IEEE float64; CSR indices int32 (nnz < 2^31); sizes int64.
+ *  - Multivectors are ROW-MAJOR N x k with leading dimension ld >= k (all k
+ *    entries of a row adjacent: the SIMD/lane axis of the paper).
+ *  - Small matrices (C, G) are ROW-MAJOR and act as RIGHT multipliers, so the
+ *    paper's "(A_2 - beta I)^T" is passed already transposed.
+ *  - Pointers to multivectors and small matrices may be DEVICE memory (of the
+ *    ctx's device) or HOST memory (pinned or pageable).  Device pointers make
+ *    the call stream-ordered and asynchronous on the ctx stream.  Host pointers
+ *    are staged through library-owned device buffers; the call then returns
+ *    only after host outputs are written (synchronous).
+ *  - The caller owns every buffer it passes; the library never frees or
+ *    retains them after return.  bk_csr_create COPIES the matrix.
+ *  - Argument/contract violations return BK_ERR_ARG before any work is
+ *    enqueued; the message is available from bk_last_error(ctx).  CUDA/NCCL
+ *    failures return BK_ERR_CUDA / BK_ERR_NCCL and are sticky for the ctx.
+ *  - One ctx per host thread / stream.  Outputs must not alias inputs unless
+ *    stated.  No CPU fallback exists: every numeric step runs in sm_100a kernels.
+ */
+#ifndef BK_H
+#define BK_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define BK_MAX_K 32          /* max block width k of apply / update / solve  */
+#define BK_MAX_KA 4096       /* max rows of a (multi-)Gram result            */
+
+enum bk_status {
+    BK_OK = 0,
+    BK_ERR_ARG = 1,          /* invalid argument, nothing was enqueued       */
+    BK_NOT_CONVERGED = 2,    /* solver hit max_iters (X = last iterate)      */
+    BK_BREAKDOWN = 3,        /* singular k x k block (report.breakdown_column) */
+    BK_ERR_CUDA = 4,
+    BK_ERR_NCCL = 5,
+    BK_ERR_OOM = 6,
+    BK_ERR_UNSUPPORTED = 7
+};
+
+typedef struct bk_ctx bk_ctx;
+typedef struct bk_csr bk_csr;
+
+/* ---------------------------------------------------------------- context */
+int         bk_version(void);                       /* e.g. 100 = 0.1.0      */
+const char *bk_status_string(int status);
+/* Message of the last failure on ctx (never NULL; "" if none).            */
+const char *bk_last_error(const bk_ctx *ctx);
+
+/* Create a context on CUDA device `device`, ordering work on `cuda_stream`
+ * (a cudaStream_t, used as is; NULL = the legacy default stream).  The
+ * stream stays owned by the caller.                                        */
+int bk_ctx_create(bk_ctx **out, int device, void *cuda_stream);
+int bk_ctx_set_stream(bk_ctx *ctx, void *cuda_stream);
+int bk_ctx_synchronize(bk_ctx *ctx);
+int bk_ctx_destroy(bk_ctx *ctx);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * contiguous row partition (z-slabs for lexicographic grids);
+ * halo rows exchanged with NCCL send/recv over NVLink, overlapped with the
+ * interior rows; k x k Gram matrices summed with NCCL allreduce.
+ * bk_get_nccl_unique_id: rank 0 fills 128 bytes, the caller broadcasts them
+ * (e.g. torch.distributed) and every rank calls bk_ctx_set_comm collectively. */
+int bk_get_nccl_unique_id(void *out128);
+int bk_ctx_set_comm(bk_ctx *ctx, const void *uid128, int nranks, int rank);
+int bk_ctx_comm_info(const bk_ctx *ctx, int *nranks, int *rank);
+
+/* ---------------------------------------------------------------- matrix
+ * Local row slab [row_begin, row_begin + n_local) of an n_global x n_global
+ * CSR matrix (SPEC S:26-31 invariants: row_ptr[0] = 0, non-decreasing,
+ * row_ptr[n_local] = nnz, columns strictly increasing per row, GLOBAL column
+ * ids in [0, n_global)).  Arrays may be host or device; they are copied (and
+ * for nranks > 1 renumbered: local columns first, then ghost columns, and
+ * split into interior/boundary rows).  For nranks > 1 the call is collective
+ * (it exchanges the halo plan).  With a single rank, row_begin must be 0 and
+ * n_local == n_global.                                                      */
+int bk_csr_create(bk_ctx *ctx, bk_csr **out, int64_t n_global, int64_t row_begin,
+                  int64_t n_local, const int32_t *row_ptr, const int32_t *col_global,
+                  const double *val, int64_t nnz);
+int bk_csr_destroy(bk_csr *A);
+
+typedef struct bk_csr_info {
+    int64_t n_global, row_begin, n_local, nnz;
+    int64_t n_ghost;          /* ghost rows received per apply              */
+    int64_t n_boundary_rows;  /* rows touching a ghost column               */
+    int64_t n_send_rows;      /* rows sent to other ranks per apply         */
+    int     n_neighbors;
+    int     interior_contiguous; /* interior rows form one contiguous range */
+} bk_csr_info;
+int bk_csr_get_info(const bk_csr *A, bk_csr_info *info);
+
+/* ---------------------------------------------------------------- kernels */
+
+/* a1: Block operator apply (BOP, §3; column independence
+ * (I_m (x) A) vec X = vec(A X), §2.1; coupling term -K Y C with
+ * C = (A_2 - beta I)^T of eq. (matrix-fixed-point-equation)):
+ *
+ *     Y = alpha * (A X) C + beta * Y
+ *
+ * X: n_local x k (ld ldx), the LOCAL slab only (ghost rows are fetched by the
+ *    library with NCCL when nranks > 1).  1 <= k <= BK_MAX_K.
+ * C: k x k_out row-major, or NULL for C = I (then k_out must equal k).
+ * Y: n_local x k_out (ld ldy).  beta == 0: Y is not read.  Y must not alias X.
+ * Streams the CSR once for all k columns.                      */
+int bspmm_apply(bk_ctx *ctx, const bk_csr *A, int k, const double *X, int64_t ldx,
+                const double *C, int k_out, double alpha, double beta,
+                double *Y, int64_t ldy);
+
+/* a3: Block Gram / block inner product (§1 P:43 "information
+ * exchange between the columns"):  G = X^T Y,  G[a][b] = sum_i X[i,a] Y[i,b].
+ * X: n x ka (ldx), Y: n x kb (ldy); 1 <= ka <= BK_MAX_KA, 1 <= kb <= BK_MAX_K.
+ * G: ka x kb row-major (host or device).  Deterministic: fixed-order two-stage
+ * reduction, bitwise reproducible run to run.  flags & BK_GRAM_ALLREDUCE sums
+ * G over the ctx's ranks (NCCL allreduce) -- every rank gets identical bits. */
+#define BK_GRAM_ALLREDUCE 1
+int block_gram(bk_ctx *ctx, int64_t n, int ka, int kb, const double *X, int64_t ldx,
+               const double *Y, int64_t ldy, double *G, int flags);
+
+/* a5: Block update (block axpy of the Krylov recurrences; the splitting RHS
+ * terms B A_2^T, -M Y (A_1 - I/tau)^T of P:389-395 with M = h^d I):
+ *
+ *     X = a * X + s * P C
+ *
+ * X: n x k (ldx), P: n x kp (ldp), C: kp x k row-major (host or device).
+ * 1 <= k <= BK_MAX_K, 1 <= kp <= BK_MAX_KA.  a == 0: X is not read.
+ * P may alias X only when P == X, ldp == ldx and kp == k (in-place X C).    */
+int block_update(bk_ctx *ctx, int64_t n, int kp, int k, double a, double *X, int64_t ldx,
+                 double s, const double *P, int64_t ldp, const double *C);
+
+/* a6: Block Krylov solve of A X = B (Algorithm 1 "solve
+ * JV = R"; DUNE-ISTL Block-CG / Block-BiCGStab P:932-934, P:1054-1056,
+ * P:1346-1348; O'Leary block CG P:43).  X holds X0 on entry (ignored when
+ * opts->x0_is_zero) and the last iterate on return.  Convergence: every column
+ * ||B_c - (A X)_c||_2 <= rtol ||B_c - (A X0)_c||_2 ("defect reduction
+ * ... for all right-hand-sides"), using the method's recurrence residual;
+ * rep->true_relres is recomputed from scratch at the end.
+ * Returns BK_OK, BK_NOT_CONVERGED or BK_BREAKDOWN (also in rep->status).   */
+enum bk_method  { BK_CG = 0, BK_GMRES = 1, BK_BICGSTAB = 2 };
+enum bk_precond { BK_PRECOND_NONE = 0, BK_PRECOND_JACOBI = 1 };
+enum bk_conv    { BK_CONV_ALL = 0, BK_CONV_FIRST = 1 };
+
+typedef struct bk_solve_opts {
+    int    method;          /* enum bk_method                                 */
+    int    max_iters;       /* block iterations (GMRES: inner steps, total)   */
+    int    restart;         /* GMRES(m): m >= 1                               */
+    int    precond;         /* enum bk_precond (JACOBI: CG only)              */
+    int    conv_mode;       /* enum bk_conv                                   */
+    int    x0_is_zero;      /* 1: ignore X on entry                           */
+    int    check_every;     /* host-side convergence poll period (>= 1)       */
+    int    use_graphs;      /* 1: replay iterations as CUDA graphs            */
+    double rtol;
+    double breakdown_tol;   /* relative pivot threshold (default 1e-13)       */
+} bk_solve_opts;
+
+typedef struct bk_solve_report {
+    int     status;           /* BK_OK / BK_NOT_CONVERGED / BK_BREAKDOWN      */
+    int     iterations;
+    int     converged;
+    int     breakdown_column; /* -1 if none                                   */
+    double  relres[BK_MAX_K];      /* recurrence residual / initial, per column */
+    double  true_relres[BK_MAX_K]; /* ||B - A X|| / initial, recomputed       */
+    double  t_total_ms;
+    int64_t n_spmm, n_gram, n_update, n_small, n_allreduce;
+} bk_solve_report;
+
+void bk_solve_opts_default(bk_solve_opts *opts);
+
+int block_krylov_solve(bk_ctx *ctx, const bk_csr *A, int k, const double *B, int64_t ldb,
+                       double *X, int64_t ldx, const bk_solve_opts *opts,
+                       bk_solve_report *rep);
+
+/* ---------------------------------------------------------------- host-only
+ * Halo plan of a contiguous row partition (pure host code, no CUDA; exported
+ * for CPU tests of the multi-GPU path).  Given this rank's local CSR columns
+ * (global ids) and the partition bounds rank_begin[0..nranks] (rank r owns
+ * rows [rank_begin[r], rank_begin[r+1])), computes:
+ *   ghost_ids[n_ghost]   sorted global ids of non-local columns,
+ *   ghost_owner[n_ghost] owning rank of each,
+ *   col_local[nnz]       renumbered columns: local j -> j - row_begin,
+ *                        ghost g -> n_local + (index of g in ghost_ids),
+ *   is_boundary[n_local] 1 if the row touches a ghost column.
+ * Output arrays are caller-allocated (ghost arrays sized nnz for safety).
+ * Returns BK_OK or BK_ERR_ARG.                                              */
+int bk_plan_halo(int nranks, int rank, const int64_t *rank_begin,
+                 int64_t n_local, const int32_t *row_ptr, const int32_t *col_global,
+                 int64_t nnz, int64_t *n_ghost, int64_t *ghost_ids, int32_t *ghost_owner,
+                 int32_t *col_local, uint8_t *is_boundary);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BK_H */

@@ -1,0 +1,594 @@
+// abi.cpp -- the C ABI of include/bk.h: argument validation, host/device
+// staging, contexts, matrix ingest (copy + renumbering + halo plan) and the
+// three kernel entry points.  Every numeric step is a kernel launched from
+// here or from solve.cpp; there is no CPU compute path.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "bk_internal.h"
+
+using namespace bk;
+
+namespace bk {
+
+int set_error(bk_ctx* ctx, int code, const std::string& msg) {
+    if (ctx) {
+        ctx->last_error = msg;
+        if (code == BK_ERR_CUDA || code == BK_ERR_NCCL) ctx->sticky = code;
+    }
+    return code;
+}
+
+int cuda_check(bk_ctx* ctx, cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return BK_OK;
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s: %s", where, cudaGetErrorString(e));
+    return set_error(ctx, e == cudaErrorMemoryAllocation ? BK_ERR_OOM : BK_ERR_CUDA, buf);
+}
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes attr;
+    cudaError_t e = cudaPointerGetAttributes(&attr, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
+}
+
+void* ws_get(bk_ctx* ctx, int slot, size_t bytes) {
+    if ((int)ctx->ws.size() <= slot) ctx->ws.resize(slot + 1);
+    bk_buf& b = ctx->ws[slot];
+    if (b.bytes >= bytes && b.p) return b.p;
+    if (b.p) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    size_t want = std::max<size_t>(bytes + 256, 4096);
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        b.p = nullptr;
+        throw bk_error(BK_ERR_OOM, "workspace allocation of " + std::to_string(want) + " bytes failed");
+    }
+    b.bytes = want;
+    return b.p;
+}
+
+static void* grow(bk_buf& b, size_t bytes, cudaStream_t st) {
+    if (b.bytes >= bytes && b.p) return b.p;
+    if (b.p) {
+        cudaStreamSynchronize(st);
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    size_t want = std::max<size_t>(bytes + 256, 4096);
+    if (cudaMalloc(&b.p, want) != cudaSuccess) {
+        cudaGetLastError();
+        throw bk_error(BK_ERR_OOM, "buffer allocation failed");
+    }
+    b.bytes = want;
+    return b.p;
+}
+
+}  // namespace bk
+
+#define BK_TRY try {
+#define BK_CATCH(ctx)                                              \
+    }                                                              \
+    catch (const bk_error& e) { return set_error(ctx, e.code, e.msg); } \
+    catch (const std::exception& e) { return set_error(ctx, BK_ERR_CUDA, e.what()); }
+
+#define ARG_CHECK(ctx, cond, msg) \
+    do { if (!(cond)) return set_error(ctx, BK_ERR_ARG, msg); } while (0)
+
+#define CUDA_OK(ctx, call) \
+    do { int _r = cuda_check(ctx, (call), #call); if (_r) return _r; } while (0)
+
+static int enter(bk_ctx* ctx) {
+    if (!ctx) return BK_ERR_ARG;
+    if (ctx->sticky) return ctx->sticky;
+    cudaError_t e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_check(ctx, e, "cudaSetDevice");
+    ctx->last_error.clear();
+    return BK_OK;
+}
+
+// After a batch of launches: surface launch errors.
+static int post_launch(bk_ctx* ctx, const char* where) {
+    cudaError_t e = cudaGetLastError();
+    return cuda_check(ctx, e, where);
+}
+
+// Stage an N x k (ld) host multivector to device (ld preserved) or return the device pointer.
+static const double* stage_in(bk_ctx* ctx, int slot, const double* p, int64_t n, int64_t ld,
+                              bool* is_host) {
+    *is_host = !is_device_ptr(p);
+    if (!*is_host) return p;
+    size_t bytes = (size_t)n * ld * sizeof(double);
+    double* d = (double*)ws_get(ctx, slot, bytes);
+    if (bytes) {
+        cudaError_t e = cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, ctx->stream);
+        if (e != cudaSuccess) throw bk_error(BK_ERR_CUDA, std::string("H2D copy: ") + cudaGetErrorString(e));
+    }
+    return d;
+}
+
+// ------------------------------------------------------------------ context
+extern "C" int bk_version(void) { return 100; }
+
+extern "C" const char* bk_status_string(int s) {
+    switch (s) {
+        case BK_OK: return "ok";
+        case BK_ERR_ARG: return "invalid argument";
+        case BK_NOT_CONVERGED: return "not converged";
+        case BK_BREAKDOWN: return "breakdown";
+        case BK_ERR_CUDA: return "CUDA error";
+        case BK_ERR_NCCL: return "NCCL error";
+        case BK_ERR_OOM: return "out of memory";
+        case BK_ERR_UNSUPPORTED: return "unsupported";
+        default: return "unknown status";
+    }
+}
+
+extern "C" const char* bk_last_error(const bk_ctx* ctx) { return ctx ? ctx->last_error.c_str() : ""; }
+
+extern "C" int bk_ctx_create(bk_ctx** out, int device, void* cuda_stream) {
+    if (!out) return BK_ERR_ARG;
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return BK_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) return BK_ERR_ARG;
+    if (cudaSetDevice(device) != cudaSuccess) return BK_ERR_CUDA;
+    bk_ctx* c = new bk_ctx();
+    c->device = device;
+    c->stream = (cudaStream_t)cuda_stream;   // NULL = the legacy default stream
+    c->own_stream = false;
+    cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking);
+    cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    c->h_pinned_bytes = 1 << 20;
+    if (cudaMallocHost(&c->h_pinned, c->h_pinned_bytes) != cudaSuccess) {
+        cudaGetLastError();
+        c->h_pinned = nullptr;
+        c->h_pinned_bytes = 0;
+    }
+    *out = c;
+    return BK_OK;
+}
+
+extern "C" int bk_ctx_set_stream(bk_ctx* ctx, void* cuda_stream) {
+    int r = enter(ctx);
+    if (r) return r;
+    if (ctx->own_stream) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaStreamDestroy(ctx->stream);
+        ctx->own_stream = false;
+    }
+    ctx->stream = (cudaStream_t)cuda_stream;
+    return BK_OK;
+}
+
+extern "C" int bk_ctx_synchronize(bk_ctx* ctx) {
+    int r = enter(ctx);
+    if (r) return r;
+    CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+}
+
+extern "C" int bk_ctx_destroy(bk_ctx* ctx) {
+    if (!ctx) return BK_OK;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& b : ctx->ws)
+        if (b.p) cudaFree(b.p);
+    if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+#ifndef BK_NO_NCCL
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+#endif
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+    if (ctx->ev_a) cudaEventDestroy(ctx->ev_a);
+    if (ctx->ev_b) cudaEventDestroy(ctx->ev_b);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+    cudaGetLastError();
+    return BK_OK;
+}
+
+extern "C" int bk_ctx_comm_info(const bk_ctx* ctx, int* nranks, int* rank) {
+    if (!ctx) return BK_ERR_ARG;
+    if (nranks) *nranks = ctx->nranks;
+    if (rank) *rank = ctx->rank;
+    return BK_OK;
+}
+
+// ------------------------------------------------------------------ halo plan (host only)
+extern "C" int bk_plan_halo(int nranks, int rank, const int64_t* rank_begin, int64_t n_local,
+                            const int32_t* row_ptr, const int32_t* col_global, int64_t nnz,
+                            int64_t* n_ghost, int64_t* ghost_ids, int32_t* ghost_owner, int32_t* col_local,
+                            uint8_t* is_boundary) {
+    if (nranks < 1 || rank < 0 || rank >= nranks || !rank_begin || !row_ptr || !n_ghost) return BK_ERR_ARG;
+    if (nnz > 0 && (!col_global || !col_local)) return BK_ERR_ARG;
+    for (int r = 0; r < nranks; ++r)
+        if (rank_begin[r + 1] < rank_begin[r]) return BK_ERR_ARG;
+    const int64_t b0 = rank_begin[rank], b1 = rank_begin[rank + 1];
+    if (b1 - b0 != n_local) return BK_ERR_ARG;
+    if (row_ptr[0] != 0 || row_ptr[n_local] != nnz) return BK_ERR_ARG;
+    const int64_t n_global = rank_begin[nranks];
+    std::vector<int64_t> ghosts;
+    for (int64_t p = 0; p < nnz; ++p) {
+        const int64_t c = col_global[p];
+        if (c < 0 || c >= n_global) return BK_ERR_ARG;
+        if (c < b0 || c >= b1) ghosts.push_back(c);
+    }
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    *n_ghost = (int64_t)ghosts.size();
+    for (size_t g = 0; g < ghosts.size(); ++g) {
+        if (ghost_ids) ghost_ids[g] = ghosts[g];
+        if (ghost_owner) {
+            // owner: last r with rank_begin[r] <= id (skip empty ranks)
+            int r = (int)(std::upper_bound(rank_begin, rank_begin + nranks + 1, ghosts[g]) - rank_begin) - 1;
+            while (r > 0 && rank_begin[r] == rank_begin[r + 1]) --r;
+            ghost_owner[g] = r;
+        }
+    }
+    for (int64_t i = 0; i < n_local; ++i) {
+        if (row_ptr[i + 1] < row_ptr[i]) return BK_ERR_ARG;
+        uint8_t bnd = 0;
+        for (int32_t p = row_ptr[i]; p < row_ptr[i + 1]; ++p) {
+            const int64_t c = col_global[p];
+            if (c >= b0 && c < b1) {
+                col_local[p] = (int32_t)(c - b0);
+            } else {
+                const int64_t g = std::lower_bound(ghosts.begin(), ghosts.end(), c) - ghosts.begin();
+                col_local[p] = (int32_t)(n_local + g);
+                bnd = 1;
+            }
+        }
+        if (is_boundary) is_boundary[i] = bnd;
+    }
+    return BK_OK;
+}
+
+// ------------------------------------------------------------------ matrix
+
+extern "C" int bk_csr_create(bk_ctx* ctx, bk_csr** out, int64_t n_global, int64_t row_begin, int64_t n_local,
+                             const int32_t* row_ptr, const int32_t* col_global, const double* val, int64_t nnz) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, out != nullptr, "bk_csr_create: out is NULL");
+    ARG_CHECK(ctx, n_global >= 0 && n_local >= 0 && row_begin >= 0 && row_begin + n_local <= n_global,
+              "bk_csr_create: bad row range");
+    ARG_CHECK(ctx, n_global < ((int64_t)1 << 31), "bk_csr_create: n_global must be < 2^31 (int32 columns)");
+    ARG_CHECK(ctx, nnz >= 0 && nnz < ((int64_t)1 << 31) - 16, "bk_csr_create: nnz must be < 2^31");
+    ARG_CHECK(ctx, row_ptr != nullptr, "bk_csr_create: row_ptr is NULL");
+    ARG_CHECK(ctx, nnz == 0 || (col_global && val), "bk_csr_create: col/val NULL");
+    if (ctx->nranks == 1)
+        ARG_CHECK(ctx, row_begin == 0 && n_local == n_global,
+                  "bk_csr_create: a single-rank ctx needs the whole matrix (row_begin 0, n_local == n_global)");
+    *out = nullptr;
+    BK_TRY
+    cudaStream_t st = ctx->stream;
+    // host copies of the index structure (validation + halo plan are host work at setup)
+    std::vector<int32_t> rp(n_local + 1), colg(nnz);
+    const bool rp_dev = is_device_ptr(row_ptr), col_dev = is_device_ptr(col_global);
+    CUDA_OK(ctx, cudaMemcpy(rp.data(), row_ptr, sizeof(int32_t) * (n_local + 1),
+                            rp_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    if (nnz)
+        CUDA_OK(ctx, cudaMemcpy(colg.data(), col_global, sizeof(int32_t) * nnz,
+                                col_dev ? cudaMemcpyDeviceToHost : cudaMemcpyHostToHost));
+    ARG_CHECK(ctx, rp[0] == 0 && rp[n_local] == nnz, "bk_csr_create: row_ptr[0] must be 0 and row_ptr[n] == nnz");
+    for (int64_t i = 0; i < n_local; ++i) {
+        ARG_CHECK(ctx, rp[i + 1] >= rp[i], "bk_csr_create: row_ptr must be non-decreasing");
+        for (int32_t p = rp[i]; p < rp[i + 1]; ++p) {
+            ARG_CHECK(ctx, colg[p] >= 0 && colg[p] < n_global, "bk_csr_create: column id out of range");
+            ARG_CHECK(ctx, p == rp[i] || colg[p] > colg[p - 1],
+                      "bk_csr_create: columns must be strictly increasing within a row");
+        }
+    }
+    bk_csr* A = new bk_csr();
+    A->ctx = ctx;
+    A->n_global = n_global;
+    A->row_begin = row_begin;
+    A->n_local = n_local;
+    A->nnz = nnz;
+    // device arrays, 256-byte aligned (cudaMalloc) and padded by 8 elements so
+    // the 16-byte vector loads of the apply kernel never leave the allocation
+    const size_t pad = 8;
+    if (cudaMalloc(&A->d_rp, sizeof(int32_t) * (n_local + 1 + pad)) != cudaSuccess ||
+        cudaMalloc(&A->d_col, sizeof(int32_t) * (nnz + pad)) != cudaSuccess ||
+        cudaMalloc(&A->d_val, sizeof(double) * (nnz + pad)) != cudaSuccess ||
+        cudaMalloc(&A->d_dinv, sizeof(double) * (n_local + pad)) != cudaSuccess) {
+        cudaGetLastError();
+        bk_csr_destroy(A);
+        return set_error(ctx, BK_ERR_OOM, "bk_csr_create: device allocation failed");
+    }
+    cudaMemsetAsync(A->d_col, 0, sizeof(int32_t) * (nnz + pad), st);
+    cudaMemsetAsync(A->d_val, 0, sizeof(double) * (nnz + pad), st);
+    std::vector<int32_t> col_local(colg);
+    if (ctx->nranks > 1) {
+        int rr = csr_setup_comm(ctx, A, rp, col_local, colg);
+        if (rr) { bk_csr_destroy(A); return rr; }
+    } else {
+        A->n_interior = n_local;
+        A->interior_contig = 1;
+        A->interior_begin = 0;
+    }
+    cudaMemcpyAsync(A->d_rp, rp.data(), sizeof(int32_t) * (n_local + 1), cudaMemcpyHostToDevice, st);
+    if (nnz) {
+        cudaMemcpyAsync(A->d_col, col_local.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(A->d_val, val, sizeof(double) * nnz, cudaMemcpyDefault, st);
+    }
+    // Jacobi diagonal (local numbering: diagonal column of row i is i)
+    launch_extract_diag_inv(n_local, 0, A->d_rp, A->d_col, A->d_val, A->d_dinv, st);
+    int rr = post_launch(ctx, "bk_csr_create");
+    if (!rr) rr = cuda_check(ctx, cudaStreamSynchronize(st), "bk_csr_create sync");
+    if (rr) { bk_csr_destroy(A); return rr; }
+    *out = A;
+    return BK_OK;
+    BK_CATCH(ctx)
+}
+
+extern "C" int bk_csr_destroy(bk_csr* A) {
+    if (!A) return BK_OK;
+    if (A->ctx) {
+        cudaSetDevice(A->ctx->device);
+        cudaStreamSynchronize(A->ctx->stream);
+    }
+    cudaFree(A->d_rp);
+    cudaFree(A->d_col);
+    cudaFree(A->d_val);
+    cudaFree(A->d_dinv);
+    cudaFree(A->d_boundary_rows);
+    cudaFree(A->d_interior_rows);
+    for (auto& nb : A->nbs) cudaFree(nb.d_send_rows);
+    if (A->ghost.p) cudaFree(A->ghost.p);
+    if (A->sendbuf.p) cudaFree(A->sendbuf.p);
+    delete A;
+    cudaGetLastError();
+    return BK_OK;
+}
+
+extern "C" int bk_csr_get_info(const bk_csr* A, bk_csr_info* info) {
+    if (!A || !info) return BK_ERR_ARG;
+    info->n_global = A->n_global;
+    info->row_begin = A->row_begin;
+    info->n_local = A->n_local;
+    info->nnz = A->nnz;
+    info->n_ghost = A->n_ghost;
+    info->n_boundary_rows = A->n_boundary;
+    info->n_send_rows = A->n_send_total;
+    info->n_neighbors = (int)A->nbs.size();
+    info->interior_contiguous = A->interior_contig;
+    return BK_OK;
+}
+
+// ------------------------------------------------------------------ a1 apply
+namespace bk {
+int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, const double* C, int kout,
+             double alpha, double beta, double* Y, int64_t ldy) {
+    SpmmArgs a{};
+    a.rp = A->d_rp;
+    a.col = A->d_col;
+    a.val = A->d_val;
+    a.X = X;
+    a.ldx = ldx;
+    a.C = C;
+    a.k = k;
+    a.kout = kout;
+    a.alpha = alpha;
+    a.beta = beta;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.ncol_local = (int32_t)A->n_local;
+    if (ctx->nranks == 1 || A->n_ghost == 0) {
+        a.row0 = 0;
+        a.nrows = A->n_local;
+        launch_bspmm(a, ctx->stream);
+        return post_launch(ctx, "bspmm_apply");
+    }
+    // p > 1: halo exchange on the comm stream overlapped with the interior rows
+    int r = halo_exchange(ctx, A, k, X, ldx);   // records ctx->ev_b when the ghosts have landed
+    if (r) return r;
+    if (A->interior_contig) {
+        a.row0 = A->interior_begin;
+        a.nrows = A->n_interior;
+        a.rows = nullptr;
+    } else {
+        a.rows = A->d_interior_rows;
+        a.nrows = A->n_interior;
+    }
+    launch_bspmm(a, ctx->stream);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
+    a.rows = A->d_boundary_rows;
+    a.nrows = A->n_boundary;
+    a.Xg = (const double*)A->ghost.p;
+    a.ldg = k;
+    launch_bspmm(a, ctx->stream);
+    return post_launch(ctx, "bspmm_apply");
+}
+}  // namespace bk
+
+extern "C" int bspmm_apply(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, const double* C,
+                           int k_out, double alpha, double beta, double* Y, int64_t ldy) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, A != nullptr && A->ctx == ctx, "bspmm_apply: matrix is NULL or from another ctx");
+    ARG_CHECK(ctx, k >= 1 && k <= BK_MAX_K, "bspmm_apply: need 1 <= k <= 32");
+    ARG_CHECK(ctx, k_out >= 1 && k_out <= BK_MAX_K, "bspmm_apply: need 1 <= k_out <= 32");
+    ARG_CHECK(ctx, C != nullptr || k_out == k, "bspmm_apply: C == NULL requires k_out == k");
+    ARG_CHECK(ctx, ldx >= k && ldy >= k_out, "bspmm_apply: leading dimension too small");
+    ARG_CHECK(ctx, A->n_local == 0 || (X != nullptr && Y != nullptr), "bspmm_apply: X or Y is NULL");
+    ARG_CHECK(ctx, (const void*)X != (const void*)Y, "bspmm_apply: Y must not alias X");
+    if (A->n_local == 0) return BK_OK;
+    BK_TRY
+    bool xh, ch = false;
+    const double* dX = stage_in(ctx, WS_STAGE_X, X, A->n_local, ldx, &xh);
+    const double* dC = nullptr;
+    if (C) dC = stage_in(ctx, WS_STAGE_C, C, k, k_out, &ch);
+    const bool yh = !is_device_ptr(Y);
+    double* dY = Y;
+    if (yh) {
+        dY = (double*)ws_get(ctx, WS_STAGE_Y, (size_t)A->n_local * ldy * sizeof(double));
+        if (beta != 0.0)
+            CUDA_OK(ctx, cudaMemcpyAsync(dY, Y, (size_t)A->n_local * ldy * sizeof(double), cudaMemcpyHostToDevice,
+                                         ctx->stream));
+    }
+    r = spmm_dev(ctx, A, k, dX, ldx, dC, k_out, alpha, beta, dY, ldy);
+    if (r) return r;
+    if (yh) {
+        CUDA_OK(ctx, cudaMemcpyAsync(Y, dY, (size_t)A->n_local * ldy * sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    }
+    if (xh || ch || yh) CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+    BK_CATCH(ctx)
+}
+
+// ------------------------------------------------------------------ a3 gram
+namespace bk {
+int gram_dev(bk_ctx* ctx, int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+             double* G, bool allreduce) {
+    if (n > 0) {
+        double* part = (double*)ws_get(ctx, WS_GRAM_PART, gram_ws_doubles(n, ka, kb, ctx->num_sms) * sizeof(double));
+        launch_gram(n, ka, kb, X, ldx, Y, ldy, G, part, ctx->num_sms, ctx->stream);
+    } else {
+        cudaMemsetAsync(G, 0, sizeof(double) * ka * kb, ctx->stream);
+    }
+    int r = post_launch(ctx, "block_gram");
+    if (r) return r;
+    if (allreduce && ctx->nranks > 1) return allreduce_sum(ctx, G, (int64_t)ka * kb);
+    return BK_OK;
+}
+}  // namespace bk
+
+extern "C" int block_gram(bk_ctx* ctx, int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y,
+                          int64_t ldy, double* G, int flags) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, n >= 0, "block_gram: n < 0");
+    ARG_CHECK(ctx, ka >= 1 && ka <= BK_MAX_KA, "block_gram: need 1 <= ka <= 4096");
+    ARG_CHECK(ctx, kb >= 1 && kb <= BK_MAX_K, "block_gram: need 1 <= kb <= 32");
+    ARG_CHECK(ctx, ldx >= ka && ldy >= kb, "block_gram: leading dimension too small");
+    ARG_CHECK(ctx, G != nullptr && (n == 0 || (X && Y)), "block_gram: NULL pointer");
+    BK_TRY
+    bool xh, yh;
+    const double* dX = stage_in(ctx, WS_STAGE_X, X, n, ldx, &xh);
+    const double* dY = (Y == X && ldy == ldx) ? dX : stage_in(ctx, WS_STAGE_Y, Y, n, ldy, &yh);
+    const bool gh = !is_device_ptr(G);
+    double* dG = gh ? (double*)ws_get(ctx, WS_STAGE_G, sizeof(double) * ka * kb) : G;
+    r = gram_dev(ctx, n, ka, kb, dX, ldx, dY, ldy, dG, (flags & BK_GRAM_ALLREDUCE) != 0);
+    if (r) return r;
+    if (gh) {
+        CUDA_OK(ctx, cudaMemcpyAsync(G, dG, sizeof(double) * ka * kb, cudaMemcpyDeviceToHost, ctx->stream));
+        CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    } else if (xh || (dY != Y)) {
+        CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    }
+    return BK_OK;
+    BK_CATCH(ctx)
+}
+
+// ------------------------------------------------------------------ a5 update
+extern "C" int block_update(bk_ctx* ctx, int64_t n, int kp, int k, double a, double* X, int64_t ldx, double s,
+                            const double* P, int64_t ldp, const double* C) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, n >= 0, "block_update: n < 0");
+    ARG_CHECK(ctx, k >= 1 && k <= BK_MAX_K, "block_update: need 1 <= k <= 32");
+    ARG_CHECK(ctx, kp >= 1 && kp <= BK_MAX_KA, "block_update: need 1 <= kp <= 4096");
+    ARG_CHECK(ctx, ldx >= k && ldp >= kp, "block_update: leading dimension too small");
+    ARG_CHECK(ctx, n == 0 || (X && P && C), "block_update: NULL pointer");
+    const bool alias = (const void*)P == (const void*)X;
+    ARG_CHECK(ctx, !alias || (ldp == ldx && kp == k), "block_update: P may alias X only with kp == k, ldp == ldx");
+    if (n == 0) return BK_OK;
+    BK_TRY
+    bool xh = !is_device_ptr(X), ph = false, ch = false;
+    double* dX = X;
+    if (xh) {
+        dX = (double*)ws_get(ctx, WS_STAGE_Y, (size_t)n * ldx * sizeof(double));
+        CUDA_OK(ctx, cudaMemcpyAsync(dX, X, (size_t)n * ldx * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    const double* dP = alias ? dX : stage_in(ctx, WS_STAGE_X, P, n, ldp, &ph);
+    const double* dC = stage_in(ctx, WS_STAGE_C, C, kp, k, &ch);
+    UpdArgs u{};
+    u.n = n; u.kp = kp; u.k = k;
+    u.a = a; u.Xin = dX; u.ldxin = ldx;
+    u.s = s; u.P = dP; u.ldp = ldp; u.C = dC;
+    u.out = dX; u.ldo = ldx;
+    launch_update(u, ctx->stream);
+    r = post_launch(ctx, "block_update");
+    if (r) return r;
+    if (xh) CUDA_OK(ctx, cudaMemcpyAsync(X, dX, (size_t)n * ldx * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    if (xh || ph || ch) CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+    BK_CATCH(ctx)
+}
+
+// ------------------------------------------------------------------ a6 solve
+extern "C" void bk_solve_opts_default(bk_solve_opts* o) {
+    if (!o) return;
+    memset(o, 0, sizeof *o);
+    o->method = BK_CG;
+    o->max_iters = 1000;
+    o->restart = 30;
+    o->precond = BK_PRECOND_NONE;
+    o->conv_mode = BK_CONV_ALL;
+    o->x0_is_zero = 0;
+    o->check_every = 1;
+    o->use_graphs = 0;
+    o->rtol = 1e-10;
+    o->breakdown_tol = 1e-13;
+}
+
+extern "C" int block_krylov_solve(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb, double* X,
+                                  int64_t ldx, const bk_solve_opts* o, bk_solve_report* rep) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, A && A->ctx == ctx, "block_krylov_solve: matrix is NULL or from another ctx");
+    ARG_CHECK(ctx, o && rep, "block_krylov_solve: opts/report NULL");
+    ARG_CHECK(ctx, k >= 1 && k <= BK_MAX_K, "block_krylov_solve: need 1 <= k <= 32");
+    ARG_CHECK(ctx, ldb >= k && ldx >= k, "block_krylov_solve: leading dimension too small");
+    ARG_CHECK(ctx, A->n_local == 0 || (B && X), "block_krylov_solve: NULL pointer");
+    ARG_CHECK(ctx, (const void*)B != (const void*)X, "block_krylov_solve: X must not alias B");
+    ARG_CHECK(ctx, o->method >= BK_CG && o->method <= BK_BICGSTAB, "block_krylov_solve: unknown method");
+    ARG_CHECK(ctx, o->max_iters >= 0 && o->check_every >= 1, "block_krylov_solve: bad max_iters/check_every");
+    ARG_CHECK(ctx, o->method != BK_GMRES || (o->restart >= 1 && (int64_t)(o->restart + 1) * k <= BK_MAX_KA),
+              "block_krylov_solve: GMRES needs restart >= 1 and (restart+1)*k <= 4096");
+    ARG_CHECK(ctx, o->rtol >= 0.0 && o->breakdown_tol >= 0.0, "block_krylov_solve: negative tolerance");
+    ARG_CHECK(ctx, o->precond == BK_PRECOND_NONE || (o->precond == BK_PRECOND_JACOBI && o->method == BK_CG),
+              "block_krylov_solve: JACOBI preconditioning is implemented for CG only");
+    BK_TRY
+    bool bh;
+    const double* dB = stage_in(ctx, WS_STAGE_X, B, A->n_local, ldb, &bh);
+    const bool xh = !is_device_ptr(X);
+    double* dX = X;
+    if (xh) {
+        dX = (double*)ws_get(ctx, WS_STAGE_Y, (size_t)A->n_local * ldx * sizeof(double));
+        if (!o->x0_is_zero)
+            CUDA_OK(ctx, cudaMemcpyAsync(dX, X, (size_t)A->n_local * ldx * sizeof(double), cudaMemcpyHostToDevice,
+                                         ctx->stream));
+    }
+    r = solve_impl(ctx, A, k, dB, ldb, dX, ldx, o, rep);
+    if (r == BK_ERR_CUDA || r == BK_ERR_NCCL || r == BK_ERR_OOM || r == BK_ERR_ARG) return r;
+    if (xh) {
+        CUDA_OK(ctx, cudaMemcpyAsync(X, dX, (size_t)A->n_local * ldx * sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    }
+    CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    return r;
+    BK_CATCH(ctx)
+}

@@ -1,0 +1,204 @@
+// bk_internal.h -- private declarations of the B200 (sm_100a) block-Krylov library.
+// Nothing here is shared with oracle/ (the CPU checker); see DESIGN.md §1.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "bk.h"
+
+#ifndef BK_NO_NCCL
+#include <nccl.h>
+#endif
+
+namespace bk {
+
+// ------------------------------------------------------------------ device status
+// Written by the small-dense / convergence kernels, polled by the host driver.
+// `halt` makes every later update kernel of the solve a no-op, so X keeps the
+// last good iterate whatever the host polling period is.
+struct DevStatus {
+    int halt;            // 1 after convergence or breakdown
+    int converged;
+    int breakdown_col;   // -1 if none
+    int iter;            // completed (un-halted) iterations
+    int gm_steps;        // GMRES: completed inner steps in the current cycle
+    int pad[3];
+    double relres[BK_MAX_K];
+    double r0[BK_MAX_K];
+    double omega;        // BiCGStab scalar
+    double neg_omega;
+};
+
+// ------------------------------------------------------------------ kernel args
+struct SpmmArgs {
+    const int32_t* rp;      // row pointers (local rows)
+    const int32_t* col;     // local column ids (ghost ids >= ncol_local)
+    const double* val;
+    const int32_t* rows;    // optional explicit row list (boundary rows); null = contiguous
+    int64_t row0;           // first row (contiguous mode)
+    int64_t nrows;
+    const double* X;
+    int64_t ldx;
+    const double* Xg;       // ghost rows (ld = ldg), column c >= ncol_local -> Xg[c - ncol_local]
+    int64_t ldg;
+    int32_t ncol_local;
+    const double* C;        // k x kout row-major, or null (identity)
+    int k, kout;
+    double alpha, beta;
+    double* Y;
+    int64_t ldy;
+};
+
+// out = a*Xin + s*(P C) + (w_host * (*w_dev)) * W     (any term may be absent)
+struct UpdArgs {
+    int64_t n;
+    int kp, k;
+    double a;
+    const double* Xin; int64_t ldxin;
+    double s;
+    const double* P; int64_t ldp;
+    const double* C;        // kp x k row-major (device)
+    double w_host;
+    const double* w_dev;    // optional device scalar multiplying w_host
+    const double* W; int64_t ldw;
+    double* out; int64_t ldo;
+    const int* halt;        // optional: skip when *halt != 0
+};
+
+void launch_bspmm(const SpmmArgs& a, cudaStream_t st);
+void launch_update(const UpdArgs& a, cudaStream_t st);
+// G (ka x kb, row-major, device) = X^T Y; `partials` workspace of gram_ws_doubles().
+size_t gram_ws_doubles(int64_t n, int ka, int kb, int num_sms);
+void launch_gram(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y,
+                 int64_t ldy, double* G, double* partials, int num_sms, cudaStream_t st);
+// d[c] = sum_i X[i,c] Y[i,c] for c < k (and optionally d2 with Y2); deterministic.
+size_t coldot_ws_doubles(int64_t n, int k, int num_sms);
+void launch_coldot(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                   const double* Y2, int64_t ldy2, double* d, double* d2, double* partials,
+                   int num_sms, cudaStream_t st);
+void launch_row_scale(int64_t n, int k, const double* dinv, const double* X, int64_t ldx,
+                      double* out, int64_t ldo, cudaStream_t st);
+void launch_extract_diag_inv(int64_t n, int64_t row_offset, const int32_t* rp, const int32_t* col,
+                             const double* val, double* dinv, cudaStream_t st);
+void launch_fill(double* p, int64_t n, double v, cudaStream_t st);
+void launch_pack_rows(int64_t nrows, int k, const int32_t* rows, const double* X, int64_t ldx,
+                      double* out, cudaStream_t st);
+
+// ------------------------------------------------------------------ small dense (1 CTA)
+// Out(k x nrhs) = G^{-1} Rhs by Cholesky; breakdown -> st->breakdown_col, st->halt.
+void sd_chol_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double tol,
+                   DevStatus* st, cudaStream_t s);
+// Out = G^{-1} (sign * Rhs) by LU with partial pivoting.
+void sd_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign,
+                 double tol, DevStatus* st, cudaStream_t s);
+// R upper (G = R^T R) and Rinv; also Racc <- R * Racc_in if Racc_in != null (Racc = R2 R1).
+void sd_chol_qr(const double* G, double* R, double* Rinv, const double* Rprev, double* Rprod,
+                int k, double tol, DevStatus* st, cudaStream_t s);
+// Convergence test: rel_c = sqrt(max(g_c,0)) / r0_c; sets converged/halt, iter++.
+// init != 0: store r0_c = sqrt(g_c) instead.
+void sd_conv_check(const double* g, int gstride, int k, double rtol, int conv_mode, int init,
+                   DevStatus* st, cudaStream_t s);
+// BiCGStab omega = sum(ts) / sum(tt) into st->omega (breakdown if tt == 0).
+void sd_omega(const double* ts, const double* tt, int k, DevStatus* st, cudaStream_t s);
+// Copy a k x k matrix (device) (used to roll RZ <- RZn).
+void sd_copy(const double* src, double* dst, int n, cudaStream_t s);
+// GMRES: apply stored rotations Q_0..Q_{j-1} to the new block column, QR the
+// 2k x k bottom block into Q_j, rotate g, write residual norms and test.
+void sd_gmres_step(double* Hcol, int j, int k, double* Qs, double* Rtri, int ldr, double* g,
+                   double rtol, int conv_mode, DevStatus* st, cudaStream_t s);
+// GMRES: solve Rtri[0:nk,0:nk] y = g[0:nk] (upper triangular), y: nk x k.
+void sd_gmres_backsolve(const double* Rtri, int ldr, const double* g, double* y, int nk, int k,
+                        cudaStream_t s);
+// H column assembly: Hc = H1 + H2 (n doubles)
+void sd_add(const double* a, const double* b, double* out, int n, cudaStream_t s);
+
+}  // namespace bk
+
+// ------------------------------------------------------------------ context / matrix
+struct bk_buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+struct bk_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    int num_sms = 148;
+    int sticky = 0;
+    std::string last_error;
+    std::vector<bk_buf> ws;       // slot-indexed grow-only device workspaces
+    double* h_pinned = nullptr;   // pinned host staging for small results
+    size_t h_pinned_bytes = 0;
+    int nranks = 1, rank = 0;
+#ifndef BK_NO_NCCL
+    ncclComm_t comm = nullptr;
+#endif
+};
+
+struct bk_neighbor {
+    int rank = -1;
+    int64_t recv_off = 0, recv_cnt = 0;   // rows into the ghost buffer
+    int64_t send_cnt = 0;
+    int32_t* d_send_rows = nullptr;       // local row ids to send
+    int send_contig = 0;
+    int64_t send_begin = 0;
+    int64_t send_off = 0;                 // offset (rows) in the packed send buffer
+};
+
+struct bk_csr {
+    bk_ctx* ctx = nullptr;
+    int64_t n_global = 0, row_begin = 0, n_local = 0, nnz = 0;
+    int32_t* d_rp = nullptr;
+    int32_t* d_col = nullptr;             // local numbering
+    double* d_val = nullptr;
+    double* d_dinv = nullptr;             // Jacobi
+    int64_t n_ghost = 0;
+    int32_t* d_boundary_rows = nullptr;
+    int64_t n_boundary = 0;
+    int32_t* d_interior_rows = nullptr;
+    int64_t n_interior = 0;
+    int interior_contig = 1;
+    int64_t interior_begin = 0;
+    std::vector<bk_neighbor> nbs;
+    int64_t n_send_total = 0;
+    bk_buf ghost, sendbuf;
+};
+
+// workspace slots used by the ABI and the solvers
+enum bk_ws_slot {
+    WS_STAGE_X = 0, WS_STAGE_Y, WS_STAGE_C, WS_STAGE_G, WS_GRAM_PART, WS_COLDOT_PART,
+    WS_SOLVE_BASE  // solvers use WS_SOLVE_BASE + i
+};
+
+namespace bk {
+void* ws_get(bk_ctx* ctx, int slot, size_t bytes);  // throws on OOM
+int set_error(bk_ctx* ctx, int code, const std::string& msg);
+int cuda_check(bk_ctx* ctx, cudaError_t e, const char* where);
+bool is_device_ptr(const void* p);
+int halo_exchange(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx);
+int allreduce_sum(bk_ctx* ctx, double* d, int64_t n);
+// collective (nranks > 1): halo plan, renumbering, neighbour lists (comm.cpp)
+int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::vector<int32_t>& col_local,
+                   const std::vector<int32_t>& colg);
+int solve_impl(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb, double* X,
+               int64_t ldx, const bk_solve_opts* o, bk_solve_report* rep);
+// device-pointer variants used by the solvers (no host staging, no validation)
+int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, const double* C,
+             int kout, double alpha, double beta, double* Y, int64_t ldy);
+int gram_dev(bk_ctx* ctx, int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y,
+             int64_t ldy, double* G, bool allreduce);
+}  // namespace bk
+
+struct bk_error : std::exception {
+    int code;
+    std::string msg;
+    bk_error(int c, std::string m) : code(c), msg(std::move(m)) {}
+    const char* what() const noexcept override { return msg.c_str(); }
+};

@@ -1,0 +1,351 @@
+// solve.cpp -- a6: block Krylov drivers (block CG, block GMRES(m), block BiCGStab).
+//
+// Host code that only ENQUEUES kernels on the ctx stream: the N x k work is
+// bspmm / gram / update (spmm.cu, blas.cu), the k x k work runs in one-CTA
+// kernels (dense.cu), and the convergence/breakdown state lives in a device
+// DevStatus that the host polls every `check_every` iterations.  Kernels after
+// a halt (convergence or breakdown) are no-ops, so X always holds the last
+// valid iterate.  The algorithms follow DESIGN.md §3 readings O4-O6 step by
+// step (the same steps as oracle/, written independently).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "bk_internal.h"
+
+namespace bk {
+namespace {
+
+struct Solver {
+    bk_ctx* ctx;
+    const bk_csr* A;
+    int64_t n;
+    int k;
+    const bk_solve_opts* o;
+    bk_solve_report* rep;
+    cudaStream_t st;
+    DevStatus* ds = nullptr;
+    DevStatus* hs = nullptr;   // pinned readback
+    int slot = WS_SOLVE_BASE;
+    bool allred;
+
+    double* vec(int ld_cols = 0) {
+        const int cols = ld_cols ? ld_cols : k;
+        return (double*)ws_get(ctx, slot++, (size_t)std::max<int64_t>(n, 1) * cols * sizeof(double));
+    }
+    double* small(size_t doubles) { return (double*)ws_get(ctx, slot++, doubles * sizeof(double)); }
+
+    int init_status() {
+        ds = (DevStatus*)ws_get(ctx, slot++, sizeof(DevStatus));
+        DevStatus h;
+        memset(&h, 0, sizeof h);
+        h.breakdown_col = -1;
+        DevStatus* pin = (DevStatus*)ctx->h_pinned;
+        hs = (DevStatus*)((char*)ctx->h_pinned + 4096);
+        if (!pin) return set_error(ctx, BK_ERR_OOM, "no pinned staging");
+        *pin = h;
+        return cuda_check(ctx, cudaMemcpyAsync(ds, pin, sizeof h, cudaMemcpyHostToDevice, st), "status init");
+    }
+    int poll() {
+        int r = cuda_check(ctx, cudaMemcpyAsync(hs, ds, sizeof(DevStatus), cudaMemcpyDeviceToHost, st), "status poll");
+        if (r) return r;
+        return cuda_check(ctx, cudaStreamSynchronize(st), "status sync");
+    }
+    int launched(const char* w) { return cuda_check(ctx, cudaGetLastError(), w); }
+
+    int spmm(const double* X, int64_t ldx, double* Y, int64_t ldy, double alpha = 1.0, double beta = 0.0) {
+        rep->n_spmm++;
+        return spmm_dev(ctx, A, k, X, ldx, nullptr, k, alpha, beta, Y, ldy);
+    }
+    int gram(const double* X, int64_t ldx, int ka, const double* Y, int64_t ldy, double* G) {
+        rep->n_gram++;
+        if (allred) rep->n_allreduce++;
+        return gram_dev(ctx, n, ka, k, X, ldx, Y, ldy, G, allred);
+    }
+    int coldot(const double* X, int64_t ldx, const double* Y, int64_t ldy, const double* Y2, int64_t ldy2,
+               double* d, double* d2) {
+        rep->n_gram++;
+        double* part = (double*)ws_get(ctx, WS_COLDOT_PART, coldot_ws_doubles(n, k, ctx->num_sms) * sizeof(double));
+        if (n > 0) {
+            launch_coldot(n, k, X, ldx, Y, ldy, Y2, ldy2, d, d2, part, ctx->num_sms, st);
+        } else {
+            cudaMemsetAsync(d, 0, sizeof(double) * k, st);
+            if (d2) cudaMemsetAsync(d2, 0, sizeof(double) * k, st);
+        }
+        int r = launched("coldot");
+        if (r) return r;
+        if (allred) {
+            rep->n_allreduce++;
+            r = allreduce_sum(ctx, d, k);
+            if (!r && d2) r = allreduce_sum(ctx, d2, k);
+        }
+        return r;
+    }
+    // out = a Xin + s P C (+ w W), optionally halted
+    int upd(double* out, int64_t ldo, double a, const double* Xin, int64_t ldxin, double s, const double* P,
+            int64_t ldp, int kp, const double* C, const double* W = nullptr, int64_t ldw = 0, double w_host = 0.0,
+            const double* w_dev = nullptr, bool halted = true) {
+        rep->n_update++;
+        UpdArgs u{};
+        u.n = n; u.kp = kp; u.k = k;
+        u.a = a; u.Xin = Xin; u.ldxin = ldxin;
+        u.s = s; u.P = P; u.ldp = ldp; u.C = C;
+        u.W = W; u.ldw = ldw; u.w_host = w_host; u.w_dev = w_dev;
+        u.out = out; u.ldo = ldo;
+        u.halt = halted ? &ds->halt : nullptr;
+        launch_update(u, st);
+        return launched("update");
+    }
+    int copy(double* dst, int64_t ldd, const double* src, int64_t lds) {
+        if (n == 0) return BK_OK;
+        return cuda_check(ctx,
+                          cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double), k * sizeof(double),
+                                            n, cudaMemcpyDeviceToDevice, st),
+                          "copy");
+    }
+    // R = B - A X  (X = 0: R = B)
+    int residual(const double* B, int64_t ldb, const double* X, int64_t ldx, double* R, bool x_zero) {
+        int r = copy(R, k, B, ldb);
+        if (r || x_zero) return r;
+        return spmm(X, ldx, R, k, -1.0, 1.0);
+    }
+};
+
+#define TRY(x) do { int _r = (x); if (_r) return _r; } while (0)
+
+int finish(Solver& S, const double* B, int64_t ldb, const double* X, int64_t ldx, cudaEvent_t e0) {
+    bk_ctx* ctx = S.ctx;
+    TRY(S.poll());
+    const DevStatus h = *S.hs;
+    bk_solve_report* rep = S.rep;
+    rep->iterations = h.iter;
+    rep->converged = h.converged;
+    rep->breakdown_column = h.breakdown_col;
+    for (int c = 0; c < S.k; ++c) rep->relres[c] = h.relres[c];
+    // true residual, recomputed from scratch (diagnostic)
+    double* R = S.vec();
+    double* d = S.small(64);
+    TRY(S.residual(B, ldb, X, ldx, R, false));
+    TRY(S.coldot(R, S.k, R, S.k, nullptr, 0, d, nullptr));
+    double* hd = (double*)((char*)ctx->h_pinned + 8192);
+    TRY(cuda_check(ctx, cudaMemcpyAsync(hd, d, sizeof(double) * S.k, cudaMemcpyDeviceToHost, S.st), "true res"));
+    cudaEvent_t e1;
+    cudaEventCreate(&e1);
+    cudaEventRecord(e1, S.st);
+    TRY(cuda_check(ctx, cudaStreamSynchronize(S.st), "finish"));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaEventDestroy(e1);
+    rep->t_total_ms = ms;
+    for (int c = 0; c < S.k; ++c) {
+        const double r0 = h.r0[c];
+        rep->true_relres[c] = std::sqrt(std::max(hd[c], 0.0)) / (r0 > 0.0 ? r0 : 1.0);
+    }
+    if (h.breakdown_col >= 0) rep->status = BK_BREAKDOWN;
+    else if (h.converged) rep->status = BK_OK;
+    else rep->status = BK_NOT_CONVERGED;
+    return rep->status;
+}
+
+// ---------------------------------------------------------------- O4 block CG
+int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
+    const int k = S.k;
+    const bool jac = S.o->precond == BK_PRECOND_JACOBI;
+    double* R = S.vec();
+    double* P = S.vec();
+    double* Q = S.vec();
+    double* Z = jac ? S.vec() : R;
+    double* sm = S.small(8 * 32 * 32);
+    double *PQ = sm, *RZ = sm + 1024, *RZn = sm + 2048, *al = sm + 3072, *be = sm + 4096, *nr = sm + 5120;
+    TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
+    if (jac) launch_row_scale(S.n, k, S.A->d_dinv, R, k, Z, k, S.st);
+    TRY(S.copy(P, k, Z, k));
+    TRY(S.gram(R, k, k, Z, k, RZ));
+    if (jac) {
+        TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
+        sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
+    } else {
+        sd_conv_check(RZ, k + 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
+    }
+    const double tol = S.o->breakdown_tol;
+    for (int it = 0; it < S.o->max_iters; ++it) {
+        TRY(S.spmm(P, k, Q, k));
+        TRY(S.gram(P, k, k, Q, k, PQ));
+        sd_chol_solve(PQ, RZ, al, k, k, tol, S.ds, S.st);
+        S.rep->n_small++;
+        TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al));
+        TRY(S.upd(R, k, 1.0, R, k, -1.0, Q, k, k, al));
+        if (jac) {
+            TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
+            sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
+            launch_row_scale(S.n, k, S.A->d_dinv, R, k, Z, k, S.st);
+            TRY(S.gram(R, k, k, Z, k, RZn));
+        } else {
+            TRY(S.gram(R, k, k, R, k, RZn));
+            sd_conv_check(RZn, k + 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
+        }
+        sd_chol_solve(RZ, RZn, be, k, k, tol, S.ds, S.st);
+        S.rep->n_small += 2;
+        TRY(S.upd(P, k, 1.0, Z, k, 1.0, P, k, k, be));
+        std::swap(RZ, RZn);
+        if ((it + 1) % S.o->check_every == 0 || it + 1 == S.o->max_iters) {
+            TRY(S.poll());
+            if (S.hs->halt) break;
+        }
+    }
+    return finish(S, B, ldb, X, ldx, e0);
+}
+
+// ---------------------------------------------------------------- O6 block BiCGStab
+int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
+    const int k = S.k;
+    double* R = S.vec();
+    double* Rt = S.vec();
+    double* P = S.vec();
+    double* V = S.vec();
+    double* Sv = S.vec();
+    double* T = S.vec();
+    double* Tmp = S.vec();
+    double* sm = S.small(8 * 32 * 32);
+    double *M1 = sm, *RR = sm + 1024, *al = sm + 2048, *RtT = sm + 3072, *be = sm + 4096, *ts = sm + 5120,
+           *tt = sm + 5120 + 32, *nr = sm + 5120 + 64;
+    TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
+    TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
+    sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
+    TRY(S.copy(Rt, k, R, k));
+    TRY(S.copy(P, k, R, k));
+    const double tol = S.o->breakdown_tol;
+    const double* om = &S.ds->omega;
+    const double* nom = &S.ds->neg_omega;
+    for (int it = 0; it < S.o->max_iters; ++it) {
+        TRY(S.spmm(P, k, V, k));
+        TRY(S.gram(Rt, k, k, V, k, M1));
+        TRY(S.gram(Rt, k, k, R, k, RR));
+        sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st);
+        TRY(S.upd(Sv, k, 1.0, R, k, -1.0, V, k, k, al));
+        TRY(S.spmm(Sv, k, T, k));
+        TRY(S.coldot(T, k, Sv, k, T, k, ts, tt));
+        sd_omega(ts, tt, k, S.ds, S.st);
+        TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al, Sv, k, 1.0, om));
+        TRY(S.upd(R, k, 1.0, Sv, k, 0.0, nullptr, k, 0, nullptr, T, k, 1.0, nom));
+        TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
+        sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
+        TRY(S.gram(Rt, k, k, T, k, RtT));
+        sd_lu_solve(M1, RtT, be, k, k, -1.0, tol, S.ds, S.st);
+        S.rep->n_small += 4;
+        TRY(S.upd(Tmp, k, 1.0, P, k, 0.0, nullptr, k, 0, nullptr, V, k, 1.0, nom));
+        TRY(S.upd(P, k, 1.0, R, k, 1.0, Tmp, k, k, be));
+        if ((it + 1) % S.o->check_every == 0 || it + 1 == S.o->max_iters) {
+            TRY(S.poll());
+            if (S.hs->halt) break;
+        }
+    }
+    return finish(S, B, ldb, X, ldx, e0);
+}
+
+// ---------------------------------------------------------------- O5 block GMRES(m)
+int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
+    const int k = S.k, m = S.o->restart;
+    const int64_t ldv = (int64_t)(m + 1) * k;
+    double* Vb = S.vec((int)ldv);
+    double* W = S.vec();
+    const size_t hk = (size_t)(m + 1) * k * k;
+    double* Hcol = S.small(hk);
+    double* H1 = S.small(hk);
+    double* H2 = S.small(hk);
+    double* g = S.small(hk);
+    double* Qs = S.small((size_t)m * 4 * k * k);
+    const int ldr = m * k;
+    double* Rtri = S.small((size_t)ldr * ldr);
+    double* y = S.small((size_t)m * k * k);
+    double* sm = S.small(8 * 32 * 32);
+    double *G1 = sm, *R1 = sm + 1024, *R1i = sm + 2048, *R2i = sm + 3072, *Sr = sm + 4096, *nr = sm + 5120;
+    const double tol = S.o->breakdown_tol;
+    TRY(S.residual(B, ldb, X, ldx, W, S.o->x0_is_zero));
+    TRY(S.coldot(W, k, W, k, nullptr, 0, nr, nullptr));
+    sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
+    int it = 0;
+    bool done = false;
+    while (!done && it < S.o->max_iters) {
+        cudaMemsetAsync(&S.ds->gm_steps, 0, sizeof(int), S.st);
+        cudaMemsetAsync(g, 0, hk * sizeof(double), S.st);
+        cudaMemsetAsync(Rtri, 0, (size_t)ldr * ldr * sizeof(double), S.st);
+        // [V_0, S] = CholQR2(R)
+        TRY(S.gram(W, k, k, W, k, G1));
+        sd_chol_qr(G1, R1, R1i, nullptr, nullptr, k, tol, S.ds, S.st);
+        TRY(S.upd(Vb, ldv, 0.0, nullptr, 0, 1.0, W, k, k, R1i));
+        TRY(S.gram(Vb, ldv, k, Vb, ldv, G1));
+        sd_chol_qr(G1, nullptr, R2i, R1, Sr, k, tol, S.ds, S.st);
+        TRY(S.upd(Vb, ldv, 0.0, nullptr, 0, 1.0, Vb, ldv, k, R2i));
+        sd_copy(Sr, g, k * k, S.st);
+        int j = 0;
+        for (; j < m; ++j) {
+            double* Vj = Vb + (int64_t)j * k;
+            double* Vn = Vb + (int64_t)(j + 1) * k;
+            const int ka = (j + 1) * k;
+            TRY(S.spmm(Vj, ldv, W, k));
+            // BCGS2: two passes of Hp = V^T W; W -= V Hp
+            TRY(S.gram(Vb, ldv, ka, W, k, H1));
+            TRY(S.upd(W, k, 1.0, W, k, -1.0, Vb, ldv, ka, H1));
+            TRY(S.gram(Vb, ldv, ka, W, k, H2));
+            TRY(S.upd(W, k, 1.0, W, k, -1.0, Vb, ldv, ka, H2));
+            sd_add(H1, H2, Hcol, ka * k, S.st);
+            // [V_{j+1}, H_{j+1,j}] = CholQR2(W)
+            TRY(S.gram(W, k, k, W, k, G1));
+            sd_chol_qr(G1, R1, R1i, nullptr, nullptr, k, tol, S.ds, S.st);
+            TRY(S.upd(Vn, ldv, 0.0, nullptr, 0, 1.0, W, k, k, R1i));
+            TRY(S.gram(Vn, ldv, k, Vn, ldv, G1));
+            sd_chol_qr(G1, nullptr, R2i, R1, Hcol + (int64_t)ka * k, k, tol, S.ds, S.st);
+            TRY(S.upd(Vn, ldv, 0.0, nullptr, 0, 1.0, Vn, ldv, k, R2i));
+            sd_gmres_step(Hcol, j, k, Qs, Rtri, ldr, g, S.o->rtol, S.o->conv_mode, S.ds, S.st);
+            S.rep->n_small += 5;
+            ++it;
+            if (it % S.o->check_every == 0 || it >= S.o->max_iters || j + 1 == m) {
+                TRY(S.poll());
+                if (S.hs->halt) { done = true; break; }
+            }
+            if (it >= S.o->max_iters) { done = true; break; }
+        }
+        // X += [V_0 .. V_{s-1}] y,  R y = g  (s completed steps of this cycle)
+        TRY(S.poll());
+        const int steps = S.hs->gm_steps;
+        if (S.hs->halt) done = true;
+        if (steps > 0) {
+            sd_gmres_backsolve(Rtri, ldr, g, y, steps * k, k, S.st);
+            TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, Vb, ldv, steps * k, y, nullptr, 0, 0.0, nullptr, false));
+        }
+        if (!done && it < S.o->max_iters) TRY(S.residual(B, ldb, X, ldx, W, false));
+    }
+    return finish(S, B, ldb, X, ldx, e0);
+}
+
+}  // namespace
+
+int solve_impl(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb, double* X, int64_t ldx,
+               const bk_solve_opts* o, bk_solve_report* rep) {
+    memset(rep, 0, sizeof *rep);
+    rep->breakdown_column = -1;
+    Solver S{ctx, A, A->n_local, k, o, rep, ctx->stream};
+    S.allred = ctx->nranks > 1;
+    cudaEvent_t e0;
+    cudaEventCreate(&e0);
+    cudaEventRecord(e0, S.st);
+    int r = S.init_status();
+    if (!r && o->x0_is_zero && A->n_local > 0)
+        r = cuda_check(ctx, cudaMemset2DAsync(X, ldx * sizeof(double), 0, k * sizeof(double), A->n_local, S.st),
+                       "zero X");
+    if (!r) {
+        switch (o->method) {
+            case BK_CG: r = block_cg(S, B, ldb, X, ldx, e0); break;
+            case BK_GMRES: r = block_gmres(S, B, ldb, X, ldx, e0); break;
+            default: r = block_bicgstab(S, B, ldb, X, ldx, e0); break;
+        }
+    }
+    cudaEventDestroy(e0);
+    return r;
+}
+
+}  // namespace bk

@@ -1,0 +1,282 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical
+seeded inputs.  Bar (BASELINE.json north_star, DESIGN.md §3 R17/R18):
+  * integer-exact inputs: bitwise;
+  * random inputs: componentwise |gpu - ref| <= 1e-12 * (|A| |X| |C|) (apply),
+    1e-12 * (|X|^T |Y|) (Gram), 1e-12 * (|a||X| + |s||P||C|) (update);
+  * solves: relative solution difference <= 1e-8 at the same tolerance,
+    iteration counts within 1, true residual <= rtol (x 10).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def bk():
+    import paper_2504_02117_b200 as m
+    return m
+
+
+@pytest.fixture(scope="module")
+def ctx(bk):
+    c = bk.Context(0)
+    yield c
+    c.close()
+
+
+def cu(t):
+    return t.to("cuda").contiguous()
+
+
+def abs_csr(A):
+    return synth.Csr(A.n_rows, A.n_cols, A.row_ptr, A.col, A.val.abs())
+
+
+def check_close(got, ref, scale, tol=TOL, what=""):
+    got = np.asarray(got); ref = np.asarray(ref)
+    err = np.abs(got - ref)
+    bound = tol * np.asarray(scale) + 1e-300
+    bad = err > bound
+    assert not bad.any(), f"{what}: {bad.sum()} entries exceed tol; max err/scale = {np.max(err / (np.asarray(scale) + 1e-300)):.3e}"
+
+
+# ----------------------------------------------------------------------------- a1 apply
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 12, 16, 24, 32])
+def test_spmm_integer_bitwise(ctx, bk, k):
+    A = synth.convdiff2d(40, integer=True)            # 1600 rows: 7 tiles incl. a ragged tail
+    X = synth.multivector(A.n_rows, k, 3, integer=True)
+    M = bk.Matrix.from_csr(ctx, A)
+    Y = torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
+    bk.bspmm_apply(ctx, M, cu(X), Y)
+    torch.cuda.synchronize()
+    assert np.array_equal(Y.cpu().numpy(), oracle.spmm(A, X))
+    C = synth.small_dense(k, k, 6, integer=True)
+    Y2 = cu(synth.multivector(A.n_rows, k, 4, integer=True))
+    Y2ref = oracle.spmm(A, X, C, alpha=-2.0, beta=3.0, Y=Y2.cpu())
+    bk.bspmm_apply(ctx, M, cu(X), Y2, C=cu(C), alpha=-2.0, beta=3.0)
+    torch.cuda.synchronize()
+    assert np.array_equal(Y2.cpu().numpy(), Y2ref)
+
+
+@pytest.mark.parametrize("cfg,k", [("c1", 4), ("c1", 16), ("c3s", 12), ("c4s", 32), ("c1", 1)])
+def test_spmm_random_within_tolerance(ctx, bk, cfg, k):
+    A = {"c1": lambda: synth.make_matrix("c1"), "c3s": lambda: synth.diffreact3d(20),
+         "c4s": lambda: synth.richards3d(24, 24, 12)}[cfg]()
+    X = synth.multivector(A.n_rows, k, 3)
+    C = synth.small_dense(k, k, 6)
+    M = bk.Matrix.from_csr(ctx, A)
+    Xg = cu(X)
+    for Cm, alpha, beta in ((None, 1.0, 0.0), (C, -1.0, 0.0), (C, 0.5, -1.5)):
+        Y0 = synth.multivector(A.n_rows, k, 4)
+        Y = cu(Y0)
+        bk.bspmm_apply(ctx, M, Xg, Y, C=None if Cm is None else cu(Cm), alpha=alpha, beta=beta)
+        ref = oracle.spmm(A, X, Cm, alpha, beta, Y0)
+        Cabs = np.eye(k) if Cm is None else np.abs(Cm.numpy())
+        scale = abs(alpha) * oracle.spmm(abs_csr(A), np.abs(X.numpy()), Cabs) + abs(beta) * np.abs(Y0.numpy())
+        check_close(Y.cpu().numpy(), ref, scale, what=f"{cfg} k={k} C={Cm is not None}")
+
+
+def test_spmm_rectangular_coupling_and_padded_ld(ctx, bk):
+    """k != k_out, ld > k (odd), host C: generic paths."""
+    A = synth.make_matrix("c1")
+    k, kout = 5, 3
+    Xf = synth.multivector(A.n_rows, 7, 3)                # ld 7, use first 5 columns
+    X = Xf[:, :k].contiguous()
+    C = synth.small_dense(k, kout, 6)
+    M = bk.Matrix.from_csr(ctx, A)
+    Yf = torch.zeros(A.n_rows, 9, dtype=torch.float64, device="cuda")
+    bk.bspmm_apply(ctx, M, cu(Xf)[:, :k], Yf[:, :kout], C=C.numpy())
+    ref = oracle.spmm(A, X, C)
+    scale = oracle.spmm(abs_csr(A), np.abs(X.numpy()), np.abs(C.numpy()))
+    check_close(Yf[:, :kout].cpu().numpy(), ref, scale, what="rect")
+    assert torch.all(Yf[:, kout:] == 0)
+
+
+def test_spmm_edge_cases(ctx, bk):
+    """Empty rows, a row longer than one tile's staging capacity, ragged tail, host buffers."""
+    n = 700
+    rp = [0]; cols = []; vals = []
+    g = torch.Generator().manual_seed(0)
+    for i in range(n):
+        if i % 97 == 5:                      # empty rows
+            rp.append(rp[-1]); continue
+        m = 3000 if i == 300 else 5          # one dense row: tile nnz > staging cap -> direct path
+        c = torch.randperm(n, generator=g)[:min(m, n)].sort().values if m < n else torch.arange(n)
+        cols.append(c); vals.append(torch.rand(len(c), generator=g, dtype=torch.float64) - 0.5)
+        rp.append(rp[-1] + len(c))
+    A = synth.Csr(n, n, torch.tensor(rp, dtype=torch.int32), torch.cat(cols).to(torch.int32), torch.cat(vals))
+    for k in (1, 4, 16):
+        X = synth.multivector(n, k, 3)
+        M = bk.Matrix.from_csr(ctx, A)
+        Yh = np.full((n, k), np.nan)
+        bk.bspmm_apply(ctx, M, X.numpy(), Yh)          # host X and Y
+        ref = oracle.spmm(A, X)
+        scale = oracle.spmm(abs_csr(A), np.abs(X.numpy()))
+        check_close(Yh, ref, scale, what=f"edge k={k}")
+        assert np.all(Yh[[5, 102, 199]] == 0.0)
+
+
+def test_spmm_rejects_bad_arguments(ctx, bk):
+    A = synth.make_matrix("c1")
+    M = bk.Matrix.from_csr(ctx, A)
+    X = cu(synth.multivector(A.n_rows, 4, 3))
+    with pytest.raises(bk.BkError) as e:
+        bk.bspmm_apply(ctx, M, X, X)                      # aliasing
+    assert e.value.status == bk.BK_ERR_ARG
+    X33 = torch.zeros(A.n_rows, 33, dtype=torch.float64, device="cuda")
+    with pytest.raises(bk.BkError):
+        bk.bspmm_apply(ctx, M, X33, X33.clone())           # k > 32
+    with pytest.raises(bk.BkError):
+        bk.Matrix(ctx, torch.tensor([0, 2, 3], dtype=torch.int32), torch.tensor([1, 0, 0], dtype=torch.int32),
+                  torch.ones(3, dtype=torch.float64))       # unsorted columns
+
+
+# ----------------------------------------------------------------------------- a3 gram
+@pytest.mark.parametrize("n,ka,kb", [(5000, 1, 1), (100003, 4, 4), (70001, 8, 8), (65537, 16, 16),
+                                     (40000, 32, 32), (30001, 12, 12), (20000, 3, 7), (50000, 96, 12),
+                                     (1, 2, 2), (255, 5, 5)])
+def test_gram_random_within_tolerance(ctx, bk, n, ka, kb):
+    X = synth.multivector(n, ka, 3)
+    Y = synth.multivector(n, kb, 4)
+    G = torch.empty(ka, kb, dtype=torch.float64, device="cuda")
+    bk.block_gram(ctx, cu(X), cu(Y), G)
+    ref = oracle.gram(X, Y)
+    scale = oracle.gram(np.abs(X.numpy()), np.abs(Y.numpy()))
+    check_close(G.cpu().numpy(), ref, scale, what=f"gram {n} {ka}x{kb}")
+    G2 = torch.empty_like(G)
+    bk.block_gram(ctx, cu(X), cu(Y), G2)
+    assert torch.equal(G, G2)                                  # deterministic
+
+
+def test_gram_integer_bitwise_and_host_output(ctx, bk):
+    X = synth.multivector(123457, 16, 3, integer=True)
+    Gh = np.zeros((16, 16))
+    bk.block_gram(ctx, cu(X), cu(X), Gh)
+    ref = (X.numpy().astype(np.int64).T @ X.numpy().astype(np.int64)).astype(np.float64)
+    assert np.array_equal(Gh, ref)
+
+
+def test_gram_strided_panel_of_basis(ctx, bk):
+    """Multi-Gram of the first j*k columns of a row-major basis with ld = (m+1) k (GMRES use)."""
+    k, m = 12, 6
+    V = synth.multivector(30000, (m + 1) * k, 3)
+    W = synth.multivector(30000, k, 4)
+    G = torch.empty(3 * k, k, dtype=torch.float64, device="cuda")
+    bk.block_gram(ctx, cu(V)[:, :3 * k], cu(W), G)
+    Vs = V[:, :3 * k].contiguous()
+    check_close(G.cpu().numpy(), oracle.gram(Vs, W), oracle.gram(np.abs(Vs.numpy()), np.abs(W.numpy())))
+
+
+# ----------------------------------------------------------------------------- a5 update
+@pytest.mark.parametrize("n,kp,k", [(10007, 4, 4), (50000, 16, 16), (30000, 32, 32), (777, 3, 5),
+                                    (20000, 300, 12), (5000, 12, 1)])
+def test_update_random_within_tolerance(ctx, bk, n, kp, k):
+    X0 = synth.multivector(n, k, 3)
+    P = synth.multivector(n, kp, 5)
+    C = synth.small_dense(kp, k, 6)
+    for a, s in ((1.0, 1.0), (0.0, -1.0), (2.5, 0.5)):
+        X = cu(X0)
+        bk.block_update(ctx, X, cu(P), cu(C), a=a, s=s)
+        ref = oracle.update(X0, P, C, a, s)
+        scale = abs(a) * np.abs(X0.numpy()) + abs(s) * (np.abs(P.numpy()) @ np.abs(C.numpy()))
+        check_close(X.cpu().numpy(), ref, scale, what=f"update {n} {kp} {k} a={a}")
+
+
+def test_update_integer_bitwise_and_inplace(ctx, bk):
+    X0 = synth.multivector(40000, 8, 3, integer=True)
+    P = synth.multivector(40000, 8, 5, integer=True)
+    C = synth.small_dense(8, 8, 6, integer=True)
+    X = cu(X0)
+    bk.block_update(ctx, X, cu(P), cu(C), a=2.0, s=-1.0)
+    assert np.array_equal(X.cpu().numpy(), oracle.update(X0, P, C, 2.0, -1.0))
+    Xi = cu(X0)
+    bk.block_update(ctx, Xi, Xi, cu(C), a=0.0, s=1.0)          # in place X <- X C
+    assert np.array_equal(Xi.cpu().numpy(), oracle.update(X0, X0, C, 0.0, 1.0))
+
+
+# ----------------------------------------------------------------------------- a6 solve
+SOLVES = [("cg", "c1s", {}), ("gmres", "c1", {"restart": 100}), ("gmres", "c1", {"restart": 20}),
+          ("bicgstab", "c1", {}), ("cg", "c1s", {"precond": "jacobi"})]
+
+
+@pytest.mark.parametrize("method,cfg,kw", SOLVES)
+@pytest.mark.parametrize("k", [1, 4])
+def test_solve_matches_oracle(ctx, bk, method, cfg, kw, k):
+    A = synth.make_matrix(cfg)
+    B = synth.multivector(A.n_rows, k, 2)
+    M = bk.Matrix.from_csr(ctx, A)
+    X = torch.zeros(A.n_rows, k, dtype=torch.float64, device="cuda")
+    st, rep = bk.block_krylov_solve(ctx, M, cu(B), X, method=method, rtol=1e-10, max_iters=2000,
+                                    x0_is_zero=True, **kw)
+    okw = dict(kw)
+    Xr, rr = oracle.SOLVERS[method](A, B, rtol=1e-10, max_iters=2000, **okw)
+    assert rr.converged and rep["converged"] and st == 0
+    assert abs(rep["iterations"] - rr.iterations) <= 1, (rep["iterations"], rr.iterations)
+    rel = np.linalg.norm(X.cpu().numpy() - Xr) / np.linalg.norm(Xr)
+    assert rel <= 1e-8, rel
+    assert np.all(rep["true_relres"] <= 1e-9)
+    Xs, rs = oracle.SOLVERS[method](A, B, rtol=1e-30, max_iters=10, **okw)        # fixed-iteration parity
+    X10 = torch.zeros_like(X)
+    bk.block_krylov_solve(ctx, M, cu(B), X10, method=method, rtol=1e-30, max_iters=10, x0_is_zero=True, **kw)
+    assert np.linalg.norm(X10.cpu().numpy() - Xs) / np.linalg.norm(Xs) <= 1e-10
+
+
+@pytest.mark.parametrize("method", ["cg", "gmres", "bicgstab"])
+def test_solve_identity_one_iteration(ctx, bk, method):
+    n = 3000
+    A = synth.Csr(n, n, torch.arange(n + 1, dtype=torch.int32), torch.arange(n, dtype=torch.int32),
+                  torch.ones(n, dtype=torch.float64))
+    B = synth.multivector(n, 8, 2)
+    X = torch.zeros(n, 8, dtype=torch.float64, device="cuda")
+    st, rep = bk.block_krylov_solve(ctx, bk.Matrix.from_csr(ctx, A), cu(B), X, method=method, x0_is_zero=True)
+    assert st == 0 and rep["iterations"] == 1
+    assert torch.allclose(X.cpu(), B, atol=1e-14)
+
+
+def test_solve_duplicated_rhs_breakdown_status(ctx, bk):
+    A = synth.make_matrix("c1s")
+    b = synth.multivector(A.n_rows, 2, 2)
+    B = torch.cat([b, b[:, :1]], dim=1)
+    X = torch.zeros(A.n_rows, 3, dtype=torch.float64, device="cuda")
+    st, rep = bk.block_krylov_solve(ctx, bk.Matrix.from_csr(ctx, A), cu(B), X, method="cg", x0_is_zero=True)
+    _, rr = oracle.block_cg(A, B)
+    assert st == bk.BK_BREAKDOWN and rep["status"] == "breakdown"
+    assert rep["breakdown_column"] == rr.breakdown_column == 2
+    assert torch.all(torch.isfinite(X))
+
+
+def test_solve_not_converged_and_host_buffers(ctx, bk):
+    A = synth.make_matrix("c1s")
+    B = synth.multivector(A.n_rows, 4, 2).numpy()
+    Xh = np.zeros_like(B)
+    st, rep = bk.block_krylov_solve(ctx, bk.Matrix.from_csr(ctx, A), B, Xh, method="cg", max_iters=5)
+    assert st == bk.BK_NOT_CONVERGED and rep["iterations"] == 5
+    Xr, _ = oracle.block_cg(A, B, rtol=1e-30, max_iters=5)
+    assert np.linalg.norm(Xh - Xr) / np.linalg.norm(Xr) < 1e-10
+
+
+# ----------------------------------------------------------------------------- full size, sampled
+@pytest.mark.parametrize("cfg,k", [("c2", 16), ("c2", 1), ("c3", 12)])
+def test_full_size_apply_sampled_rows(ctx, bk, cfg, k):
+    """BASELINE sizes in the bench launch configuration; rows sampled (rows are independent)."""
+    A = synth.make_matrix(cfg, device="cuda")
+    X = synth.multivector(A.n_rows, k, 3, device="cuda")
+    M = bk.Matrix.from_csr(ctx, A)
+    Y = torch.empty_like(X)
+    bk.bspmm_apply(ctx, M, X, Y)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(1)
+    rows = np.unique(np.concatenate([rng.integers(0, A.n_rows, 4000), [0, 1, A.n_rows - 1],
+                                     np.arange(255, A.n_rows, 256)[:500]]))
+    Ac = A.to("cpu")
+    Xc = X.cpu()
+    ref = oracle.spmm_rows(Ac, rows, Xc)
+    scale = oracle.spmm_rows(abs_csr(Ac), rows, Xc.abs())
+    check_close(Y.cpu().numpy()[rows], ref, scale, what=f"{cfg} k={k}")
