@@ -59,6 +59,9 @@ int         bk_version(void);                       /* e.g. 100 = 0.1.0      */
 const char *bk_status_string(int status);
 /* Message of the last failure on ctx (never NULL; "" if none).            */
 const char *bk_last_error(const bk_ctx *ctx);
+/* Number of CUDA kernels this library has launched in this process (all
+ * contexts, monotonically increasing; for launch accounting in benchmarks). */
+int64_t     bk_kernel_launch_count(void);
 
 /* Create a context on CUDA device `device`, ordering work on `cuda_stream`
  * (a cudaStream_t, used as is; NULL = the legacy default stream).  The

@@ -34,7 +34,7 @@ METHODS = {"cg": 0, "gmres": 1, "bicgstab": 2}
 PRECONDS = {"none": 0, "jacobi": 1}
 CONV = {"all": 0, "first": 1}
 
-EXPORTED = ["bk_version", "bk_status_string", "bk_last_error", "bk_ctx_create", "bk_ctx_set_stream",
+EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last_error", "bk_ctx_create", "bk_ctx_set_stream",
             "bk_ctx_synchronize", "bk_ctx_destroy", "bk_get_nccl_unique_id", "bk_ctx_set_comm",
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
             "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo"]
@@ -65,6 +65,7 @@ class CsrInfo(ctypes.Structure):
 _P, _I, _I64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
 _sig = {
     "bk_version": ([], _I),
+    "bk_kernel_launch_count": ([], _I64),
     "bk_status_string": ([_I], ctypes.c_char_p),
     "bk_last_error": ([_P], ctypes.c_char_p),
     "bk_ctx_create": ([ctypes.POINTER(_P), _I, _P], _I),
@@ -99,6 +100,11 @@ class BkError(RuntimeError):
 
 def version() -> int:
     return _lib.bk_version()
+
+
+def kernel_launch_count() -> int:
+    """Kernels launched by libbk.so in this process so far (bk_kernel_launch_count)."""
+    return int(_lib.bk_kernel_launch_count())
 
 
 # ----------------------------------------------------------------- marshalling

@@ -16,6 +16,8 @@ using namespace bk;
 
 namespace bk {
 
+std::atomic<long long> g_launches{0};
+
 int set_error(bk_ctx* ctx, int code, const std::string& msg) {
     if (ctx) {
         ctx->last_error = msg;
@@ -124,6 +126,8 @@ static const double* stage_in(bk_ctx* ctx, int slot, const double* p, int64_t n,
 
 // ------------------------------------------------------------------ context
 extern "C" int bk_version(void) { return 100; }
+
+extern "C" int64_t bk_kernel_launch_count(void) { return (int64_t)g_launches.load(); }
 
 extern "C" const char* bk_status_string(int s) {
     switch (s) {

@@ -14,7 +14,14 @@
 #include <nccl.h>
 #endif
 
+#include <atomic>
+
 namespace bk {
+
+// Every kernel launch of the library goes through BK_KERNEL so the process-wide
+// count is exact (bk_kernel_launch_count(); bench.py reports it as gpu_launches).
+extern std::atomic<long long> g_launches;
+#define BK_KERNEL(...) (++::bk::g_launches, __VA_ARGS__)
 
 // ------------------------------------------------------------------ device status
 // Written by the small-dense / convergence kernels, polled by the host driver.

@@ -139,10 +139,10 @@ void gram_t(int64_t n, int ka, int kb, const double* X, int64_t ldx, const doubl
     const int npanels = (ka + KAP - 1) / KAP;
     const int nchunks = nchunks_for(n, npanels, num_sms);
     const int64_t rpc = (n + nchunks - 1) / nchunks;
-    gram_partial_kernel<KAP, KBP><<<nchunks * npanels, kThreads, 0, st>>>(n, ka, kb, X, ldx, Y, ldy, part,
-                                                                       npanels, rpc > 0 ? rpc : 1);
+    BK_KERNEL(gram_partial_kernel<KAP, KBP><<<nchunks * npanels, kThreads, 0, st>>>(n, ka, kb, X, ldx, Y, ldy, part,
+                                                                       npanels, rpc > 0 ? rpc : 1));
     const int warps = ka * kb;
-    gram_reduce_kernel<KAP, KBP><<<(warps * 32 + 255) / 256, 256, 0, st>>>(part, nchunks, npanels, ka, kb, G);
+    BK_KERNEL(gram_reduce_kernel<KAP, KBP><<<(warps * 32 + 255) / 256, 256, 0, st>>>(part, nchunks, npanels, ka, kb, G));
 }
 
 template <int KAP>
@@ -208,9 +208,9 @@ void coldot_t(int64_t n, int k, const double* X, int64_t ldx, const double* Y, i
               cudaStream_t st) {
     const int nchunks = nchunks_for(n, 1, num_sms);
     const int64_t rpc = (n + nchunks - 1) / nchunks;
-    coldot_partial_kernel<KP><<<nchunks, kThreads, 0, st>>>(n, k, X, ldx, Y, ldy, Y2, ldy2, part,
-                                                           rpc > 0 ? rpc : 1);
-    coldot_reduce_kernel<KP><<<1, 1024, 0, st>>>(part, nchunks, k, d, d2);
+    BK_KERNEL(coldot_partial_kernel<KP><<<nchunks, kThreads, 0, st>>>(n, k, X, ldx, Y, ldy, Y2, ldy2, part,
+                                                           rpc > 0 ? rpc : 1));
+    BK_KERNEL(coldot_reduce_kernel<KP><<<1, 1024, 0, st>>>(part, nchunks, k, d, d2));
 }
 
 // ------------------------------------------------------------------ update
@@ -284,7 +284,7 @@ void update_k(const UpdArgs& a, cudaStream_t st) {
     constexpr int RPP = kThreads / (KP / VEC);
     constexpr int PASSES = kUpdRowsPerCta / RPP > 0 ? kUpdRowsPerCta / RPP : 1;
     const unsigned grid = (unsigned)((a.n + RPP * PASSES - 1) / (RPP * PASSES));
-    if (grid) update_kernel<KP, VEC><<<grid, kThreads, 0, st>>>(a);
+    if (grid) BK_KERNEL(update_kernel<KP, VEC><<<grid, kThreads, 0, st>>>(a));
 }
 
 // ------------------------------------------------------------------ misc
@@ -380,22 +380,22 @@ void launch_update(const UpdArgs& a, cudaStream_t st) {
 void launch_row_scale(int64_t n, int k, const double* dinv, const double* X, int64_t ldx, double* out,
                       int64_t ldo, cudaStream_t st) {
     const int64_t t = n * k;
-    if (t > 0) row_scale_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(n, k, dinv, X, ldx, out, ldo);
+    if (t > 0) BK_KERNEL(row_scale_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(n, k, dinv, X, ldx, out, ldo));
 }
 
 void launch_extract_diag_inv(int64_t n, int64_t row_offset, const int32_t* rp, const int32_t* col,
                              const double* val, double* dinv, cudaStream_t st) {
-    if (n > 0) diag_inv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, row_offset, rp, col, val, dinv);
+    if (n > 0) BK_KERNEL(diag_inv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, row_offset, rp, col, val, dinv));
 }
 
 void launch_fill(double* p, int64_t n, double v, cudaStream_t st) {
-    if (n > 0) fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n, v);
+    if (n > 0) BK_KERNEL(fill_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(p, n, v));
 }
 
 void launch_pack_rows(int64_t nrows, int k, const int32_t* rows, const double* X, int64_t ldx,
                       double* out, cudaStream_t st) {
     const int64_t t = nrows * k;
-    if (t > 0) pack_rows_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(nrows, k, rows, X, ldx, out);
+    if (t > 0) BK_KERNEL(pack_rows_kernel<<<(unsigned)((t + 255) / 256), 256, 0, st>>>(nrows, k, rows, X, ldx, out));
 }
 
 }  // namespace bk

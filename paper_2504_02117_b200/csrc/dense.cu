@@ -379,26 +379,26 @@ __global__ void gmres_backsolve_kernel(const double* __restrict__ Rtri, int ldr,
 
 void sd_chol_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double tol, DevStatus* st,
                    cudaStream_t s) {
-    chol_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, tol, st);
+    BK_KERNEL(chol_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, tol, st));
 }
 void sd_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign, double tol,
                  DevStatus* st, cudaStream_t s) {
-    lu_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, sign, tol, st);
+    BK_KERNEL(lu_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, sign, tol, st));
 }
 void sd_chol_qr(const double* G, double* R, double* Rinv, const double* Rprev, double* Rprod, int k, double tol,
                 DevStatus* st, cudaStream_t s) {
-    chol_qr_kernel<<<1, 256, 0, s>>>(G, R, Rinv, Rprev, Rprod, k, tol, st);
+    BK_KERNEL(chol_qr_kernel<<<1, 256, 0, s>>>(G, R, Rinv, Rprev, Rprod, k, tol, st));
 }
 void sd_conv_check(const double* g, int gstride, int k, double rtol, int conv_mode, int init, DevStatus* st,
                    cudaStream_t s) {
-    conv_check_kernel<<<1, 32, 0, s>>>(g, gstride, k, rtol, conv_mode, init, st);
+    BK_KERNEL(conv_check_kernel<<<1, 32, 0, s>>>(g, gstride, k, rtol, conv_mode, init, st));
 }
 void sd_omega(const double* ts, const double* tt, int k, DevStatus* st, cudaStream_t s) {
-    omega_kernel<<<1, 32, 0, s>>>(ts, tt, k, st);
+    BK_KERNEL(omega_kernel<<<1, 32, 0, s>>>(ts, tt, k, st));
 }
-void sd_copy(const double* src, double* dst, int n, cudaStream_t s) { copy_kernel<<<1, 256, 0, s>>>(src, dst, n); }
+void sd_copy(const double* src, double* dst, int n, cudaStream_t s) { BK_KERNEL(copy_kernel<<<1, 256, 0, s>>>(src, dst, n)); }
 void sd_add(const double* a, const double* b, double* out, int n, cudaStream_t s) {
-    add_kernel<<<(n + 255) / 256 < 64 ? (n + 255) / 256 : 64, 256, 0, s>>>(a, b, out, n);
+    BK_KERNEL(add_kernel<<<(n + 255) / 256 < 64 ? (n + 255) / 256 : 64, 256, 0, s>>>(a, b, out, n));
 }
 void sd_gmres_step(double* Hcol, int j, int k, double* Qs, double* Rtri, int ldr, double* g, double rtol,
                    int conv_mode, DevStatus* st, cudaStream_t s) {
@@ -408,10 +408,10 @@ void sd_gmres_step(double* Hcol, int j, int k, double* Qs, double* Rtri, int ldr
         cudaFuncSetAttribute(gmres_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         attr_set = true;
     }
-    gmres_step_kernel<<<1, 512, smem, s>>>(Hcol, j, k, Qs, Rtri, ldr, g, rtol, conv_mode, st);
+    BK_KERNEL(gmres_step_kernel<<<1, 512, smem, s>>>(Hcol, j, k, Qs, Rtri, ldr, g, rtol, conv_mode, st));
 }
 void sd_gmres_backsolve(const double* Rtri, int ldr, const double* g, double* y, int nk, int k, cudaStream_t s) {
-    gmres_backsolve_kernel<<<1, 512, 0, s>>>(Rtri, ldr, g, y, nk, k);
+    BK_KERNEL(gmres_backsolve_kernel<<<1, 512, 0, s>>>(Rtri, ldr, g, y, nk, k));
 }
 
 }  // namespace bk

@@ -271,10 +271,10 @@ void launch_t(const SpmmArgs& a, cudaStream_t st) {
     if (a.rows) {
         constexpr int RPP = kThreads / (KP / VEC);
         unsigned grid = (unsigned)((a.nrows + RPP - 1) / RPP);
-        bspmm_rows_kernel<KP, VEC, HAS_C, GHOST><<<grid, kThreads, 0, st>>>(a);
+        BK_KERNEL(bspmm_rows_kernel<KP, VEC, HAS_C, GHOST><<<grid, kThreads, 0, st>>>(a));
     } else {
         unsigned grid = (unsigned)((a.nrows + kTileRows - 1) / kTileRows);
-        bspmm_tile_kernel<KP, VEC, HAS_C, GHOST><<<grid, kThreads, 0, st>>>(a);
+        BK_KERNEL(bspmm_tile_kernel<KP, VEC, HAS_C, GHOST><<<grid, kThreads, 0, st>>>(a));
     }
 }
 
