@@ -1,0 +1,494 @@
+#!/usr/bin/env python
+"""Benchmark of the block-Krylov hot path (BASELINE.json metric: block-SpMM GB/s & GFLOP/s,
+fraction of HBM peak, vs k; block-Krylov solve time) on B200.
+
+One STEP = one pass of the whole hot path over the c2 workload (BASELINE.json
+configs[1]: 2-D convection-diffusion, 1024 x 1024 cells, 5-point CSR fp64):
+    for k in (1, 2, 4, 8, 16):  bspmm_apply (Y = A X_k), block_gram (X_k^T Y_k),
+                                block_update (P_k += 1e-3 X_k C_k)
+    + block_krylov_solve: 5 fixed block-BiCGStab iterations at k = 16
+(a1 apply, a3 Gram, a4 small dense, a5 update, a6 solver; a2 halo when N > 1).
+`value` = algorithmic bytes of the step / device time of the step (GB/s).
+L2 (126 MB) is flushed by a 512 MiB write before every timed step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+N > 1 (torchrun): weak scaling, a 1024 x (1024 N) grid row-partitioned across
+ranks (z/y-slabs), NCCL halo exchange inside bspmm_apply, NCCL allreduce of the
+Gram matrices; time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+KS = (1, 2, 4, 8, 16)
+SOLVE_K = 16
+SOLVE_ITERS = 5
+UPD_SCALE = 1e-3
+NX = 1024
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            mp = json.load(f)
+        return float(mp["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def step_bytes(pm, n, nnz, ks=KS, solve_k=SOLVE_K, solve_iters=SOLVE_ITERS, n_ghost_rows=0):
+    """Algorithmic bytes / flops of one step (perfmodel.py)."""
+    b = f = 0
+    parts = {}
+    for k in ks:
+        sb = pm.spmm_bytes(n, nnz, k, n_ghost=n_ghost_rows)
+        gb = pm.gram_bytes(n, k, k)
+        ub = pm.update_bytes(n, k, k)
+        parts[k] = dict(spmm=sb, gram=gb, update=ub, spmm_flops=pm.spmm_flops(nnz, k),
+                        gram_flops=pm.gram_flops(n, k, k), update_flops=pm.update_flops(n, k, k))
+        b += sb + gb + ub
+        f += parts[k]["spmm_flops"] + parts[k]["gram_flops"] + parts[k]["update_flops"]
+    # solve: x0 = 0 -> R = B (copy), ||R||, Rt = R, P = R, iterations, final true residual
+    k = solve_k
+    sb = (16 * n * k + pm.coldot_bytes(n, k) + 2 * 16 * n * k
+          + solve_iters * pm.bicgstab_iter_bytes(n, nnz, k)
+          + 16 * n * k + pm.spmm_bytes(n, nnz, k, beta_nonzero=True) + pm.coldot_bytes(n, k))
+    parts["solve"] = dict(bytes=sb)
+    b += sb
+    return b, f, parts
+
+
+# ------------------------------------------------------------------ clocks
+class Clocks:
+    def __init__(self, path):
+        self.path = path
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self, device_index=0):
+        try:
+            rows = [ln.split(",") for ln in open(self.path) if ln.strip()]
+        except Exception:
+            return None
+        rows = [[c.strip() for c in r] for r in rows if len(r) >= 9 and r[0].strip() == str(device_index)]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = max(float(r[2]) for r in rows if r[2].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower().startswith("active")})
+        load = [s for s in sm if s > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2504_02117_b200 as bk
+    from paper_2504_02117_b200 import perfmodel as pm
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        if rank == 0:
+            print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}; using WORLD_SIZE", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    ctx = bk.Context(local)
+    if world > 1:
+        uid = bk.Context.nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8, device=dev)
+        dist.broadcast(t, 0)
+        ctx.set_comm(bytes(t.cpu().tolist()), world, rank)
+
+    # ---- workload: c2 (N = 1) or the weak-scaled 1024 x 1024N grid, this rank's row slab
+    ny = NX * world
+    A_full = synth.convdiff2d(NX, ny=ny, device=dev)
+    n_glob = A_full.n_rows
+    r0, r1 = rank * n_glob // world, (rank + 1) * n_glob // world
+    A = A_full.rows(r0, r1) if world > 1 else A_full
+    del A_full
+    M = bk.Matrix(ctx, A.row_ptr, A.col, A.val, n_global=n_glob, row_begin=r0, n_local=r1 - r0)
+    info = M.info()
+    n, nnz = info["n_local"], info["nnz"]
+    X = {k: synth.multivector(n, k, synth.SEEDS["X"], row_begin=r0, n_global=n_glob, device=dev) for k in KS}
+    Y = {k: torch.empty(n, k, dtype=torch.float64, device=dev) for k in KS}
+    P = {k: synth.multivector(n, k, synth.SEEDS["P"], row_begin=r0, n_global=n_glob, device=dev) for k in KS}
+    C = {k: synth.small_dense(k, k, synth.SEEDS["C"], device=dev) for k in KS}
+    G = {k: torch.empty(k, k, dtype=torch.float64, device=dev) for k in KS}
+    B = synth.multivector(n, SOLVE_K, synth.SEEDS["B"], row_begin=r0, n_global=n_glob, device=dev)
+    Xs = torch.zeros(n, SOLVE_K, dtype=torch.float64, device=dev)
+    flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    allred = world > 1
+
+    def one_step(ev=None):
+        # ev[key] = (start, end); start is the previous key's end event (recorded already)
+        for k in KS:
+            bk.bspmm_apply(ctx, M, X[k], Y[k])
+            if ev is not None:
+                ev[("spmm", k)][1].record(stream)
+            bk.block_gram(ctx, X[k], Y[k], G[k], allreduce=allred)
+            if ev is not None:
+                ev[("gram", k)][1].record(stream)
+            bk.block_update(ctx, P[k], X[k], C[k], a=1.0, s=UPD_SCALE)
+            if ev is not None:
+                ev[("update", k)][1].record(stream)
+        st, rep = bk.block_krylov_solve(ctx, M, B, Xs, method="bicgstab", rtol=0.0, max_iters=SOLVE_ITERS,
+                                        x0_is_zero=True, check_every=SOLVE_ITERS)
+        if ev is not None:
+            ev[("solve", SOLVE_K)][1].record(stream)
+        return rep
+
+    # warm-up
+    for _ in range(args.warmup):
+        one_step()
+    torch.cuda.synchronize()
+
+    keys = [(c, k) for k in KS for c in ("spmm", "gram", "update")] + [("solve", SOLVE_K)]
+    durs = {kk: [] for kk in keys}
+    step_ms = []
+    launches0 = bk.kernel_launch_count()
+    clocks = Clocks(os.path.join(ROOT, "gpurun_out" if os.path.isdir(os.path.join(ROOT, "gpurun_out")) else ".",
+                                 f".bench_clocks_{rank}.csv"))
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with clocks:
+        for _ in range(args.steps):
+            flush.fill_(1.0)                                   # L2 flush (outside the step timing)
+            ev = {kk: (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for kk in keys}
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            # chain: each kernel's start event is the previous kernel's end event
+            prev = e0
+            one_step_ev = {}
+            for kk in keys:
+                one_step_ev[kk] = (prev, ev[kk][1])
+                prev = ev[kk][1]
+            one_step(one_step_ev)
+            torch.cuda.synchronize()
+            step_ms.append(e0.elapsed_time(prev))
+            for kk in keys:
+                a, b = one_step_ev[kk]
+                durs[kk].append(a.elapsed_time(b))
+        torch.cuda.synchronize()
+    launches = bk.kernel_launch_count() - launches0
+    if world > 1:
+        dist.barrier()
+    total_ms = sum(step_ms)
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    n_ghost = info["n_ghost"]
+    bytes_rank, flops_rank, parts = step_bytes(pm, n, nnz, n_ghost_rows=n_ghost)
+    bytes_all = bytes_rank * world
+    value = bytes_all / (ms_per_step * 1e-3) / 1e9
+
+    # ---- per-kernel (mean device time inside the timed region)
+    peak, peak_src = peaks()
+    per = {}
+    for (c, k) in keys:
+        mean_ms = sum(durs[(c, k)]) / len(durs[(c, k)])
+        if c == "solve":
+            by = parts["solve"]["bytes"]
+            per[f"solve_k{k}"] = dict(ms=mean_ms, gbs=by / (mean_ms * 1e-3) / 1e9,
+                                      ms_per_iter=mean_ms / SOLVE_ITERS)
+        else:
+            by = parts[k][c]
+            fl = parts[k][c + "_flops"]
+            per[f"{c}_k{k}"] = dict(ms=mean_ms, gbs=by / (mean_ms * 1e-3) / 1e9,
+                                    gflops=fl / (mean_ms * 1e-3) / 1e9, frac=by / (mean_ms * 1e-3) / 1e9 / peak)
+    # dominant kernel: largest share of the step among the single-kernel calls
+    dom = max((kk for kk in per if not kk.startswith("solve")), key=lambda kk: per[kk]["ms"])
+    dk = dom.split("_k")
+    dom_bytes = parts[int(dk[1])][dk[0]]
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom)
+        except Exception:
+            traffic = None
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": per[dom]["gbs"], "peak": peak, "unit": "GB/s",
+                "frac": per[dom]["gbs"] / peak, "traffic": traffic, "alg_bytes": dom_bytes, "peak_source": peak_src,
+                "share_of_step": per[dom]["ms"] / ms_per_step}
+
+    # ---- isolated k sweep (flush before every kernel; adds k = 32), outside the timed region
+    sweep = {}
+    if not args.no_sweep:
+        for k in (1, 2, 4, 8, 16, 32):
+            Xk = X[k] if k in X else synth.multivector(n, k, synth.SEEDS["X"], row_begin=r0, n_global=n_glob, device=dev)
+            Yk = torch.empty(n, k, dtype=torch.float64, device=dev)
+            Pk = P[k] if k in P else synth.multivector(n, k, synth.SEEDS["P"], device=dev)
+            Ck = C[k] if k in C else synth.small_dense(k, k, synth.SEEDS["C"], device=dev)
+            Gk = torch.empty(k, k, dtype=torch.float64, device=dev)
+            row = {}
+            for name, fn, by, fl in (
+                    ("spmm", lambda: bk.bspmm_apply(ctx, M, Xk, Yk), pm.spmm_bytes(n, nnz, k, n_ghost=n_ghost),
+                     pm.spmm_flops(nnz, k)),
+                    ("spmm_C", lambda: bk.bspmm_apply(ctx, M, Xk, Yk, C=Ck), pm.spmm_bytes(n, nnz, k, n_ghost=n_ghost),
+                     pm.spmm_flops(nnz, k, n, coupled=True)),
+                    ("gram", lambda: bk.block_gram(ctx, Xk, Yk, Gk, allreduce=allred), pm.gram_bytes(n, k, k),
+                     pm.gram_flops(n, k, k)),
+                    ("update", lambda: bk.block_update(ctx, Pk, Xk, Ck, a=1.0, s=UPD_SCALE), pm.update_bytes(n, k, k),
+                     pm.update_flops(n, k, k))):
+                ts = []
+                for _ in range(7):
+                    flush.fill_(1.0)
+                    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    a.record(stream)
+                    fn()
+                    b.record(stream)
+                    torch.cuda.synchronize()
+                    ts.append(a.elapsed_time(b))
+                ms = statistics.median(ts[1:])
+                row[name] = dict(us=round(ms * 1e3, 2), gbs=round(by / (ms * 1e-3) / 1e9, 1),
+                                 gflops=round(fl / (ms * 1e-3) / 1e9, 1), frac=round(by / (ms * 1e-3) / 1e9 / peak, 4))
+            sweep[k] = row
+
+    # ---- solve time (full solves, outside the timed region): c1 block GMRES k=4 to 1e-10
+    solve_report = None
+    if world == 1 and not args.no_sweep:
+        A1 = synth.make_matrix("c1")
+        M1 = bk.Matrix.from_csr(ctx, A1)
+        B1 = synth.multivector(A1.n_rows, 4, synth.SEEDS["B"], device=dev)
+        X1 = torch.zeros_like(B1)
+        ts = []
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            st, rep = bk.block_krylov_solve(ctx, M1, B1, X1, method="gmres", restart=100, rtol=1e-10, x0_is_zero=True)
+            b.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(b))
+        solve_report = {"c1_gmres_k4_ms": statistics.median(ts), "iterations": rep["iterations"],
+                        "converged": rep["converged"], "max_true_relres": float(max(rep["true_relres"]))}
+
+    # ---- e2e: same step through the C ABI with pinned HOST buffers (H2D/D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        hX = {k: X[k].cpu().pin_memory() for k in KS}
+        hY = {k: torch.empty(n, k, dtype=torch.float64).pin_memory() for k in KS}
+        hP = {k: P[k].cpu().pin_memory() for k in KS}
+        hC = {k: C[k].cpu().pin_memory() for k in KS}
+        hG = {k: torch.empty(k, k, dtype=torch.float64).pin_memory() for k in KS}
+        hB = B.cpu().pin_memory()
+        hXs = torch.zeros(n, SOLVE_K, dtype=torch.float64).pin_memory()
+
+        def host_step():
+            for k in KS:
+                bk.bspmm_apply(ctx, M, hX[k], hY[k])
+                bk.block_gram(ctx, hX[k], hY[k], hG[k], allreduce=allred)
+                bk.block_update(ctx, hP[k], hX[k], hC[k], a=1.0, s=UPD_SCALE)
+            bk.block_krylov_solve(ctx, M, hB, hXs, method="bicgstab", rtol=0.0, max_iters=SOLVE_ITERS,
+                                  x0_is_zero=True, check_every=SOLVE_ITERS)
+
+        host_step()
+        e_steps = max(3, min(args.steps, 10))
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(e_steps):
+            flush.fill_(1.0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            host_step()
+            torch.cuda.synchronize()
+            ts.append((time.perf_counter() - t0) * 1e3)
+        e_ms = sum(ts) / len(ts)
+        if world > 1:
+            t = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        h2d = sum(8 * n * k + 16 * n * k + (16 * n * k + 8 * k * k) for k in KS) + 8 * n * SOLVE_K
+        d2h = sum(8 * n * k + 8 * k * k + 8 * n * k for k in KS) + 8 * n * SOLVE_K
+        e2e = {"value": bytes_all / (e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "note": "same step via the C ABI with pinned host X/Y/P/C/G/B buffers; host wall clock"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1): bounded sample of the same step
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(rows=65536, reps=args.cpu_reps)
+
+    if rank == 0:
+        cs = clocks.summary(local)
+        line = {
+            "metric": "block-SpMM GB/s & GFLOP/s (fraction of HBM peak) vs k; block-Krylov solve time",
+            "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic (seeded SplitMix64 inputs; FV matrices assembled on device)",
+            "config": {"workload": "c2" if world == 1 else f"c2-weak-{world}",
+                       "grid": f"{NX}x{ny}", "rows_per_gpu": n, "nnz_per_gpu": nnz, "ks": list(KS),
+                       "solve": f"block BiCGStab k={SOLVE_K}, {SOLVE_ITERS} iterations",
+                       "step_alg_bytes_per_gpu": bytes_rank, "step_flops_per_gpu": flops_rank,
+                       "l2": "flushed (512 MiB write) before every timed step",
+                       "parallelism": "single GPU" if world == 1 else f"row partition x{world}, NCCL halo + allreduce"},
+            "gpu_launches": launches,
+            "roofline": roofline,
+            "per_kernel": per,
+            "sweep": sweep,
+            "solve": solve_report,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "clocks": cs,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ oracle (CPU) arm
+def _oracle_sample(rows):
+    """Leading `rows` x `rows` principal block of c2 (a valid smaller instance of the same operator)."""
+    import synth
+    A = synth.make_matrix("c2")
+    rows = min(rows, A.n_rows)
+    S = A.rows(0, rows)
+    keep = S.col < rows
+    counts = torch_counts(S.row_ptr, keep)
+    import torch
+    rp = torch.zeros(rows + 1, dtype=torch.int64)
+    rp[1:] = torch.cumsum(counts, 0)
+    return synth.Csr(rows, rows, rp.to(torch.int32), S.col[keep].contiguous(), S.val[keep].contiguous(), "c2-sample")
+
+
+def torch_counts(row_ptr, keep):
+    import torch
+    rp = row_ptr.to(torch.int64)
+    cs = torch.zeros(len(keep) + 1, dtype=torch.int64)
+    cs[1:] = torch.cumsum(keep.to(torch.int64), 0)
+    return cs[rp[1:]] - cs[rp[:-1]]
+
+
+def oracle_step_fn(rows):
+    import numpy as np
+    import oracle
+    import synth
+    A = _oracle_sample(rows)
+    Ao = oracle.CsrNp.of(A)
+    n = A.n_rows
+    X = {k: synth.multivector(n, k, synth.SEEDS["X"]).numpy() for k in KS}
+    P = {k: synth.multivector(n, k, synth.SEEDS["P"]).numpy() for k in KS}
+    C = {k: synth.small_dense(k, k, synth.SEEDS["C"]).numpy() for k in KS}
+    B = synth.multivector(n, SOLVE_K, synth.SEEDS["B"]).numpy()
+
+    def step():
+        for k in KS:
+            Y = oracle.spmm(Ao, X[k])
+            oracle.gram(X[k], Y)
+            P[k] = oracle.update(P[k], X[k], C[k], 1.0, UPD_SCALE)
+        oracle.block_bicgstab(Ao, B, rtol=0.0, max_iters=SOLVE_ITERS)
+        return np.zeros(1)
+
+    return step, n, A.nnz
+
+
+def cpu_baseline(rows=262144, reps=1):
+    from paper_2504_02117_b200 import perfmodel as pm
+    step, n, nnz = oracle_step_fn(rows)
+    ts = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    t = statistics.median(ts)
+    by, _, _ = step_bytes(pm, n, nnz)
+    return {"value": by / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": f"same step on the leading {n}-row principal block of c2 ({nnz} nnz), {reps} rep(s), "
+                      f"{t:.2f} s/step; oracle = plain C (gcc -O2, 1 thread) + numpy solver"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from paper_2504_02117_b200 import perfmodel as pm
+    rows = 32768
+    step, n, nnz = oracle_step_fn(rows)
+    for _ in range(args.warmup):
+        step()
+    ts = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        step()
+        ts.append(time.perf_counter() - t0)
+    ms = sum(ts) / len(ts) * 1e3
+    by, _, _ = step_bytes(pm, n, nnz)
+    v = by / (ms * 1e-3) / 1e9
+    sample = (f"same step (bspmm/gram/update at k=1,2,4,8,16 + 5 block-BiCGStab its at k=16) on the leading "
+              f"{n}-row principal block of c2 ({nnz} nnz)")
+    print(json.dumps({
+        "impl": "reference", "metric": "block-SpMM GB/s & GFLOP/s (fraction of HBM peak) vs k; block-Krylov solve time",
+        "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "c2" if world == 1 else f"c2-weak-{world}", "sample_rows": n},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-reps", type=int, default=2)
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        print("note: warmup < 3 violates the timing rules; using 3", file=sys.stderr)
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,100 @@
+"""Algorithmic traffic / flop counts and the paper's performance model (host logic only).
+
+* Paper (context): AI(spMV) = 1/8 (§1); AI(spBOP) = k / (4 (k+1))
+  (§3, Fig. AIBOP); simplified ECM counts omega = 2kz FLOP,
+  beta = 2z + 2kz doubles, tau = z (2 + 2k) doubles (§3).
+* Algorithmic bytes (what the method must move): the CSR streamed
+  once, every multivector read once and written once.  These are the numerators
+  of every GB/s this repo reports (bench.py `roofline.achieved`).
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+D = 8   # bytes per float64
+I = 4   # bytes per int32
+
+
+# ------------------------------------------------------------------ paper model
+def paper_ai_spmv() -> Fraction:
+    """two FLOP per two doubles -> 1/8 FLOP/byte."""
+    return Fraction(2, 2 * D)
+
+
+def paper_ai_spbop(k: int) -> Fraction:
+    """2k FLOP per (k + 1) doubles -> k / (4 (k+1)) FLOP/byte."""
+    return Fraction(2 * k, (k + 1) * D)
+
+
+def paper_ecm_counts(k: int, z: int):
+    """(omega FLOP, beta doubles from memory, tau doubles L1<->registers)."""
+    return 2 * k * z, 2 * z + 2 * k * z, z * (2 + 2 * k)
+
+
+# ------------------------------------------------------------------ algorithmic model
+def spmm_bytes(n_rows: int, nnz: int, k: int, k_out: int | None = None, beta_nonzero: bool = False,
+               n_ghost: int = 0) -> int:
+    """12 nnz + 4 (N + 1) [CSR] + 8 k (N + N_ghost) [X read once] + 8 k_out N [Y write] (+ Y read if beta)."""
+    k_out = k if k_out is None else k_out
+    b = (I + D) * nnz + I * (n_rows + 1) + D * k * (n_rows + n_ghost) + D * k_out * n_rows
+    if beta_nonzero:
+        b += D * k_out * n_rows
+    return b
+
+
+def spmm_flops(nnz: int, k: int, n_rows: int = 0, k_out: int | None = None, coupled: bool = False) -> int:
+    """2 nnz k (+ 2 N k k_out for the k x k_out coupling)."""
+    f = 2 * nnz * k
+    if coupled:
+        f += 2 * n_rows * k * (k if k_out is None else k_out)
+    return f
+
+
+def gram_bytes(n: int, ka: int, kb: int, same: bool = False) -> int:
+    """8 N (ka + kb); 8 N k for X^T X."""
+    return D * n * (ka if same else ka + kb)
+
+
+def gram_flops(n: int, ka: int, kb: int) -> int:
+    return 2 * n * ka * kb
+
+
+def update_bytes(n: int, kp: int, k: int, a_nonzero: bool = True, extra_term: bool = False) -> int:
+    """8 N (kp + k) + 8 N k [X read if a != 0] (+ 8 N k for a third operand W)."""
+    return D * n * (kp + k + (k if a_nonzero else 0) + (k if extra_term else 0))
+
+
+def update_flops(n: int, kp: int, k: int) -> int:
+    return 2 * n * kp * k
+
+
+def coldot_bytes(n: int, k: int, n_y: int = 1) -> int:
+    return D * n * k * (1 + n_y)
+
+
+def bicgstab_iter_bytes(n: int, nnz: int, k: int) -> int:
+    """One block BiCGStab iteration as enqueued by solve.cpp (DESIGN.md §3 O6)."""
+    b = 2 * spmm_bytes(n, nnz, k)                     # V = A P, T = A S
+    b += 3 * gram_bytes(n, k, k)                      # Rt^T V, Rt^T R, Rt^T T
+    b += coldot_bytes(n, k, 2) + coldot_bytes(n, k, 1)  # <T,S>, <T,T>; ||R||
+    b += update_bytes(n, k, k)                        # S = R - V alpha
+    b += update_bytes(n, k, k, extra_term=True)       # X += P alpha + omega S
+    b += update_bytes(n, 0, k, extra_term=True)       # R = S - omega T
+    b += update_bytes(n, 0, k, extra_term=True)       # Tmp = P - omega V
+    b += update_bytes(n, k, k)                        # P = R + Tmp beta
+    return b
+
+
+def cg_iter_bytes(n: int, nnz: int, k: int) -> int:
+    """One block CG iteration (unpreconditioned) as enqueued by solve.cpp (O4)."""
+    return (spmm_bytes(n, nnz, k) + gram_bytes(n, k, k) + 2 * update_bytes(n, k, k)
+            + gram_bytes(n, k, k, same=True) + update_bytes(n, k, k))
+
+
+def gmres_step_bytes(n: int, nnz: int, k: int, j: int) -> int:
+    """Inner step j (0-based) of block GMRES with BCGS2 + CholQR2 (O5)."""
+    ka = (j + 1) * k
+    b = spmm_bytes(n, nnz, k)
+    b += 2 * (gram_bytes(n, ka, k) + update_bytes(n, ka, k))
+    b += 2 * (gram_bytes(n, k, k, same=True) + update_bytes(n, k, k, a_nonzero=False))
+    return b

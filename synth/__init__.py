@@ -202,8 +202,8 @@ SDIRK3_GAMMA = 0.43586652150845900                  # DESIGN.md R10
 
 
 def convdiff2d(n: int, *, D: float = 1.0, v=(1.0, 0.5), tau: float = 0.12,
-               gamma: float = SDIRK2_GAMMA, integer: bool = False, device="cpu") -> Csr:
-    """J = M/tau + gamma*K on an n x n cell-centred grid of [0,1]^2 (h = 1/n).
+               gamma: float = SDIRK2_GAMMA, integer: bool = False, device="cpu", ny: int | None = None) -> Csr:
+    """J = M/tau + gamma*K on an n x ny cell-centred grid (h = 1/n; ny defaults to n: [0,1]^2).
 
     K: TPFA diffusion (interior T = D, Dirichlet ghost cell T_b = 2D) plus
     first-order upwind convection with face flux q = h (v . n); inflow
@@ -211,7 +211,8 @@ def convdiff2d(n: int, *, D: float = 1.0, v=(1.0, 0.5), tau: float = 0.12,
     M = h^2 I.  integer=True: the exact-arithmetic 4 / -1 stencil variant.
     """
     h = 1.0 / n
-    N, (ix, iy, _), dirs = _face_dirs(n, n, 1, device)
+    ny = n if ny is None else ny
+    N, (ix, iy, _), dirs = _face_dirs(n, ny, 1, device)
     offs, vals, masks = [], [], []
     if integer:
         for off, m, _, _ in dirs:
@@ -222,7 +223,7 @@ def convdiff2d(n: int, *, D: float = 1.0, v=(1.0, 0.5), tau: float = 0.12,
             else:
                 vals.append(torch.full((N,), -1.0, dtype=torch.float64, device=device))
                 masks.append(m)
-        return _assemble(offs, vals, masks, N, device, f"convdiff2d_int_{n}", (n, n, 1))
+        return _assemble(offs, vals, masks, N, device, f"convdiff2d_int_{n}x{ny}", (n, ny, 1))
     diag = torch.full((N,), h * h / tau, dtype=torch.float64, device=device)
     Kdiag = torch.zeros(N, dtype=torch.float64, device=device)
     T = D
@@ -242,7 +243,7 @@ def convdiff2d(n: int, *, D: float = 1.0, v=(1.0, 0.5), tau: float = 0.12,
     offs2 = [(offs + [0])[j] for j in pos]
     vals2 = [(vals + [diag])[j] for j in pos]
     masks2 = [(masks + [torch.ones(N, dtype=torch.bool, device=device)])[j] for j in pos]
-    return _assemble(offs2, vals2, masks2, N, device, f"convdiff2d_{n}", (n, n, 1))
+    return _assemble(offs2, vals2, masks2, N, device, f"convdiff2d_{n}x{ny}", (n, ny, 1))
 
 
 # ---------------------------------------------------------------------------

@@ -1,0 +1,36 @@
+"""Pins of the performance model against the paper's printed closed forms (CPU only)."""
+from fractions import Fraction
+
+from paper_2504_02117_b200 import perfmodel as pm
+
+GOLD = __file__.rsplit("/", 1)[0] + "/golden/ai_spbop.txt"
+
+
+def test_paper_ai_closed_forms_golden():
+    """P:31 AI(spMV) = 1/8; P:675 AI(spBOP) = k/(4(k+1)) at the Fig. AIBOP samples; ~1.8x at k = 16."""
+    rows = [ln.split() for ln in open(GOLD) if ln.strip() and not ln.startswith("#")]
+    assert pm.paper_ai_spmv() == Fraction(1, 8)
+    for r in rows:
+        if r[0] == "factor_k16_about":
+            ratio = pm.paper_ai_spbop(16) / pm.paper_ai_spmv()
+            assert abs(float(ratio) - float(r[1])) < 0.1        # "a factor of about 1.8" (exact 32/17)
+            assert ratio == Fraction(32, 17)
+        else:
+            assert pm.paper_ai_spbop(int(r[0])) == Fraction(r[1])
+    assert pm.paper_ai_spbop(1) == pm.paper_ai_spmv()           # k = 1 reduces to spMV
+
+
+def test_paper_ecm_counts():
+    """omega = 2kz, beta = 2z + 2kz, tau = z(2+2k)."""
+    assert pm.paper_ecm_counts(8, 1000) == (16000, 18000, 18000)
+
+
+def test_algorithmic_bytes():
+    n, nnz = 1048576, 5238784
+    # c2 k = 8 -> 201.3 MB, k = 16 -> 335.5 MB, k = 1 -> 83.8 MB
+    assert round(pm.spmm_bytes(n, nnz, 8) / 1e6, 1) == 201.3
+    assert round(pm.spmm_bytes(n, nnz, 16) / 1e6, 1) == 335.5
+    assert round(pm.spmm_bytes(n, nnz, 1) / 1e6, 1) == 83.8
+    assert pm.gram_bytes(10, 3, 2) == 8 * 10 * 5 and pm.gram_bytes(10, 3, 3, same=True) == 240
+    assert pm.update_bytes(10, 4, 4) == 8 * 10 * 12 and pm.update_bytes(10, 4, 4, a_nonzero=False) == 640
+    assert pm.spmm_flops(100, 4) == 800 and pm.spmm_flops(100, 4, 10, coupled=True) == 800 + 320
