@@ -214,77 +214,78 @@ void coldot_t(int64_t n, int k, const double* X, int64_t ldx, const double* Y, i
 }
 
 // ------------------------------------------------------------------ update
-constexpr int kUpdRowsPerCta = 256;
-constexpr int kUpdCRows = 128;     // rows of C staged per chunk
+// One group of LANES = KP threads per row, lane l owns output column l.  All
+// PASSES rows of a thread issue their X / W / P loads before any arithmetic
+// (many independent 8-byte loads in flight per thread, coalesced across the
+// group); the P row is then broadcast with warp shuffles against C rows held
+// in shared memory.  kp > KP (GMRES multi-update) loops over KP-wide chunks.
+constexpr int kUpdPasses = 8;
 
-template <int KP, int VEC>
+template <int KP>
 __global__ void __launch_bounds__(kThreads)
 update_kernel(const UpdArgs a) {
-    constexpr int LANES = KP / VEC;
+    constexpr int LANES = KP;
     constexpr int RPP = kThreads / LANES;
-    constexpr int PASSES = kUpdRowsPerCta / RPP > 0 ? kUpdRowsPerCta / RPP : 1;
-    constexpr int CW = LANES * VEC;               // P values per lane-group chunk (== KP)
-    __shared__ double s_C[kUpdCRows * KP];
+    constexpr int PASSES = kUpdPasses;
+    __shared__ double s_C[KP * KP];
     if (a.halt && *a.halt) return;
-    const int tid = threadIdx.x, grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
+    const int tid = threadIdx.x, grp = tid / LANES, lane = tid % LANES;
     const int k = a.k, kp = a.kp;
-    const int64_t base = (int64_t)blockIdx.x * (RPP * PASSES);
-    double acc[PASSES][VEC];
+    const bool lane_in = lane < k;
+    const int64_t base = (int64_t)blockIdx.x * (RPP * PASSES) + grp;
+    double xv[PASSES], wv[PASSES], acc[PASSES];
 #pragma unroll
-    for (int q = 0; q < PASSES; ++q)
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) acc[q][t] = 0.0;
-    static_assert(VEC == 1, "update_kernel: one column per lane");
-    for (int cb = 0; cb < kp; cb += kUpdCRows) {
-        const int nrows_c = min(kUpdCRows, kp - cb);
-        __syncthreads();
-        for (int i = tid; i < kUpdCRows * KP; i += kThreads) {
+    for (int q = 0; q < PASSES; ++q) {
+        const int64_t row = base + (int64_t)q * RPP;
+        const bool act = row < a.n && lane_in;
+        xv[q] = (act && a.a != 0.0) ? a.Xin[row * a.ldxin + lane] : 0.0;
+        wv[q] = (act && a.W) ? a.W[row * a.ldw + lane] : 0.0;
+        acc[q] = 0.0;
+    }
+    for (int cb = 0; cb < kp; cb += KP) {
+        const int nc = min(KP, kp - cb);
+        if (cb > 0) __syncthreads();
+        for (int i = tid; i < KP * KP; i += kThreads) {
             const int r = i / KP, c = i % KP;
-            s_C[i] = (r < nrows_c && c < k) ? a.C[(int64_t)(cb + r) * k + c] : 0.0;
+            s_C[i] = (r < nc && c < k) ? a.C[(int64_t)(cb + r) * k + c] : 0.0;
+        }
+        double pv[PASSES];
+#pragma unroll
+        for (int q = 0; q < PASSES; ++q) {
+            const int64_t row = base + (int64_t)q * RPP;
+            pv[q] = (row < a.n && lane < nc) ? a.P[row * a.ldp + cb + lane] : 0.0;
         }
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < PASSES; ++q) {
-            const int64_t row = base + (int64_t)q * RPP + grp;
-            const bool active = row < a.n;
-            for (int qb = 0; qb < nrows_c; qb += CW) {
-                // lane l loads P[row, cb + qb + l] (coalesced); the group then
-                // broadcasts each value with a shuffle (all lanes of the warp
-                // execute this loop: its bounds are CTA-uniform)
-                const double pv = (active && qb + lane < nrows_c) ? __ldg(a.P + row * a.ldp + cb + qb + lane) : 0.0;
-                const int lim = min(CW, nrows_c - qb);
-                for (int qq = 0; qq < lim; ++qq) {
-                    const double p = (LANES == 1) ? pv : __shfl_sync(0xffffffffu, pv, qq, LANES);
+        for (int qq = 0; qq < KP; ++qq) {
+            if (qq < nc) {                                   // CTA-uniform
+                const double cv = s_C[qq * KP + lane];
 #pragma unroll
-                    for (int t = 0; t < VEC; ++t) acc[q][t] = fma(p, s_C[(qb + qq) * KP + c0 + t], acc[q][t]);
+                for (int q = 0; q < PASSES; ++q) {
+                    const double p = (LANES == 1) ? pv[q] : __shfl_sync(0xffffffffu, pv[q], qq, LANES);
+                    acc[q] = fma(p, cv, acc[q]);
                 }
             }
         }
     }
+    const double w = a.W ? (a.w_dev ? a.w_host * *a.w_dev : a.w_host) : 0.0;
 #pragma unroll
     for (int q = 0; q < PASSES; ++q) {
-        const int64_t row = base + (int64_t)q * RPP + grp;
-        if (row >= a.n) continue;
-        const double wv = a.W ? (a.w_dev ? a.w_host * *a.w_dev : a.w_host) : 0.0;
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) {
-            const int c = c0 + t;
-            if (c >= k) continue;
-            double v = a.s * acc[q][t];
-            if (a.a != 0.0) v = fma(a.a, a.Xin[row * a.ldxin + c], v);
-            if (a.W) v = fma(wv, a.W[row * a.ldw + c], v);
-            a.out[row * a.ldo + c] = v;
+        const int64_t row = base + (int64_t)q * RPP;
+        if (row < a.n && lane_in) {
+            double v = a.s * acc[q];
+            v = fma(a.a, xv[q], v);
+            v = fma(w, wv[q], v);
+            a.out[row * a.ldo + lane] = v;
         }
     }
 }
 
 template <int KP>
 void update_k(const UpdArgs& a, cudaStream_t st) {
-    constexpr int VEC = 1;
-    constexpr int RPP = kThreads / (KP / VEC);
-    constexpr int PASSES = kUpdRowsPerCta / RPP > 0 ? kUpdRowsPerCta / RPP : 1;
-    const unsigned grid = (unsigned)((a.n + RPP * PASSES - 1) / (RPP * PASSES));
-    if (grid) BK_KERNEL(update_kernel<KP, VEC><<<grid, kThreads, 0, st>>>(a));
+    constexpr int RPP = kThreads / KP;
+    const unsigned grid = (unsigned)((a.n + RPP * kUpdPasses - 1) / (RPP * kUpdPasses));
+    if (grid) BK_KERNEL(update_kernel<KP><<<grid, kThreads, 0, st>>>(a));
 }
 
 // ------------------------------------------------------------------ misc

@@ -2,54 +2,109 @@
 //
 // PAPER.md §3: the BOP kernel "Y <- A X" loads the matrix once for
 // all k columns.  B200 mapping:
-//  * one CTA = one tile of TR consecutive rows; the tile's row pointers,
-//    column ids and values (a contiguous CSR range) are streamed from HBM
-//    exactly once with coalesced 16-byte loads into shared memory;
-//  * a group of LANES = KP/VEC threads owns one row; lane l holds columns
-//    [l*VEC, l*VEC+VEC) (VEC = 2 -> 16-byte vector gathers of X);
-//  * X rows are gathered through L1/L2 (neighbouring rows of a stencil hit the
-//    same lines), Y is written once with streaming (evict-first) stores;
+//  * persistent, warp-specialised CTAs (3 per SM): one PRODUCER warp streams
+//    CSR tiles (TR = 256 rows: row pointers, column ids, values -- one
+//    contiguous range each) from HBM into a 2-stage shared-memory ring with
+//    TMA bulk copies (cp.async.bulk + mbarrier complete_tx, evict-first L2
+//    policy), so the matrix is read exactly once and several tiles are always
+//    in flight; eight CONSUMER warps compute tile t while t+1 lands;
+//  * a group of LANES = KP/VEC consumer threads owns one row; lane l holds
+//    columns [l*VEC, l*VEC+VEC) (VEC = 4 -> two 16-byte gathers of X per
+//    nonzero); a row's gathers are issued in batches (B*VEC = 16 doubles)
+//    before any FMA (memory-level parallelism for the L2-resident stencil
+//    neighbours).  Variants (tile kernel, stage/CTA counts, VEC, row pairing)
+//    are selectable with BK_SPMM_KERNEL / BK_SPMM_VEC for A/B runs;
+//  * Y is written once with streaming (evict-first) stores;
 //  * the optional k x k_out coupling C is applied in the epilogue
 //    from shared memory, so the coupled apply costs no extra HBM pass.
+// A simpler one-tile-per-CTA kernel (load, sync, compute) is kept as the
+// `BK_SPMM_KERNEL=tile` variant for A/B measurements; row lists (boundary rows
+// of a partitioned matrix) use a direct, unstaged kernel.
+#include <cstdlib>
+#include <cstring>
+
 #include "bk_internal.h"
 
 namespace bk {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kTileRows = 256;   // rows per CTA tile
-constexpr int kCap = 2048;       // staged nonzeros per tile (fallback: direct loads)
+constexpr int kThreads = 256;    // consumer threads
+constexpr int kTileRows = 256;   // rows per CSR tile
+constexpr int kCap = 2304;       // staged nonzeros per tile (9 per row); larger tiles load directly
+// X gathers in flight per row and thread: B rows of X (VEC doubles each), B*VEC = 16
+template <int VEC>
+struct Batch { static constexpr int B = VEC >= 8 ? 2 : (VEC >= 4 ? 4 : 8); };
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try(bar, parity)) {
+    }
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// TMA bulk copy global -> shared (1-D), completion counted on `bar`
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
 
 __device__ __forceinline__ void ld_x(const double* p, double (&x)[1]) { x[0] = __ldg(p); }
-__device__ __forceinline__ void ld_x(const double* p, double (&x)[2]) {
-    double2 v = __ldg(reinterpret_cast<const double2*>(p));
-    x[0] = v.x; x[1] = v.y;
+template <int VEC>
+__device__ __forceinline__ void ld_x(const double* p, double (&x)[VEC]) {
+#pragma unroll
+    for (int t = 0; t < VEC; t += 2) {
+        double2 v = __ldg(reinterpret_cast<const double2*>(p) + t / 2);
+        x[t] = v.x;
+        x[t + 1] = v.y;
+    }
 }
-__device__ __forceinline__ void ld_x4(const double* p, double (&x)[4]) {
-    double2 v0 = __ldg(reinterpret_cast<const double2*>(p));
-    double2 v1 = __ldg(reinterpret_cast<const double2*>(p + 2));
-    x[0] = v0.x; x[1] = v0.y; x[2] = v1.x; x[3] = v1.y;
-}
-__device__ __forceinline__ void ld_x(const double* p, double (&x)[4]) { ld_x4(p, x); }
 
 // streaming 16-byte load of CSR data (read once: do not pollute L1)
 __device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
     int4 r;
     asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(p));
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                 : "l"(p));
     return r;
 }
 __device__ __forceinline__ double2 ld_stream_d2(const double2* p) {
     double2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];"
-                 : "=d"(r.x), "=d"(r.y) : "l"(p));
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
     return r;
 }
 
 template <int VEC>
 __device__ __forceinline__ void st_y(double* p, const double (&v)[VEC], int valid) {
-    if (VEC == 2 && valid == 2) {
-        __stcs(reinterpret_cast<double2*>(p), make_double2(v[0], v[1]));
+    if (VEC >= 2 && valid == VEC) {
+#pragma unroll
+        for (int t = 0; t < VEC; t += 2) __stcs(reinterpret_cast<double2*>(p) + t / 2, make_double2(v[t], v[t + 1]));
     } else {
 #pragma unroll
         for (int t = 0; t < VEC; ++t)
@@ -57,31 +112,296 @@ __device__ __forceinline__ void st_y(double* p, const double (&v)[VEC], int vali
     }
 }
 
-template <int KP, int VEC, bool HAS_C, bool GHOST>
+template <bool GHOST>
+__device__ __forceinline__ const double* xrow(const SpmmArgs& a, int c) {
+    return (GHOST && c >= a.ncol_local) ? a.Xg + (int64_t)(c - a.ncol_local) * a.ldg : a.X + (int64_t)c * a.ldx;
+}
+
+// acc += sum_{p in [s,e)} val[p] * X[col[p], c0 : c0+VEC], in CSR order, gathers batched
+template <int VEC, bool GHOST>
+__device__ __forceinline__ void row_accumulate(const SpmmArgs& a, const int* col, const double* val, int s, int e,
+                                               int c0, bool lane_in, double (&acc)[VEC]) {
+    constexpr int kBatch = Batch<VEC>::B;
+    for (int p = s; p < e; p += kBatch) {
+        double x[kBatch][VEC];
+        double v[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            if (p + u < e && lane_in) {
+                const int c = col[p + u];
+                v[u] = val[p + u];
+                ld_x(xrow<GHOST>(a, c) + c0, x[u]);
+            } else {
+                v[u] = 0.0;
+#pragma unroll
+                for (int t = 0; t < VEC; ++t) x[u][t] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u)
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) acc[t] = fma(v[u], x[u][t], acc[t]);
+    }
+}
+
+// Two rows per thread group at once: both rows' gathers (up to B each) are in
+// flight together (memory-level parallelism at 2 columns per thread, where a
+// warp instruction covers whole 128-byte X lines).
+template <int VEC>
+__device__ __forceinline__ void row_accumulate2(const SpmmArgs& a, const int* col, const double* val, int sA, int eA,
+                                                int sB, int eB, int c0, bool lane_in, double (&accA)[VEC],
+                                                double (&accB)[VEC]) {
+    constexpr int kBatch = Batch<VEC>::B;
+    int pA = sA, pB = sB;
+    while (pA < eA || pB < eB) {
+        double xa[kBatch][VEC], xb[kBatch][VEC];
+        double va[kBatch], vb[kBatch];
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u) {
+            if (pA + u < eA && lane_in) {
+                va[u] = val[pA + u];
+                ld_x(xrow<false>(a, col[pA + u]) + c0, xa[u]);
+            } else {
+                va[u] = 0.0;
+#pragma unroll
+                for (int t = 0; t < VEC; ++t) xa[u][t] = 0.0;
+            }
+            if (pB + u < eB && lane_in) {
+                vb[u] = val[pB + u];
+                ld_x(xrow<false>(a, col[pB + u]) + c0, xb[u]);
+            } else {
+                vb[u] = 0.0;
+#pragma unroll
+                for (int t = 0; t < VEC; ++t) xb[u][t] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kBatch; ++u)
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) {
+                accA[t] = fma(va[u], xa[u][t], accA[t]);
+                accB[t] = fma(vb[u], xb[u][t], accB[t]);
+            }
+        pA += kBatch;
+        pB += kBatch;
+    }
+}
+
+// out = acc C (C from shared memory via a per-row scratch line) or acc; then
+// Y = alpha out + beta Y.  Every lane of the warp must call it (__syncwarp).
+template <int KP, int VEC, bool HAS_C>
+__device__ __forceinline__ void row_epilogue(const SpmmArgs& a, const double* s_C, double* t_row, int c0,
+                                             bool active, int64_t row, const double (&acc)[VEC]) {
+    const int k = a.k, kout = a.kout;
+    double out[VEC];
+    if (HAS_C) {
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) t_row[c0 + t] = (c0 + t < k) ? acc[t] : 0.0;
+        __syncwarp();
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) out[t] = 0.0;
+        for (int c = 0; c < k; ++c) {
+            const double tv = t_row[c];
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) out[t] = fma(tv, s_C[c * KP + c0 + t], out[t]);
+        }
+        __syncwarp();
+    } else {
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) out[t] = acc[t];
+    }
+    if (active && c0 < kout) {
+        double* yp = a.Y + row * a.ldy + c0;
+        const int valid = min(VEC, kout - c0);
+        double v[VEC];
+        if (a.beta != 0.0) {
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) v[t] = (t < valid) ? a.alpha * out[t] + a.beta * yp[t] : 0.0;
+        } else {
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) v[t] = a.alpha * out[t];
+        }
+        st_y<VEC>(yp, v, valid);
+    }
+}
+
+template <int KP, bool HAS_C>
+__device__ __forceinline__ void load_C(const SpmmArgs& a, double* s_C, int tid, int nthreads) {
+    if (HAS_C) {
+        for (int i = tid; i < KP * KP; i += nthreads) {
+            const int r = i / KP, c = i % KP;
+            s_C[i] = (r < a.k && c < a.kout) ? a.C[r * a.kout + c] : 0.0;
+        }
+    }
+}
+
+// All passes over one tile's rows (NC consumer threads).  Called separately
+// with shared-memory and with global col/val pointers so the compiler emits
+// LDS (not generic loads) for the staged case.
+template <int KP, int VEC, bool HAS_C, int NC = kThreads, int TR = kTileRows, bool PAIR = false>
+__device__ __forceinline__ void tile_rows(const SpmmArgs& a, const int* col, const double* val, const int* s_rp,
+                                          int nr, int64_t r0, int grp, int c0, bool lane_in, const double* s_C,
+                                          double* t_row) {
+    constexpr int RPP = NC / (KP / VEC);
+    constexpr int PASSES = (TR + RPP - 1) / RPP;
+    if constexpr (PAIR) {
+        constexpr int HALF = (PASSES + 1) / 2;
+#pragma unroll 1
+        for (int pass = 0; pass < HALF; ++pass) {
+            const int r = pass * RPP + grp, r2 = (pass + HALF) * RPP + grp;
+            const bool act = r < nr, act2 = (pass + HALF < PASSES) && r2 < nr;
+            double acc[VEC], acc2[VEC];
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) { acc[t] = 0.0; acc2[t] = 0.0; }
+            row_accumulate2<VEC>(a, col, val, act ? s_rp[r] : 0, act ? s_rp[r + 1] : 0, act2 ? s_rp[r2] : 0,
+                                 act2 ? s_rp[r2 + 1] : 0, c0, lane_in, acc, acc2);
+            row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, act, r0 + r, acc);
+            row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, act2, r0 + r2, acc2);
+        }
+        return;
+    }
+#pragma unroll 1
+    for (int pass = 0; pass < PASSES; ++pass) {
+        const int r = pass * RPP + grp;
+        const bool active = r < nr;
+        double acc[VEC];
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
+        if (active) row_accumulate<VEC, false>(a, col, val, s_rp[r], s_rp[r + 1], c0, lane_in, acc);
+        row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
+    }
+}
+
+// ------------------------------------------------------------------ persistent TMA pipeline
+// NC consumer threads, NS ring stages, MINB CTAs per SM (variants: DESIGN.md §4.1)
+template <int NC, int NS, int MINB, int TR_, int CAP_>
+struct PipeCfg {
+    static constexpr int TR = TR_, CAP = CAP_;
+    static constexpr int RP_INTS = TR + 8;                 // rows + 1, aligned start/end slack
+    static constexpr int COL_INTS = CAP + 8;
+    static constexpr int VAL_DBL = CAP + 8;
+    static constexpr int RP_BYTES = RP_INTS * 4;
+    static constexpr int COL_BYTES = COL_INTS * 4;
+    static constexpr int VAL_BYTES = VAL_DBL * 8;
+    static constexpr int STAGE_BYTES = RP_BYTES + COL_BYTES + VAL_BYTES;
+    // ring + barriers/meta + (C and one scratch line per row group when coupled)
+    static constexpr int bytes(int kp, int rpp, bool has_c) {
+        return NS * STAGE_BYTES + 64 * 8 + (has_c ? (kp * kp + rpp * (kp + 1)) * 8 : 0);
+    }
+};
+
+template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP, bool PAIR>
+__global__ void __launch_bounds__(NC + 32, MINB)
+bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
+    using L = PipeCfg<NC, NS, MINB, TR, CAP>;
+    constexpr int LANES = KP / VEC;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * L::STAGE_BYTES);
+    uint64_t* empty = full + NS;
+    int* s_staged = reinterpret_cast<int*>(empty + NS);
+    double* s_C = reinterpret_cast<double*>(smem + NS * L::STAGE_BYTES + 64 * 8);
+    double* s_t = s_C + KP * KP;
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    if (tid == 0) {
+        for (int s = 0; s < NS; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    if (tid < NC) load_C<KP, HAS_C>(a, s_C, tid, NC);
+    __syncthreads();
+
+    if (warp == NC / 32) {
+        // ------------------------------------------------ producer warp
+        if ((tid & 31) == 0) {
+            const uint64_t pol = evict_first_policy();
+            int i = 0;
+            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+                const int s = i % NS;
+                if (i >= NS) mbar_wait(&empty[s], ((i / NS) - 1) & 1);
+                unsigned char* st = smem + s * L::STAGE_BYTES;
+                const int64_t r0 = a.row0 + (int64_t)tile * TR;
+                const int nr = (int)((a.row0 + a.nrows - r0) < TR ? (a.row0 + a.nrows - r0) : TR);
+                const int p0 = a.rp[r0], p1 = a.rp[r0 + nr];
+                const int64_t ra = r0 & ~(int64_t)3;
+                const uint32_t rp_bytes = (uint32_t)((((r0 - ra) + nr + 1 + 3) & ~3) * 4);
+                const bool staged = (p1 - p0) <= CAP;
+                const int pa = p0 & ~3;
+                const uint32_t n4 = (uint32_t)(((p0 - pa) + (p1 - p0) + 3) >> 2);
+                s_staged[s] = staged ? 1 : 0;
+                const uint32_t tx = rp_bytes + (staged && n4 ? n4 * 16u + n4 * 32u : 0u);
+                mbar_expect_tx(&full[s], tx);
+                bulk_g2s(st, a.rp + ra, rp_bytes, &full[s], pol);
+                if (staged && n4) {
+                    bulk_g2s(st + L::RP_BYTES, a.col + pa, n4 * 16u, &full[s], pol);
+                    bulk_g2s(st + L::RP_BYTES + L::COL_BYTES, a.val + pa, n4 * 32u, &full[s], pol);
+                }
+            }
+        }
+        return;
+    }
+    // ---------------------------------------------------- consumer warps
+    const int grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
+    const bool lane_in = c0 < a.k;
+    double* t_row = s_t + grp * (KP + 1);
+    int i = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i % NS;
+        mbar_wait(&full[s], (i / NS) & 1);
+        const unsigned char* st = smem + s * L::STAGE_BYTES;
+        const int64_t r0 = a.row0 + (int64_t)tile * TR;
+        const int nr = (int)((a.row0 + a.nrows - r0) < TR ? (a.row0 + a.nrows - r0) : TR);
+        const int roff = (int)(r0 & 3);
+        const int* s_rp = reinterpret_cast<const int*>(st) + roff;
+        const int p0 = s_rp[0];
+        const int off = p0 & 3;
+        const bool staged = s_staged[s] != 0;
+        if (staged) {
+            const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
+            const double* sval = reinterpret_cast<const double*>(st + L::RP_BYTES + L::COL_BYTES) + off - p0;
+            tile_rows<KP, VEC, HAS_C, NC, TR, PAIR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, t_row);
+        } else {
+            tile_rows<KP, VEC, HAS_C, NC, TR, PAIR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, t_row);
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(&empty[s]);
+    }
+}
+
+template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP, bool PAIR = false>
+void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
+    using L = PipeCfg<NC, NS, MINB, TR, CAP>;
+    const int64_t ntiles = (a.nrows + TR - 1) / TR;
+    const int smem = L::bytes(KP, NC / (KP / VEC), HAS_C);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr = true;
+    }
+    const int64_t cap = (int64_t)MINB * num_sms;
+    const int64_t grid = ntiles < cap ? ntiles : cap;
+    BK_KERNEL(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR><<<(unsigned)grid, NC + 32, smem, st>>>(a, (int)ntiles));
+}
+
+// ------------------------------------------------------------------ simple tile kernel (A/B variant)
+template <int KP, int VEC, bool HAS_C>
 __global__ void __launch_bounds__(kThreads)
 bspmm_tile_kernel(const SpmmArgs a) {
     constexpr int LANES = KP / VEC;
-    constexpr int RPP = kThreads / LANES;       // rows per pass
+    constexpr int RPP = kThreads / LANES;
     constexpr int PASSES = kTileRows / RPP;
     __shared__ int32_t s_rp[kTileRows + 1];
-    __shared__ __align__(16) int32_t s_col[kCap + 4];
-    __shared__ __align__(16) double s_val[kCap + 4];
+    __shared__ __align__(16) int32_t s_col[kCap + 8];
+    __shared__ __align__(16) double s_val[kCap + 8];
     __shared__ double s_C[HAS_C ? KP * KP : 1];
     __shared__ double s_t[HAS_C ? RPP * (KP + 1) : 1];
-
-    const int tid = threadIdx.x;
-    const int grp = tid / LANES;
-    const int lane = tid % LANES;
-    const int c0 = lane * VEC;
-    const int k = a.k;
-    const int kout = a.kout;
-
-    if (HAS_C) {
-        for (int i = tid; i < KP * KP; i += kThreads) {
-            int r = i / KP, c = i % KP;
-            s_C[i] = (r < k && c < kout) ? a.C[r * kout + c] : 0.0;
-        }
-    }
+    const int tid = threadIdx.x, grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
+    load_C<KP, HAS_C>(a, s_C, tid, kThreads);
     const int64_t tile0 = a.row0 + (int64_t)blockIdx.x * kTileRows;
     const int nr = (int)((a.row0 + a.nrows - tile0) < kTileRows ? (a.row0 + a.nrows - tile0) : kTileRows);
     for (int i = tid; i <= nr; i += kThreads) s_rp[i] = a.rp[tile0 + i];
@@ -89,12 +409,10 @@ bspmm_tile_kernel(const SpmmArgs a) {
     const int p0 = s_rp[0];
     const int nnz = s_rp[nr] - p0;
     const bool staged = nnz <= kCap;
-    // aligned start so that the 16-byte vector loads are legal (arrays are
-    // 256-byte aligned and padded by the library, see abi.cpp)
     const int pa = p0 & ~3;
     const int off = p0 - pa;
     if (staged) {
-        const int n4 = (off + nnz + 3) >> 2;           // int4 / 2x double2 chunks
+        const int n4 = (off + nnz + 3) >> 2;
         const int4* gc = reinterpret_cast<const int4*>(a.col + pa);
         const double2* gv = reinterpret_cast<const double2*>(a.val + pa);
         int4* sc = reinterpret_cast<int4*>(s_col);
@@ -106,103 +424,16 @@ bspmm_tile_kernel(const SpmmArgs a) {
         }
     }
     __syncthreads();
-
-    const bool lane_in = c0 < k;
-    for (int pass = 0; pass < PASSES; ++pass) {
-        const int r = pass * RPP + grp;
-        const bool active = r < nr;
-        double acc[VEC];
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
-        if (active) {
-            const int s = s_rp[r] - p0, e = s_rp[r + 1] - p0;
-            if (staged) {
-                const int* scol = s_col + off;
-                const double* sval = s_val + off;
-                int p = s;
-                for (; p + 1 < e; p += 2) {
-                    const int ca = scol[p], cb = scol[p + 1];
-                    const double va = sval[p], vb = sval[p + 1];
-                    const double* xa = (GHOST && ca >= a.ncol_local)
-                                           ? a.Xg + (int64_t)(ca - a.ncol_local) * a.ldg
-                                           : a.X + (int64_t)ca * a.ldx;
-                    const double* xb = (GHOST && cb >= a.ncol_local)
-                                           ? a.Xg + (int64_t)(cb - a.ncol_local) * a.ldg
-                                           : a.X + (int64_t)cb * a.ldx;
-                    if (lane_in) {
-                        double x0[VEC], x1[VEC];
-                        ld_x(xa + c0, x0);
-                        ld_x(xb + c0, x1);
-#pragma unroll
-                        for (int t = 0; t < VEC; ++t) acc[t] = fma(va, x0[t], acc[t]);
-#pragma unroll
-                        for (int t = 0; t < VEC; ++t) acc[t] = fma(vb, x1[t], acc[t]);
-                    }
-                }
-                if (p < e) {
-                    const int ca = scol[p];
-                    const double va = sval[p];
-                    const double* xa = (GHOST && ca >= a.ncol_local)
-                                           ? a.Xg + (int64_t)(ca - a.ncol_local) * a.ldg
-                                           : a.X + (int64_t)ca * a.ldx;
-                    if (lane_in) {
-                        double x0[VEC];
-                        ld_x(xa + c0, x0);
-#pragma unroll
-                        for (int t = 0; t < VEC; ++t) acc[t] = fma(va, x0[t], acc[t]);
-                    }
-                }
-            } else {
-                for (int p = s; p < e; ++p) {
-                    const int ca = __ldg(a.col + p0 + p);
-                    const double va = __ldg(a.val + p0 + p);
-                    const double* xa = (GHOST && ca >= a.ncol_local)
-                                           ? a.Xg + (int64_t)(ca - a.ncol_local) * a.ldg
-                                           : a.X + (int64_t)ca * a.ldx;
-                    if (lane_in) {
-                        double x0[VEC];
-                        ld_x(xa + c0, x0);
-#pragma unroll
-                        for (int t = 0; t < VEC; ++t) acc[t] = fma(va, x0[t], acc[t]);
-                    }
-                }
-            }
-        }
-        double out[VEC];
-        if (HAS_C) {
-            double* t_row = s_t + grp * (KP + 1);
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) t_row[c0 + t] = (c0 + t < k) ? acc[t] : 0.0;
-            __syncwarp();
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) out[t] = 0.0;
-            for (int c = 0; c < k; ++c) {
-                const double tv = t_row[c];
-#pragma unroll
-                for (int t = 0; t < VEC; ++t) out[t] = fma(tv, s_C[c * KP + c0 + t], out[t]);
-            }
-            __syncwarp();
-        } else {
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) out[t] = acc[t];
-        }
-        if (active && c0 < kout) {
-            double* yp = a.Y + (tile0 + r) * a.ldy + c0;
-            const int valid = min(VEC, kout - c0);
-            double v[VEC];
-            if (a.beta != 0.0) {
-#pragma unroll
-                for (int t = 0; t < VEC; ++t) v[t] = (t < valid) ? a.alpha * out[t] + a.beta * yp[t] : 0.0;
-            } else {
-#pragma unroll
-                for (int t = 0; t < VEC; ++t) v[t] = a.alpha * out[t];
-            }
-            st_y<VEC>(yp, v, valid);
-        }
-    }
+    const bool lane_in = c0 < a.k;
+    if (staged)
+        tile_rows<KP, VEC, HAS_C>(a, s_col + off - p0, s_val + off - p0, s_rp, nr, tile0, grp, c0, lane_in, s_C,
+                                  s_t + grp * (KP + 1));
+    else
+        tile_rows<KP, VEC, HAS_C>(a, a.col, a.val, s_rp, nr, tile0, grp, c0, lane_in, s_C, s_t + grp * (KP + 1));
 }
 
-// Explicit row list (boundary rows of a partitioned matrix): no staging.
+// ------------------------------------------------------------------ explicit row list
+// Boundary rows of a partitioned matrix (ghost columns): no staging.
 template <int KP, int VEC, bool HAS_C, bool GHOST>
 __global__ void __launch_bounds__(kThreads)
 bspmm_rows_kernel(const SpmmArgs a) {
@@ -211,70 +442,72 @@ bspmm_rows_kernel(const SpmmArgs a) {
     __shared__ double s_C[HAS_C ? KP * KP : 1];
     __shared__ double s_t[HAS_C ? RPP * (KP + 1) : 1];
     const int tid = threadIdx.x, grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
-    const int k = a.k, kout = a.kout;
-    if (HAS_C) {
-        for (int i = tid; i < KP * KP; i += kThreads) {
-            int r = i / KP, c = i % KP;
-            s_C[i] = (r < k && c < kout) ? a.C[r * kout + c] : 0.0;
-        }
-        __syncthreads();
-    }
+    load_C<KP, HAS_C>(a, s_C, tid, kThreads);
+    if (HAS_C) __syncthreads();
     const int64_t idx = (int64_t)blockIdx.x * RPP + grp;
     const bool active = idx < a.nrows;
     const int64_t row = active ? (a.rows ? (int64_t)a.rows[idx] : a.row0 + idx) : 0;
     double acc[VEC];
 #pragma unroll
     for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
-    if (active && c0 < k) {
-        for (int p = a.rp[row]; p < a.rp[row + 1]; ++p) {
-            const int ca = __ldg(a.col + p);
-            const double va = __ldg(a.val + p);
-            const double* xa = (GHOST && ca >= a.ncol_local) ? a.Xg + (int64_t)(ca - a.ncol_local) * a.ldg
-                                                             : a.X + (int64_t)ca * a.ldx;
-            double x0[VEC];
-            ld_x(xa + c0, x0);
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) acc[t] = fma(va, x0[t], acc[t]);
-        }
+    if (active) row_accumulate<VEC, GHOST>(a, a.col, a.val, a.rp[row], a.rp[row + 1], c0, c0 < a.k, acc);
+    row_epilogue<KP, VEC, HAS_C>(a, s_C, s_t + grp * (KP + 1), c0, active, row, acc);
+}
+
+// ------------------------------------------------------------------ dispatch
+int variant() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("BK_SPMM_KERNEL");
+        // default = 3 CTAs/SM x 8 consumer warps, 2 stages, 256-row tiles (A/B: tools/ab_spmm.sh)
+        v = 0;
+        const char* names[] = {"pipe", "tile", "pipe2x3", "pipe3x2", "pipe4x2", "pipe4x3t128", "pipe8x3t128n128",
+                               "pipe3x2n384", "pipe3x2pair", "pipe2x2pair"};
+        for (int i = 0; e && i < 10; ++i)
+            if (strcmp(e, names[i]) == 0) v = i;
     }
-    double out[VEC];
-    if (HAS_C) {
-        double* t_row = s_t + grp * (KP + 1);
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) t_row[c0 + t] = (c0 + t < k) ? acc[t] : 0.0;
-        __syncwarp();
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) out[t] = 0.0;
-        for (int c = 0; c < k; ++c) {
-            const double tv = t_row[c];
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) out[t] = fma(tv, s_C[c * KP + c0 + t], out[t]);
-        }
-    } else {
-#pragma unroll
-        for (int t = 0; t < VEC; ++t) out[t] = acc[t];
+    return v;
+}
+
+int num_sms_cached() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
     }
-    if (active && c0 < kout) {
-        double* yp = a.Y + row * a.ldy + c0;
-        const int valid = min(VEC, kout - c0);
-        double v[VEC];
-#pragma unroll
-        for (int t = 0; t < VEC; ++t)
-            v[t] = (t < valid) ? (a.beta != 0.0 ? a.alpha * out[t] + a.beta * yp[t] : a.alpha * out[t]) : 0.0;
-        st_y<VEC>(yp, v, valid);
-    }
+    return n;
 }
 
 template <int KP, int VEC, bool HAS_C, bool GHOST>
 void launch_t(const SpmmArgs& a, cudaStream_t st) {
     if (a.nrows <= 0) return;
-    if (a.rows) {
+    if (a.rows || GHOST) {
         constexpr int RPP = kThreads / (KP / VEC);
-        unsigned grid = (unsigned)((a.nrows + RPP - 1) / RPP);
+        const unsigned grid = (unsigned)((a.nrows + RPP - 1) / RPP);
         BK_KERNEL(bspmm_rows_kernel<KP, VEC, HAS_C, GHOST><<<grid, kThreads, 0, st>>>(a));
-    } else {
-        unsigned grid = (unsigned)((a.nrows + kTileRows - 1) / kTileRows);
-        BK_KERNEL(bspmm_tile_kernel<KP, VEC, HAS_C, GHOST><<<grid, kThreads, 0, st>>>(a));
+        return;
+    }
+    if constexpr (!GHOST) {
+        if constexpr (!HAS_C) {   // A/B variant (static smem: uncoupled apply only)
+            if (variant() == 1) {
+                const int64_t ntiles = (a.nrows + kTileRows - 1) / kTileRows;
+                BK_KERNEL(bspmm_tile_kernel<KP, VEC, false><<<(unsigned)ntiles, kThreads, 0, st>>>(a));
+                return;
+            }
+        }
+        const int ns = num_sms_cached();
+        switch (variant()) {
+            case 2: launch_pipe<KP, VEC, HAS_C, 256, 3, 2, 256, 2304>(a, ns, st); break;
+            case 4: launch_pipe<KP, VEC, HAS_C, 256, 2, 4, 256, 2048>(a, ns, st); break;
+            case 5: launch_pipe<KP, VEC, HAS_C, 256, 3, 4, 128, 1152>(a, ns, st); break;
+            case 6: launch_pipe<KP, VEC, HAS_C, 128, 3, 8, 128, 1152>(a, ns, st); break;
+            case 7: launch_pipe<KP, VEC, HAS_C, 384, 2, 3, 256, 2304>(a, ns, st); break;
+            case 8: launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304, true>(a, ns, st); break;
+            case 9: launch_pipe<KP, VEC, HAS_C, 256, 2, 2, 256, 2304, true>(a, ns, st); break;
+            default: launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304>(a, ns, st); break;
+        }
     }
 }
 
@@ -288,8 +521,27 @@ void launch_kv(const SpmmArgs& a, cudaStream_t st) {
     }
 }
 
+int max_vec() {
+    static int v = 0;
+    if (!v) {
+        const char* e = getenv("BK_SPMM_VEC");
+        v = e ? atoi(e) : 4;   // 4 columns per thread measured best (tools/ab_spmm.sh)
+        if (v != 2 && v != 4 && v != 8) v = 4;
+    }
+    return v;
+}
+
+// columns per thread: VEC = min(KP, max_vec()) when 16-byte vector access is legal
 template <int KP>
 void launch_k(const SpmmArgs& a, cudaStream_t st, bool vec2) {
+    // a lane's VEC columns must lie inside the row: k, k_out multiples of VEC
+    const int mv = max_vec();
+    if constexpr (KP >= 8) {
+        if (vec2 && mv >= 8 && a.k % 8 == 0 && a.kout % 8 == 0) return launch_kv<KP, 8>(a, st);
+    }
+    if constexpr (KP >= 4) {
+        if (vec2 && mv >= 4 && a.k % 4 == 0 && a.kout % 4 == 0) return launch_kv<KP, 4>(a, st);
+    }
     if constexpr (KP >= 2) {
         if (vec2) return launch_kv<KP, 2>(a, st);
     }

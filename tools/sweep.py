@@ -1,0 +1,65 @@
+"""Isolated kernel sweep (L2 flushed before every launch): bspmm / gram / update GB/s vs k.
+
+    python tools/sweep.py [--cfg c2] [--ks 1,2,4,8,16,32] [--ops spmm,gram,update] [--reps 7]
+Prints one JSON line per (op, k).  Used for A/B runs of kernel variants
+(env BK_SPMM_KERNEL=tile|pipe, BK_SPMM_VEC=2|4|8).
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+import paper_2504_02117_b200 as bk  # noqa: E402
+from paper_2504_02117_b200 import perfmodel as pm  # noqa: E402
+import synth  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cfg", default="c2")
+    ap.add_argument("--ks", default="1,2,4,8,16,32")
+    ap.add_argument("--ops", default="spmm")
+    ap.add_argument("--reps", type=int, default=7)
+    args = ap.parse_args()
+    peak = 6548.8
+    dev = torch.device("cuda", 0)
+    ctx = bk.Context(0)
+    A = synth.make_matrix(args.cfg, device=dev)
+    M = bk.Matrix.from_csr(ctx, A)
+    n, nnz = A.n_rows, A.nnz
+    flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    st = torch.cuda.current_stream()
+    tag = f"{os.environ.get('BK_SPMM_KERNEL', 'pipe')}/vec{os.environ.get('BK_SPMM_VEC', '8')}"
+    for k in [int(x) for x in args.ks.split(",")]:
+        X = synth.multivector(n, k, 3, device=dev)
+        Y = torch.empty_like(X)
+        C = synth.small_dense(k, k, 6, device=dev)
+        G = torch.empty(k, k, dtype=torch.float64, device=dev)
+        ops = {"spmm": (lambda: bk.bspmm_apply(ctx, M, X, Y), pm.spmm_bytes(n, nnz, k)),
+               "spmm_C": (lambda: bk.bspmm_apply(ctx, M, X, Y, C=C), pm.spmm_bytes(n, nnz, k)),
+               "gram": (lambda: bk.block_gram(ctx, X, Y, G), pm.gram_bytes(n, k, k)),
+               "update": (lambda: bk.block_update(ctx, Y, X, C, a=1.0, s=1e-3), pm.update_bytes(n, k, k))}
+        for op in args.ops.split(","):
+            fn, by = ops[op]
+            ts = []
+            for _ in range(args.reps):
+                flush.fill_(1.0)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                fn()
+                b.record(st)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            ms = statistics.median(ts[1:])
+            gbs = by / (ms * 1e-3) / 1e9
+            print(json.dumps({"tag": tag, "cfg": args.cfg, "op": op, "k": k, "us": round(ms * 1e3, 2),
+                              "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}))
+
+
+if __name__ == "__main__":
+    main()
