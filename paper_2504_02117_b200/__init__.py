@@ -18,7 +18,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libbk.so")
+LIB_PATH = os.environ.get("BK_LIB_PATH") or os.path.join(_HERE, "lib", "libbk.so")   # override: A/B builds only
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2504_02117_b200.build` "

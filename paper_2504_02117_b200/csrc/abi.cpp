@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <numeric>
@@ -163,6 +164,12 @@ extern "C" int bk_ctx_create(bk_ctx** out, int device, void* cuda_stream) {
     cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+    if (cudaMalloc(&c->d_tickets, 64 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(c->d_tickets, 0, 64 * sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return BK_ERR_CUDA;
+    }
     c->h_pinned_bytes = 1 << 20;
     if (cudaMallocHost(&c->h_pinned, c->h_pinned_bytes) != cudaSuccess) {
         cudaGetLastError();
@@ -199,6 +206,7 @@ extern "C" int bk_ctx_destroy(bk_ctx* ctx) {
     for (auto& b : ctx->ws)
         if (b.p) cudaFree(b.p);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+    if (ctx->d_tickets) cudaFree(ctx->d_tickets);
 #ifndef BK_NO_NCCL
     if (ctx->comm) ncclCommDestroy(ctx->comm);
 #endif
@@ -466,7 +474,20 @@ extern "C" int bspmm_apply(bk_ctx* ctx, const bk_csr* A, int k, const double* X,
 namespace bk {
 int gram_dev(bk_ctx* ctx, int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
              double* G, bool allreduce) {
-    if (n > 0) {
+    static int use_mma = -1;
+    if (use_mma < 0) {
+        const char* e = getenv("BK_GRAM");
+        use_mma = (e && strcmp(e, "fma") == 0) ? 0 : 1;
+    }
+    double* spart = nullptr;
+    if (n > 0 && use_stream_kernels())
+        spart = (double*)ws_get(ctx, WS_GRAM_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double));
+    if (spart && launch_gram_stream(n, ka, kb, X, ldx, Y, ldy, G, spart, ctx->d_tickets, ctx->num_sms, ctx->stream)) {
+        // TMA-staged DMMA Gram
+    } else if (n > 0 && use_mma && (ka >= 8 || kb >= 8)) {
+        double* part = (double*)ws_get(ctx, WS_GRAM_PART, gram_mma_ws_doubles(n, ka, kb, ctx->num_sms) * sizeof(double));
+        launch_gram_mma(n, ka, kb, X, ldx, Y, ldy, G, part, ctx->d_tickets, ctx->num_sms, ctx->stream);
+    } else if (n > 0) {
         double* part = (double*)ws_get(ctx, WS_GRAM_PART, gram_ws_doubles(n, ka, kb, ctx->num_sms) * sizeof(double));
         launch_gram(n, ka, kb, X, ldx, Y, ldy, G, part, ctx->num_sms, ctx->stream);
     } else {

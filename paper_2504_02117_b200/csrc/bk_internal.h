@@ -82,6 +82,21 @@ void launch_update(const UpdArgs& a, cudaStream_t st);
 size_t gram_ws_doubles(int64_t n, int ka, int kb, int num_sms);
 void launch_gram(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y,
                  int64_t ldy, double* G, double* partials, int num_sms, cudaStream_t st);
+// Same on the FP64 tensor cores (DMMA m8n8k4), one launch; `ticket` is a zeroed
+// device int (the last CTA reduces and resets it).
+size_t gram_mma_ws_doubles(int64_t n, int ka, int kb, int num_sms);
+void launch_gram_mma(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                     double* G, double* part, int* ticket, int num_sms, cudaStream_t st);
+// TMA-staged streaming versions (stream.cu); return false when not applicable
+// (strided / > 32-wide operands), the caller then uses the generic kernels.
+size_t stream_part_doubles(int num_sms);
+bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st);
+bool launch_gram_stream(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                        double* G, double* part, int* ticket, int num_sms, cudaStream_t st);
+bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                          const double* Y2, int64_t ldy2, double* d, double* d2, double* part, int* ticket,
+                          int num_sms, cudaStream_t st);
+bool use_stream_kernels();
 // d[c] = sum_i X[i,c] Y[i,c] for c < k (and optionally d2 with Y2); deterministic.
 size_t coldot_ws_doubles(int64_t n, int k, int num_sms);
 void launch_coldot(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,
@@ -142,6 +157,7 @@ struct bk_ctx {
     std::string last_error;
     std::vector<bk_buf> ws;       // slot-indexed grow-only device workspaces
     double* h_pinned = nullptr;   // pinned host staging for small results
+    int* d_tickets = nullptr;     // zeroed device counters for last-CTA reductions
     size_t h_pinned_bytes = 0;
     int nranks = 1, rank = 0;
 #ifndef BK_NO_NCCL

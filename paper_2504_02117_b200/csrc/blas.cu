@@ -365,8 +365,24 @@ void launch_coldot(int64_t n, int k, const double* X, int64_t ldx, const double*
     }
 }
 
+bool use_stream_kernels() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("BK_STREAM");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
 void launch_update(const UpdArgs& a, cudaStream_t st) {
     if (a.n <= 0) return;
+    static int nsm = 0;
+    if (!nsm) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    }
+    if (use_stream_kernels() && launch_update_stream(a, nsm, st)) return;
     const int kp = pow2_at_least(a.k);
     switch (kp) {
         case 1: return update_k<1>(a, st);

@@ -69,7 +69,13 @@ struct Solver {
                double* d, double* d2) {
         rep->n_gram++;
         double* part = (double*)ws_get(ctx, WS_COLDOT_PART, coldot_ws_doubles(n, k, ctx->num_sms) * sizeof(double));
-        if (n > 0) {
+        double* spart = use_stream_kernels()
+                            ? (double*)ws_get(ctx, WS_COLDOT_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double))
+                            : nullptr;
+        if (n > 0 && spart &&
+            launch_coldot_stream(n, k, X, ldx, Y, ldy, Y2, ldy2, d, d2, spart, ctx->d_tickets + 32, ctx->num_sms, st)) {
+            // TMA-staged column dots
+        } else if (n > 0) {
             launch_coldot(n, k, X, ldx, Y, ldy, Y2, ldy2, d, d2, part, ctx->num_sms, st);
         } else {
             cudaMemsetAsync(d, 0, sizeof(double) * k, st);

@@ -1,0 +1,759 @@
+// stream.cu -- TMA-staged streaming kernels for the N x k passes of the block
+// Krylov iteration (a3 Gram, a5 update, column dots) on sm_100a.
+//
+// The block vectors are row-major with ld == width, so a tile of T rows of
+// each operand is ONE contiguous range: a producer warp moves it HBM -> shared
+// memory with a single cp.async.bulk per operand (mbarrier complete_tx, 2-stage
+// ring, persistent grid of 2 CTAs per SM), which keeps ~100 KB per SM in
+// flight -- the memory-level parallelism the plain per-thread loads lacked
+// (profiles/).  Eight consumer warps compute from shared memory:
+//   update : out = a Xin + s P C + w W          (C in shared memory, FMA)
+//   gram   : G  = X^T Y  on the FP64 tensor cores (mma.sync m8n8k4, DMMA),
+//            per-CTA partial + last-CTA fixed-order reduction (deterministic)
+//   coldot : d_c = sum_r X[r,c] Y[r,c] (+ d2 with Y2), same reduction scheme.
+// Tiles whose byte count is not a multiple of 16 (only a ragged last tile can
+// be) are read directly from global memory by the consumers.
+#include "bk_internal.h"
+
+#ifndef BK_STREAM_NSTAGE
+#define BK_STREAM_NSTAGE 2
+#endif
+#ifndef BK_STREAM_STAGE_KB
+#define BK_STREAM_STAGE_KB 48
+#endif
+
+namespace bk {
+namespace {
+
+constexpr int NC = 256;            // consumer threads
+constexpr int NSTAGE = BK_STREAM_NSTAGE;
+constexpr int STAGE_BYTES = BK_STREAM_STAGE_KB * 1024;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try(bar, parity)) {
+    }
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+// Up to 3 contiguous row-major operands streamed tile by tile.
+struct Streams {
+    const double* p[3];
+    int w[3];        // doubles per row (0 = unused)
+    int off[3];      // byte offset of the operand inside a stage
+    int nin;
+    int T;           // rows per tile
+    int64_t n;
+    int ntiles;
+};
+
+__device__ __forceinline__ void stream_setup(uint64_t* full, uint64_t* empty) {
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NSTAGE; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+}
+
+// producer warp, lane 0: returns after the last tile is issued
+__device__ __forceinline__ void stream_produce(const Streams& S, unsigned char* smem, uint64_t* full, uint64_t* empty,
+                                               int* s_direct) {
+    const uint64_t pol = evict_first_policy();
+    int i = 0;
+    for (int tile = blockIdx.x; tile < S.ntiles; tile += gridDim.x, ++i) {
+        const int s = i % NSTAGE;
+        if (i >= NSTAGE) mbar_wait(&empty[s], ((i / NSTAGE) - 1) & 1);
+        const int64_t r0 = (int64_t)tile * S.T;
+        const int nr = (int)((S.n - r0) < S.T ? (S.n - r0) : S.T);
+        bool ok = true;
+        uint32_t tx = 0;
+        for (int j = 0; j < S.nin; ++j) {
+            const uint32_t b = (uint32_t)nr * S.w[j] * 8u;
+            if ((b & 15u) || (((uintptr_t)(S.p[j] + r0 * S.w[j])) & 15u)) ok = false;
+            tx += b;
+        }
+        s_direct[s] = ok ? 0 : 1;
+        mbar_expect_tx(&full[s], ok ? tx : 0u);
+        if (ok) {
+            unsigned char* st = smem + s * STAGE_BYTES;
+            for (int j = 0; j < S.nin; ++j)
+                if (S.w[j] > 0)
+                    bulk_g2s(st + S.off[j], S.p[j] + r0 * S.w[j], (uint32_t)nr * S.w[j] * 8u, &full[s], pol);
+        }
+    }
+}
+
+// ------------------------------------------------------------------ update
+// out[r, c] = a Xin[r, c] + s sum_q P[r, q] C[q, c] + wv W[r, c];  P, Xin, W contiguous.
+struct UpdStream {
+    Streams S;          // 0 = P (kp), 1 = Xin (k, if a != 0), 2 = W (k, if present)
+    int iX, iW;         // stream index of Xin / W, -1 if absent
+    int kp, k, cw;      // cw = columns per thread (1, 2 or 4)
+    double a, s, w_host;
+    const double* w_dev;
+    const double* C;    // kp x k
+    double* out;
+    const int* halt;
+};
+
+template <int CW>
+__device__ __forceinline__ void upd_tile(const UpdStream& U, const double* Pt, const double* Xt, const double* Wt,
+                                         const double* sC, int nr, int64_t r0, double wv) {
+    const int k = U.k, kp = U.kp;
+    const int tpr = k / CW;
+    for (int idx = threadIdx.x; idx < nr * tpr; idx += NC) {
+        const int r = idx / tpr, cb = (idx - r * tpr) * CW;
+        double acc[CW];
+#pragma unroll
+        for (int j = 0; j < CW; ++j) acc[j] = 0.0;
+        const double* pr = Pt + (int64_t)r * kp;
+        for (int q = 0; q < kp; ++q) {
+            const double p = pr[q];
+#pragma unroll
+            for (int j = 0; j < CW; ++j) acc[j] = fma(p, sC[q * k + cb + j], acc[j]);
+        }
+        double o[CW];
+#pragma unroll
+        for (int j = 0; j < CW; ++j) {
+            double v = U.s * acc[j];
+            if (Xt) v = fma(U.a, Xt[(int64_t)r * k + cb + j], v);
+            if (Wt) v = fma(wv, Wt[(int64_t)r * k + cb + j], v);
+            o[j] = v;
+        }
+        double* op = U.out + (r0 + r) * k + cb;
+        if (CW == 4) {
+            reinterpret_cast<double2*>(op)[0] = make_double2(o[0], o[1]);
+            reinterpret_cast<double2*>(op)[1] = make_double2(o[2], o[3]);
+        } else if (CW == 2) {
+            reinterpret_cast<double2*>(op)[0] = make_double2(o[0], o[1]);
+        } else {
+            op[0] = o[0];
+        }
+    }
+}
+
+// Tensor-core tile: out(8-row block) = a X + w W + P (s C), P (8 x kp) as A
+// fragments (m8n8k4: lane holds P[row 4g+.., q]), s C as B fragments held in
+// registers for the whole kernel.  Needs k % 8 == 0 and kp % 4 == 0.
+template <int NQ, int NK>
+__device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* Pt, const double* Xt, const double* Wt,
+                                             const double (&bf)[NQ][NK], int nr, int64_t r0, double wv) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, mg = lane >> 2;
+    const int k = U.k, kp = U.kp;
+    for (int rb = 8 * warp; rb < nr; rb += 8 * (NC / 32)) {
+        const int r = rb + mg;
+        const bool rin = r < nr;
+        double af[NQ];
+#pragma unroll
+        for (int ks = 0; ks < NQ; ++ks) af[ks] = rin ? Pt[(int64_t)r * kp + 4 * ks + kq] : 0.0;
+#pragma unroll
+        for (int nb = 0; nb < NK; ++nb) {
+            const int c = 8 * nb + 2 * kq;
+            double d0 = 0.0, d1 = 0.0;
+            if (rin && Xt) {
+                const double2 x = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
+                d0 = U.a * x.x;
+                d1 = U.a * x.y;
+            }
+            if (rin && Wt) {
+                const double2 w = *reinterpret_cast<const double2*>(Wt + (int64_t)r * k + c);
+                d0 = fma(wv, w.x, d0);
+                d1 = fma(wv, w.y, d1);
+            }
+            // D(row = mg, cols 2kq, 2kq+1): the accumulator layout of m8n8k4
+#pragma unroll
+            for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], bf[ks][nb]);
+            if (rin) *reinterpret_cast<double2*>(U.out + (r0 + r) * k + c) = make_double2(d0, d1);
+        }
+    }
+}
+
+template <int NQ, int NK>
+__global__ void __launch_bounds__(NC + 32, 2) upd_stream_mma_kernel(const UpdStream U) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    if (U.halt && *U.halt) return;
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(U.S, smem, full, empty, s_direct);
+        return;
+    }
+    // B fragments of s C: lane holds (sC)[4 ks + kq][8 nb + mg]
+    double bf[NQ][NK];
+#pragma unroll
+    for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+        for (int nb = 0; nb < NK; ++nb) bf[ks][nb] = U.s * U.C[(4 * ks + (lane & 3)) * U.k + 8 * nb + (lane >> 2)];
+    const double wv = U.iW >= 0 ? (U.w_dev ? U.w_host * *U.w_dev : U.w_host) : 0.0;
+    int i = 0;
+    for (int tile = blockIdx.x; tile < U.S.ntiles; tile += gridDim.x, ++i) {
+        const int s = i % NSTAGE;
+        mbar_wait(&full[s], (i / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * U.S.T;
+        const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
+        if (!s_direct[s]) {
+            const unsigned char* st = smem + s * STAGE_BYTES;
+            const double* Pt = reinterpret_cast<const double*>(st + U.S.off[0]);
+            const double* Xt = U.iX >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iX]) : nullptr;
+            const double* Wt = U.iW >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iW]) : nullptr;
+            upd_tile_mma<NQ, NK>(U, Pt, Xt, Wt, bf, nr, r0, wv);
+        } else {
+            const double* Pt = U.S.p[0] + r0 * U.kp;
+            const double* Xt = U.iX >= 0 ? U.S.p[U.iX] + r0 * U.k : nullptr;
+            const double* Wt = U.iW >= 0 ? U.S.p[U.iW] + r0 * U.k : nullptr;
+            upd_tile_mma<NQ, NK>(U, Pt, Xt, Wt, bf, nr, r0, wv);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
+template <int CW>
+__global__ void __launch_bounds__(NC + 32, 2) upd_stream_kernel(const UpdStream U) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    double* sC = reinterpret_cast<double*>(smem + NSTAGE * STAGE_BYTES + 128);
+    if (U.halt && *U.halt) return;
+    stream_setup(full, empty);
+    for (int i = threadIdx.x; i < U.kp * U.k; i += blockDim.x) sC[i] = U.C[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5;
+    if (warp == NC / 32) {
+        if ((threadIdx.x & 31) == 0) stream_produce(U.S, smem, full, empty, s_direct);
+        return;
+    }
+    const double wv = U.iW >= 0 ? (U.w_dev ? U.w_host * *U.w_dev : U.w_host) : 0.0;
+    int i = 0;
+    for (int tile = blockIdx.x; tile < U.S.ntiles; tile += gridDim.x, ++i) {
+        const int s = i % NSTAGE;
+        mbar_wait(&full[s], (i / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * U.S.T;
+        const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
+        if (!s_direct[s]) {
+            const unsigned char* st = smem + s * STAGE_BYTES;
+            const double* Pt = reinterpret_cast<const double*>(st + U.S.off[0]);
+            const double* Xt = U.iX >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iX]) : nullptr;
+            const double* Wt = U.iW >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iW]) : nullptr;
+            upd_tile<CW>(U, Pt, Xt, Wt, sC, nr, r0, wv);
+        } else {
+            const double* Pt = U.S.p[0] + r0 * U.kp;
+            const double* Xt = U.iX >= 0 ? U.S.p[U.iX] + r0 * U.k : nullptr;
+            const double* Wt = U.iW >= 0 ? U.S.p[U.iW] + r0 * U.k : nullptr;
+            upd_tile<CW>(U, Pt, Xt, Wt, sC, nr, r0, wv);
+        }
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+    }
+}
+
+// ------------------------------------------------------------------ gram (DMMA) / coldot
+struct GramStream {
+    Streams S;          // 0 = X (ka), 1 = Y (kb) (absent when X == Y), 2 = Y2 for coldot
+    int ka, kb;
+    int same;           // Y == X
+    double* part;       // [gridDim.x][NOUT]
+    int* ticket;
+    double* G;          // gram: ka x kb; coldot: d[k]
+    double* G2;         // coldot second output
+};
+
+// NSET independent accumulator sets (quads alternate between them) so the
+// DMMA accumulation is not one long dependent chain per warp.
+template <int NA, int NB>
+struct GramSets { static constexpr int NSET = (NA * NB <= 4) ? 4 : ((NA * NB <= 9) ? 2 : 1); };
+
+template <int NA, int NB>
+__device__ __forceinline__ void gram_tile(const GramStream& Gs, const double* Xt, const double* Yt, int nr,
+                                          double (&acc)[GramSets<NA, NB>::NSET][NA][NB][2]) {
+    constexpr int NSET = GramSets<NA, NB>::NSET;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, mg = lane >> 2;
+    const int ka = Gs.ka, kb = Gs.kb;
+    for (int q0 = 4 * warp; q0 < nr; q0 += 4 * (NC / 32) * NSET) {
+        double av[NSET][NA], bv[NSET][NB];
+#pragma unroll
+        for (int s = 0; s < NSET; ++s) {
+            const int r = q0 + 4 * (NC / 32) * s + kq;
+            const bool rin = r < nr;
+#pragma unroll
+            for (int i = 0; i < NA; ++i) av[s][i] = (rin && 8 * i + mg < ka) ? Xt[(int64_t)r * ka + 8 * i + mg] : 0.0;
+#pragma unroll
+            for (int j = 0; j < NB; ++j) bv[s][j] = (rin && 8 * j + mg < kb) ? Yt[(int64_t)r * kb + 8 * j + mg] : 0.0;
+        }
+#pragma unroll
+        for (int s = 0; s < NSET; ++s)
+#pragma unroll
+            for (int i = 0; i < NA; ++i)
+#pragma unroll
+                for (int j = 0; j < NB; ++j) dmma(acc[s][i][j][0], acc[s][i][j][1], av[s][i], bv[s][j]);
+    }
+}
+
+// fixed-order cross-warp combine -> CTA partial -> last CTA sums partials in order
+template <int NOUT>
+__device__ __forceinline__ void finish_reduce(const GramStream& Gs, double* s_red, int nout_real, int kb_real,
+                                              int ld_out, bool coldot) {
+    __shared__ int s_last;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __syncwarp();
+    // (caller has written s_red[warp * NOUT + o])
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    double* out = Gs.part + (int64_t)blockIdx.x * NOUT;
+    for (int o = tid; o < NOUT; o += NC) {
+        double s = 0.0;
+#pragma unroll
+        for (int w = 0; w < NC / 32; ++w) s += s_red[w * NOUT + o];
+        out[o] = s;
+    }
+    // two-level fixed-order tree: the last CTA of each group of RG CTAs sums its
+    // group's partials, the last group reducer sums the group results.  Every
+    // sum has <= RG terms loaded in one batch (one L2 round trip per level).
+    constexpr int RG = 16;
+    const int nblk = gridDim.x;
+    const int ngrp = (nblk + RG - 1) / RG;
+    const int g = blockIdx.x / RG;
+    const int gsz = (nblk - g * RG) < RG ? (nblk - g * RG) : RG;
+    double* P2 = Gs.part + (int64_t)nblk * NOUT;
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    if (tid == 0) s_last = (atomicAdd(Gs.ticket + 1 + g, 1) == gsz - 1);
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    if (!s_last) return;
+    __threadfence();
+    for (int o = tid; o < NOUT; o += NC) {
+        double v[RG];
+#pragma unroll
+        for (int b = 0; b < RG; ++b) v[b] = b < gsz ? __ldcg(Gs.part + (int64_t)(g * RG + b) * NOUT + o) : 0.0;
+        double s = v[0];
+#pragma unroll
+        for (int b = 1; b < RG; ++b) s += v[b];
+        P2[(int64_t)g * NOUT + o] = s;
+    }
+    if (tid == 0) Gs.ticket[1 + g] = 0;
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    if (tid == 0) s_last = (atomicAdd(Gs.ticket, 1) == ngrp - 1);
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    if (!s_last) return;
+    __threadfence();
+    for (int o = tid; o < nout_real; o += NC) {
+        int idx, dst;
+        double* G;
+        if (coldot) {
+            const int which = o / kb_real, c = o % kb_real;
+            idx = which * 32 + c;
+            dst = c;
+            G = which ? Gs.G2 : Gs.G;
+        } else {
+            const int a = o / kb_real, b = o % kb_real;
+            idx = a * ld_out + b;
+            dst = a * kb_real + b;
+            G = Gs.G;
+        }
+        constexpr int MAXG = 32;   // up to 512 CTAs
+        double v[MAXG];
+#pragma unroll
+        for (int q = 0; q < MAXG; ++q) v[q] = q < ngrp ? __ldcg(P2 + (int64_t)q * NOUT + idx) : 0.0;
+        double s = v[0];
+#pragma unroll
+        for (int q = 1; q < MAXG; ++q) s += v[q];
+        G[dst] = s;
+    }
+    if (tid == 0) *Gs.ticket = 0;
+    (void)lane;
+    (void)warp;
+}
+
+template <int NA, int NB>
+__global__ void __launch_bounds__(NC + 32, 2) gram_stream_kernel(const GramStream Gs) {
+    constexpr int KAP = 8 * NA, KBP = 8 * NB, NOUT = KAP * KBP;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    double* s_red = reinterpret_cast<double*>(smem + NSTAGE * STAGE_BYTES + 128);
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(Gs.S, smem, full, empty, s_direct);
+        return;
+    }
+    constexpr int NSET = GramSets<NA, NB>::NSET;
+    double acc[NSET][NA][NB][2];
+#pragma unroll
+    for (int s = 0; s < NSET; ++s)
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) acc[s][i][j][0] = acc[s][i][j][1] = 0.0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < Gs.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * Gs.S.T;
+        const int nr = (int)((Gs.S.n - r0) < Gs.S.T ? (Gs.S.n - r0) : Gs.S.T);
+        if (!s_direct[s]) {
+            const unsigned char* st = smem + s * STAGE_BYTES;
+            const double* Xt = reinterpret_cast<const double*>(st + Gs.S.off[0]);
+            const double* Yt = Gs.same ? Xt : reinterpret_cast<const double*>(st + Gs.S.off[1]);
+            gram_tile<NA, NB>(Gs, Xt, Yt, nr, acc);
+        } else {
+            const double* Xt = Gs.S.p[0] + r0 * Gs.ka;
+            const double* Yt = (Gs.same ? Gs.S.p[0] : Gs.S.p[1]) + r0 * Gs.kb;
+            gram_tile<NA, NB>(Gs, Xt, Yt, nr, acc);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // every issued bulk copy has completed (each was waited on), so once all
+    // consumer warps are past the loop the ring memory is reused for the combine
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    s_red = reinterpret_cast<double*>(smem);
+    const int kq = lane & 3, mg = lane >> 2;
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + 8 * j + 2 * kq;
+            double v0 = acc[0][i][j][0], v1 = acc[0][i][j][1];
+#pragma unroll
+            for (int s = 1; s < NSET; ++s) { v0 += acc[s][i][j][0]; v1 += acc[s][i][j][1]; }   // fixed order
+            d[0] = v0;
+            d[1] = v1;
+        }
+    finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb, Gs.kb, KBP, false);
+}
+
+// ka, kb <= 4: FMA consumer (an 8 x 8 DMMA block would waste most lanes).
+// Thread t walks rows t, t + NC, ... of each tile; fixed-order shuffle tree per
+// warp, then the common CTA / grid reduction.
+__global__ void __launch_bounds__(NC + 32, 2) gram_small_stream_kernel(const GramStream Gs) {
+    constexpr int NOUT = 16;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(Gs.S, smem, full, empty, s_direct);
+        return;
+    }
+    const int ka = Gs.ka, kb = Gs.kb;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < Gs.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * Gs.S.T;
+        const int nr = (int)((Gs.S.n - r0) < Gs.S.T ? (Gs.S.n - r0) : Gs.S.T);
+        const unsigned char* st = smem + s * STAGE_BYTES;
+        const bool dir = s_direct[s] != 0;
+        const double* Xt = dir ? Gs.S.p[0] + r0 * ka : reinterpret_cast<const double*>(st + Gs.S.off[0]);
+        const double* Yt = Gs.same ? Xt : (dir ? Gs.S.p[1] + r0 * kb : reinterpret_cast<const double*>(st + Gs.S.off[1]));
+        for (int r = threadIdx.x; r < nr; r += NC) {
+            double x[4], y[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) x[a] = a < ka ? Xt[(int64_t)r * ka + a] : 0.0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) y[b] = b < kb ? Yt[(int64_t)r * kb + b] : 0.0;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a][b] = fma(x[a], y[b], acc[a][b]);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    double* s_red = reinterpret_cast<double*>(smem);
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            double v = acc[a][b];
+#pragma unroll
+            for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+            if (lane == 0) s_red[warp * NOUT + a * 4 + b] = v;
+        }
+    finish_reduce<NOUT>(Gs, s_red, ka * kb, kb, 4, false);
+}
+
+// coldot: d_c = sum_r X[r,c] Y[r,c], d2_c with Y2 (X, Y, Y2 all k wide)
+__global__ void __launch_bounds__(NC + 32, 2) coldot_stream_kernel(const GramStream Gs) {
+    constexpr int NOUT = 64;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    double* s_red = reinterpret_cast<double*>(smem + NSTAGE * STAGE_BYTES + 128);
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(Gs.S, smem, full, empty, s_direct);
+        return;
+    }
+    const int k = Gs.ka;
+    const bool two = Gs.G2 != nullptr;
+    // k | 32: flattened walk over the tile's nr*k elements, thread t always sees
+    // column t % k (all lanes busy, conflict-free); otherwise lane = column.
+    const bool flat = (32 % k) == 0;
+    const int c = flat ? (lane % k) : lane;
+    double d1 = 0.0, d2 = 0.0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < Gs.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * Gs.S.T;
+        const int nr = (int)((Gs.S.n - r0) < Gs.S.T ? (Gs.S.n - r0) : Gs.S.T);
+        const unsigned char* st = smem + s * STAGE_BYTES;
+        const bool dir = s_direct[s] != 0;
+        const double* Xt = dir ? Gs.S.p[0] + r0 * k : reinterpret_cast<const double*>(st + Gs.S.off[0]);
+        const double* Yt = Gs.same ? Xt : (dir ? Gs.S.p[1] + r0 * k : reinterpret_cast<const double*>(st + Gs.S.off[1]));
+        const double* Y2t = two ? (dir ? Gs.S.p[2] + r0 * k : reinterpret_cast<const double*>(st + Gs.S.off[2])) : nullptr;
+        if (flat) {
+            const int ne = nr * k;
+            for (int e = threadIdx.x; e < ne; e += NC) {
+                const double x = Xt[e];
+                d1 = fma(x, Yt[e], d1);
+                if (two) d2 = fma(x, Y2t[e], d2);
+            }
+        } else if (c < k) {
+            for (int r = warp; r < nr; r += NC / 32) {
+                const double x = Xt[(int64_t)r * k + c];
+                d1 = fma(x, Yt[(int64_t)r * k + c], d1);
+                if (two) d2 = fma(x, Y2t[(int64_t)r * k + c], d2);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (flat) {   // lanes l, l + k, l + 2k, ... share a column: fixed xor tree
+        for (int m = 16; m >= k; m >>= 1) {
+            d1 += __shfl_xor_sync(0xffffffffu, d1, m);
+            d2 += __shfl_xor_sync(0xffffffffu, d2, m);
+        }
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    s_red = reinterpret_cast<double*>(smem);
+    if (!flat || lane < k) {
+        s_red[warp * NOUT + lane] = d1;
+        s_red[warp * NOUT + 32 + lane] = d2;
+    }
+    finish_reduce<NOUT>(Gs, s_red, (two ? 2 : 1) * k, k, 32, true);
+}
+
+int grid_for(int ntiles, int num_sms) { return ntiles < 2 * num_sms ? ntiles : 2 * num_sms; }
+
+int tile_rows_for(int bytes_per_row) {
+    int T = STAGE_BYTES / (bytes_per_row > 0 ? bytes_per_row : 8);
+    T &= ~7;  // multiple of 8 rows keeps every full tile 16-byte sized and aligned
+    if (T > 1024) T = 1024;
+    return T < 8 ? 8 : T;
+}
+
+void set_smem(const void* fn, int bytes) { cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes); }
+
+template <int NA, int NB>
+void gram_stream_t(const GramStream& Gs, int grid, cudaStream_t st) {
+    static_assert((NC / 32) * 64 * NA * NB * 8 <= NSTAGE * STAGE_BYTES, "combine buffer must fit in the ring");
+    const int smem = NSTAGE * STAGE_BYTES + 128;
+    static bool a = false;
+    if (!a) { set_smem((const void*)gram_stream_kernel<NA, NB>, smem); a = true; }
+    BK_KERNEL(gram_stream_kernel<NA, NB><<<grid, NC + 32, smem, st>>>(Gs));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ launchers (return false = not applicable)
+// CTA partials + group partials (<= 32 groups of 16), NOUT <= 1024 each
+size_t stream_part_doubles(int num_sms) { return (size_t)(2 * num_sms + 40) * 1024; }
+
+bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
+    // contiguous operands only, kp and k <= 32, out not aliasing P/Xin/W rows in other tiles is fine
+    if (u.kp < 1 || u.kp > 32 || u.k > 32 || u.ldp != u.kp || u.ldo != u.k) return false;
+    if ((const double*)u.out == u.P) return false;   // in-place X <- X C: rows are read whole first (blas.cu)
+    if (u.a != 0.0 && (u.ldxin != u.k || !u.Xin)) return false;
+    if (u.W && u.ldw != u.k) return false;
+    if (((uintptr_t)u.out & 15) || ((uintptr_t)u.P & 15)) return false;
+    const int cw = (u.k % 4 == 0) ? 4 : ((u.k % 2 == 0) ? 2 : 1);
+    UpdStream U{};
+    int nin = 0;
+    U.S.p[nin] = u.P; U.S.w[nin] = u.kp; ++nin;
+    U.iX = -1; U.iW = -1;
+    if (u.a != 0.0) { U.iX = nin; U.S.p[nin] = u.Xin; U.S.w[nin] = u.k; ++nin; }
+    if (u.W) { U.iW = nin; U.S.p[nin] = u.W; U.S.w[nin] = u.k; ++nin; }
+    int bpr = 0;
+    for (int j = 0; j < nin; ++j) bpr += U.S.w[j] * 8;
+    U.S.nin = nin;
+    U.S.T = tile_rows_for(bpr);
+    int off = 0;
+    for (int j = 0; j < nin; ++j) { U.S.off[j] = off; off += U.S.T * U.S.w[j] * 8; off = (off + 127) & ~127; }
+    if (off > STAGE_BYTES) { U.S.T /= 2; U.S.T &= ~7; off = 0;
+        for (int j = 0; j < nin; ++j) { U.S.off[j] = off; off += U.S.T * U.S.w[j] * 8; off = (off + 127) & ~127; } }
+    U.S.n = u.n;
+    U.S.ntiles = (int)((u.n + U.S.T - 1) / U.S.T);
+    U.kp = u.kp; U.k = u.k; U.cw = cw;
+    U.a = u.a; U.s = u.s; U.w_host = u.w_host; U.w_dev = u.w_dev;
+    U.C = u.C; U.out = u.out; U.halt = u.halt;
+    const int smem = NSTAGE * STAGE_BYTES + 128 + 32 * 32 * 8;
+    const int grid = grid_for(U.S.ntiles, num_sms);
+    if (grid <= 0) return true;
+    static int mma = -1;
+    if (mma < 0) {
+        const char* e = getenv("BK_UPD");
+        mma = (e && strcmp(e, "fma") == 0) ? 0 : 1;
+    }
+    if (mma && u.k % 8 == 0 && u.kp % 4 == 0) {
+        const int nq = u.kp / 4, nk = u.k / 8;
+#define BK_UM(Q, K)                                                                            \
+    if (nq == Q && nk == K) {                                                                  \
+        static bool at = false;                                                                \
+        if (!at) { set_smem((const void*)upd_stream_mma_kernel<Q, K>, smem); at = true; }       \
+        BK_KERNEL(upd_stream_mma_kernel<Q, K><<<grid, NC + 32, smem, st>>>(U));                 \
+        return true;                                                                           \
+    }
+        BK_UM(1, 1) BK_UM(2, 1) BK_UM(3, 1) BK_UM(4, 1) BK_UM(5, 1) BK_UM(6, 1) BK_UM(7, 1) BK_UM(8, 1)
+        BK_UM(1, 2) BK_UM(2, 2) BK_UM(3, 2) BK_UM(4, 2) BK_UM(5, 2) BK_UM(6, 2) BK_UM(7, 2) BK_UM(8, 2)
+        BK_UM(1, 3) BK_UM(2, 3) BK_UM(3, 3) BK_UM(4, 3) BK_UM(5, 3) BK_UM(6, 3) BK_UM(7, 3) BK_UM(8, 3)
+        BK_UM(1, 4) BK_UM(2, 4) BK_UM(3, 4) BK_UM(4, 4) BK_UM(5, 4) BK_UM(6, 4) BK_UM(7, 4) BK_UM(8, 4)
+#undef BK_UM
+    }
+    static bool a1 = false, a2 = false, a4 = false;
+    if (cw == 4) {
+        if (!a4) { set_smem((const void*)upd_stream_kernel<4>, smem); a4 = true; }
+        BK_KERNEL(upd_stream_kernel<4><<<grid, NC + 32, smem, st>>>(U));
+    } else if (cw == 2) {
+        if (!a2) { set_smem((const void*)upd_stream_kernel<2>, smem); a2 = true; }
+        BK_KERNEL(upd_stream_kernel<2><<<grid, NC + 32, smem, st>>>(U));
+    } else {
+        if (!a1) { set_smem((const void*)upd_stream_kernel<1>, smem); a1 = true; }
+        BK_KERNEL(upd_stream_kernel<1><<<grid, NC + 32, smem, st>>>(U));
+    }
+    return true;
+}
+
+bool launch_gram_stream(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                        double* G, double* part, int* ticket, int num_sms, cudaStream_t st) {
+    if (ka > 32 || kb > 32 || ldx != ka || ldy != kb || n <= 0) return false;
+    if (((uintptr_t)X & 15) || ((uintptr_t)Y & 15)) return false;
+    GramStream Gs{};
+    Gs.same = (X == Y && ka == kb) ? 1 : 0;
+    int nin = 0;
+    Gs.S.p[nin] = X; Gs.S.w[nin] = ka; ++nin;
+    if (!Gs.same) { Gs.S.p[nin] = Y; Gs.S.w[nin] = kb; ++nin; }
+    int bpr = 0;
+    for (int j = 0; j < nin; ++j) bpr += Gs.S.w[j] * 8;
+    Gs.S.nin = nin;
+    Gs.S.T = tile_rows_for(bpr);
+    int off = 0;
+    for (int j = 0; j < nin; ++j) { Gs.S.off[j] = off; off += Gs.S.T * Gs.S.w[j] * 8; off = (off + 127) & ~127; }
+    if (off > STAGE_BYTES) { Gs.S.T /= 2; Gs.S.T &= ~7; off = 0;
+        for (int j = 0; j < nin; ++j) { Gs.S.off[j] = off; off += Gs.S.T * Gs.S.w[j] * 8; off = (off + 127) & ~127; } }
+    Gs.S.n = n;
+    Gs.S.ntiles = (int)((n + Gs.S.T - 1) / Gs.S.T);
+    Gs.ka = ka; Gs.kb = kb; Gs.part = part; Gs.ticket = ticket; Gs.G = G; Gs.G2 = nullptr;
+    const int grid = grid_for(Gs.S.ntiles, num_sms);
+    if (ka <= 4 && kb <= 4) {
+        const int smem = NSTAGE * STAGE_BYTES + 128;
+        static bool a = false;
+        if (!a) { set_smem((const void*)gram_small_stream_kernel, smem); a = true; }
+        BK_KERNEL(gram_small_stream_kernel<<<grid, NC + 32, smem, st>>>(Gs));
+        return true;
+    }
+    const int na = (ka + 7) / 8, nb = (kb + 7) / 8;
+#define BK_GS(A, B) if (na == A && nb == B) { gram_stream_t<A, B>(Gs, grid, st); return true; }
+    BK_GS(1, 1) BK_GS(1, 2) BK_GS(1, 3) BK_GS(1, 4) BK_GS(2, 1) BK_GS(2, 2) BK_GS(2, 3) BK_GS(2, 4)
+    BK_GS(3, 1) BK_GS(3, 2) BK_GS(3, 3) BK_GS(3, 4) BK_GS(4, 1) BK_GS(4, 2) BK_GS(4, 3) BK_GS(4, 4)
+#undef BK_GS
+    return false;
+}
+
+bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                          const double* Y2, int64_t ldy2, double* d, double* d2, double* part, int* ticket,
+                          int num_sms, cudaStream_t st) {
+    if (k > 32 || ldx != k || ldy != k || (Y2 && ldy2 != k) || n <= 0) return false;
+    if (((uintptr_t)X & 15) || ((uintptr_t)Y & 15) || (Y2 && ((uintptr_t)Y2 & 15))) return false;
+    GramStream Gs{};
+    Gs.same = (X == Y) ? 1 : 0;
+    int nin = 0;
+    Gs.S.p[nin] = X; Gs.S.w[nin] = k; ++nin;
+    Gs.S.p[nin] = Gs.same ? X : Y; Gs.S.w[nin] = Gs.same ? 0 : k; if (!Gs.same) ++nin; else Gs.S.p[1] = X;
+    if (Y2) {
+        if (Gs.same) { Gs.S.p[1] = X; Gs.S.w[1] = 0; }
+        Gs.S.p[2] = Y2; Gs.S.w[2] = k;
+        nin = 3;
+    }
+    // compact: stream list may contain a zero-width slot (same == 1) -- it moves no bytes
+    int bpr = 0;
+    for (int j = 0; j < nin; ++j) bpr += Gs.S.w[j] * 8;
+    Gs.S.nin = nin;
+    Gs.S.T = tile_rows_for(bpr);
+    int off = 0;
+    for (int j = 0; j < nin; ++j) { Gs.S.off[j] = off; off += Gs.S.T * Gs.S.w[j] * 8; off = (off + 127) & ~127; }
+    if (off > STAGE_BYTES) { Gs.S.T /= 2; Gs.S.T &= ~7; off = 0;
+        for (int j = 0; j < nin; ++j) { Gs.S.off[j] = off; off += Gs.S.T * Gs.S.w[j] * 8; off = (off + 127) & ~127; } }
+    Gs.S.n = n;
+    Gs.S.ntiles = (int)((n + Gs.S.T - 1) / Gs.S.T);
+    Gs.ka = k; Gs.kb = k; Gs.part = part; Gs.ticket = ticket; Gs.G = d; Gs.G2 = Y2 ? d2 : nullptr;
+    const int grid = grid_for(Gs.S.ntiles, num_sms);
+    const int smem = NSTAGE * STAGE_BYTES + 128;
+    static bool a = false;
+    if (!a) { set_smem((const void*)coldot_stream_kernel, smem); a = true; }
+    BK_KERNEL(coldot_stream_kernel<<<grid, NC + 32, smem, st>>>(Gs));
+    return true;
+}
+
+}  // namespace bk

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--ks", default="1,2,4,8,16,32")
     ap.add_argument("--ops", default="spmm")
     ap.add_argument("--reps", type=int, default=7)
+    ap.add_argument("--batch", type=int, default=1, help="launches per timed region (amortises host overhead)")
     args = ap.parse_args()
     peak = 6548.8
     dev = torch.device("cuda", 0)
@@ -33,7 +34,30 @@ def main():
     M = bk.Matrix.from_csr(ctx, A)
     n, nnz = A.n_rows, A.nnz
     flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+    flush2 = torch.ones(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
     st = torch.cuda.current_stream()
+    mode = os.environ.get("FLUSH", "wr")
+
+    def do_flush():
+        flush.fill_(1.0)                 # write a buffer > L2 ...
+        if mode == "wr":
+            flush2.sum()                 # ... then read one, so L2 holds clean lines (no write-back in the timed kernel)
+
+    # calibration: plain device copy of 1 GiB (read + write bytes), as MEASURED_PEAKS.json does
+    a1 = torch.empty(1 << 27, dtype=torch.float64, device=dev)
+    b1 = torch.empty_like(a1)
+    ts = []
+    for _ in range(5):
+        do_flush()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        b1.copy_(a1)
+        e1.record(st)
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    print(json.dumps({"tag": "copy", "cfg": "1GiB", "op": "copy", "k": 0,
+                      "gbs": round(2 * a1.numel() * 8 / (min(ts) * 1e-3) / 1e9, 1)}))
+    del a1, b1
     tag = f"{os.environ.get('BK_SPMM_KERNEL', 'pipe')}/vec{os.environ.get('BK_SPMM_VEC', '8')}"
     for k in [int(x) for x in args.ks.split(",")]:
         X = synth.multivector(n, k, 3, device=dev)
@@ -48,14 +72,15 @@ def main():
             fn, by = ops[op]
             ts = []
             for _ in range(args.reps):
-                flush.fill_(1.0)
+                do_flush()
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 a.record(st)
-                fn()
+                for _ in range(args.batch):
+                    fn()
                 b.record(st)
                 torch.cuda.synchronize()
                 ts.append(a.elapsed_time(b))
-            ms = statistics.median(ts[1:])
+            ms = statistics.median(ts[1:]) / args.batch
             gbs = by / (ms * 1e-3) / 1e9
             print(json.dumps({"tag": tag, "cfg": args.cfg, "op": op, "k": k, "us": round(ms * 1e3, 2),
                               "gbs": round(gbs, 1), "frac": round(gbs / peak, 4)}))
