@@ -377,16 +377,34 @@ __global__ void gmres_backsolve_kernel(const double* __restrict__ Rtri, int ldr,
 
 }  // namespace
 
+// single-warp register versions (dense_warp.cu) are the default; BK_DENSE=cta
+// selects the shared-memory CTA kernels above (A/B and cross-check)
+void sdw_lu_solve(const double*, const double*, double*, int, int, double, double, DevStatus*, cudaStream_t);
+void sdw_chol_solve(const double*, const double*, double*, int, int, double, DevStatus*, cudaStream_t);
+void sdw_chol_qr(const double*, double*, double*, const double*, double*, int, double, DevStatus*, cudaStream_t);
+
+static bool dense_cta() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("BK_DENSE");
+        v = (e && e[0] == 'c') ? 1 : 0;
+    }
+    return v == 1;
+}
+
 void sd_chol_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double tol, DevStatus* st,
                    cudaStream_t s) {
+    if (!dense_cta()) return sdw_chol_solve(G, Rhs, Out, k, nrhs, tol, st, s);
     BK_KERNEL(chol_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, tol, st));
 }
 void sd_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign, double tol,
                  DevStatus* st, cudaStream_t s) {
+    if (!dense_cta()) return sdw_lu_solve(G, Rhs, Out, k, nrhs, sign, tol, st, s);
     BK_KERNEL(lu_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, sign, tol, st));
 }
 void sd_chol_qr(const double* G, double* R, double* Rinv, const double* Rprev, double* Rprod, int k, double tol,
                 DevStatus* st, cudaStream_t s) {
+    if (!dense_cta()) return sdw_chol_qr(G, R, Rinv, Rprev, Rprod, k, tol, st, s);
     BK_KERNEL(chol_qr_kernel<<<1, 256, 0, s>>>(G, R, Rinv, Rprev, Rprod, k, tol, st));
 }
 void sd_conv_check(const double* g, int gstride, int k, double rtol, int conv_mode, int init, DevStatus* st,

@@ -1,0 +1,194 @@
+// dense_warp.cu -- a4 small dense k x k stage as single-warp kernels (k <= 32).
+//
+// One warp, matrices in shared memory (padded rows, conflict-free), lanes work
+// on rows (elimination) or on right-hand-side columns (substitution), loops
+// rolled (compact code: a fully unrolled register version was 57 K SASS
+// instructions and I-cache bound), only __syncwarp between steps (the
+// 256-thread CTA versions in dense.cu spend ~100 block barriers per call).
+// Breakdown is a status (DevStatus), never a crash (R6).
+#include "bk_internal.h"
+
+namespace bk {
+namespace {
+
+constexpr int KM = BK_MAX_K;
+constexpr int LD = KM + 1;
+
+__device__ __forceinline__ double wmax(double v) {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, m));
+    return v;
+}
+
+// LU with partial pivoting (explicit row swaps), Out = G^{-1} (sign Rhs).
+__global__ void __launch_bounds__(32) lu_solve_w(const double* __restrict__ G, const double* __restrict__ Rhs,
+                                                 double* __restrict__ Out, int k, int nrhs, double sign, double tol,
+                                                 DevStatus* st) {
+    __shared__ double A[KM * LD], B[KM * LD];
+    if (st && st->halt) return;
+    const int l = threadIdx.x;
+    double mx = 0.0;
+    for (int r = 0; r < k; ++r) {
+        if (l < k) { const double g = G[r * k + l]; A[r * LD + l] = g; mx = fmax(mx, fabs(g)); }
+        if (l < nrhs) B[r * LD + l] = sign * Rhs[r * nrhs + l];
+    }
+    mx = wmax(mx);
+    if (!(mx > 0.0)) mx = 2.2250738585072014e-308;
+    __syncwarp();
+#pragma unroll 1
+    for (int j = 0; j < k; ++j) {
+        double v = (l >= j && l < k) ? fabs(A[l * LD + j]) : -1.0;
+        int p = l;
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, m);
+            const int op = __shfl_xor_sync(0xffffffffu, p, m);
+            if (ov > v || (ov == v && op < p)) { v = ov; p = op; }
+        }
+        if (!(v > tol * mx)) {
+            if (l == 0 && st) { st->breakdown_col = j; st->halt = 1; }
+            return;
+        }
+        if (p != j) {   // lane l swaps column l of rows j and p
+            if (l < k) { const double t = A[j * LD + l]; A[j * LD + l] = A[p * LD + l]; A[p * LD + l] = t; }
+            if (l < nrhs) { const double t = B[j * LD + l]; B[j * LD + l] = B[p * LD + l]; B[p * LD + l] = t; }
+        }
+        __syncwarp();
+        if (l > j && l < k) {
+            const double f = A[l * LD + j] / A[j * LD + j];
+#pragma unroll 4
+            for (int c = j + 1; c < k; ++c) A[l * LD + c] = fma(-f, A[j * LD + c], A[l * LD + c]);
+#pragma unroll 4
+            for (int c = 0; c < nrhs; ++c) B[l * LD + c] = fma(-f, B[j * LD + c], B[l * LD + c]);
+        }
+        __syncwarp();
+    }
+    // back substitution, lane = right-hand-side column (solution overwrites B)
+    if (l < nrhs) {
+#pragma unroll 1
+        for (int i = k - 1; i >= 0; --i) {
+            double v = B[i * LD + l];
+#pragma unroll 4
+            for (int q = i + 1; q < k; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
+            B[i * LD + l] = v / A[i * LD + i];
+        }
+        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
+    }
+}
+
+// Cholesky of A (lower part, lane = row); returns breakdown column or -1.
+__device__ int chol_w(double* A, int k, double tol) {
+    const int l = threadIdx.x;
+    double scale = wmax(l < k ? fabs(A[l * LD + l]) : 0.0);
+    if (!(scale > 0.0)) scale = 2.2250738585072014e-308;
+#pragma unroll 1
+    for (int j = 0; j < k; ++j) {
+        const double d = A[j * LD + j];
+        if (!(d > tol * scale)) return j;
+        const double ljj = sqrt(d);
+        __syncwarp();
+        if (l == j) A[j * LD + j] = ljj;
+        if (l > j && l < k) A[l * LD + j] /= ljj;
+        __syncwarp();
+        if (l > j && l < k) {
+            const double lij = A[l * LD + j];
+#pragma unroll 4
+            for (int c = j + 1; c <= l; ++c) A[l * LD + c] = fma(-lij, A[c * LD + j], A[l * LD + c]);
+        }
+        __syncwarp();
+    }
+    return -1;
+}
+
+// Out = G^{-1} Rhs by Cholesky: L w = Rhs, L^T z = w (lane = rhs column).
+__global__ void __launch_bounds__(32) chol_solve_w(const double* __restrict__ G, const double* __restrict__ Rhs,
+                                                   double* __restrict__ Out, int k, int nrhs, double tol,
+                                                   DevStatus* st) {
+    __shared__ double A[KM * LD], B[KM * LD];
+    if (st && st->halt) return;
+    const int l = threadIdx.x;
+    for (int r = 0; r < k; ++r) {
+        if (l < k) A[r * LD + l] = G[r * k + l];
+        if (l < nrhs) B[r * LD + l] = Rhs[r * nrhs + l];
+    }
+    __syncwarp();
+    const int fail = chol_w(A, k, tol);
+    if (fail >= 0) {
+        if (l == 0 && st) { st->breakdown_col = fail; st->halt = 1; }
+        return;
+    }
+    if (l < nrhs) {
+#pragma unroll 1
+        for (int i = 0; i < k; ++i) {
+            double v = B[i * LD + l];
+#pragma unroll 4
+            for (int q = 0; q < i; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
+            B[i * LD + l] = v / A[i * LD + i];
+        }
+#pragma unroll 1
+        for (int i = k - 1; i >= 0; --i) {
+            double v = B[i * LD + l];
+#pragma unroll 4
+            for (int q = i + 1; q < k; ++q) v = fma(-A[q * LD + i], B[q * LD + l], v);
+            B[i * LD + l] = v / A[i * LD + i];
+        }
+        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
+    }
+}
+
+// CholQR factor: G = R^T R (R = L^T), Rinv = R^{-1} (lane = column), Rprod = R Rprev.
+__global__ void __launch_bounds__(32) chol_qr_w(const double* __restrict__ G, double* __restrict__ R,
+                                                double* __restrict__ Rinv, const double* __restrict__ Rprev,
+                                                double* __restrict__ Rprod, int k, double tol, DevStatus* st) {
+    __shared__ double A[KM * LD], Z[KM * LD];
+    if (st && st->halt) return;
+    const int l = threadIdx.x;
+    for (int r = 0; r < k; ++r)
+        if (l < k) A[r * LD + l] = G[r * k + l];
+    __syncwarp();
+    const int fail = chol_w(A, k, tol);
+    if (fail >= 0) {
+        if (l == 0 && st) { st->breakdown_col = fail; st->halt = 1; }
+        return;
+    }
+    if (l < k) {
+        // R[r][c] = L[c][r] (c >= r); column l of R^{-1}: R z = e_l, R[q][p] = L[p][q]
+#pragma unroll 1
+        for (int q = k - 1; q >= 0; --q) {
+            double v = (q == l) ? 1.0 : 0.0;
+#pragma unroll 4
+            for (int p = q + 1; p < k; ++p) v = fma(-A[p * LD + q], Z[p * LD + l], v);
+            Z[q * LD + l] = v / A[q * LD + q];
+        }
+        for (int q = 0; q < k; ++q) {
+            Rinv[q * k + l] = (q <= l) ? Z[q * LD + l] : 0.0;
+            if (R) R[q * k + l] = (l >= q) ? A[l * LD + q] : 0.0;
+        }
+        if (Rprev && Rprod) {
+            for (int r = 0; r < k; ++r) {
+                double v = 0.0;
+                for (int q = r; q < k; ++q) v = fma(A[q * LD + r], Rprev[q * k + l], v);
+                Rprod[r * k + l] = v;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+void sdw_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign, double tol,
+                  DevStatus* st, cudaStream_t s) {
+    BK_KERNEL(lu_solve_w<<<1, 32, 0, s>>>(G, Rhs, Out, k, nrhs, sign, tol, st));
+}
+
+void sdw_chol_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double tol, DevStatus* st,
+                    cudaStream_t s) {
+    BK_KERNEL(chol_solve_w<<<1, 32, 0, s>>>(G, Rhs, Out, k, nrhs, tol, st));
+}
+
+void sdw_chol_qr(const double* G, double* R, double* Rinv, const double* Rprev, double* Rprod, int k, double tol,
+                 DevStatus* st, cudaStream_t s) {
+    BK_KERNEL(chol_qr_w<<<1, 32, 0, s>>>(G, R, Rinv, Rprev, Rprod, k, tol, st));
+}
+
+}  // namespace bk

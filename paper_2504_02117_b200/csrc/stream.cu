@@ -126,6 +126,7 @@ __device__ __forceinline__ void stream_produce(const Streams& S, unsigned char* 
 struct UpdStream {
     Streams S;          // 0 = P (kp), 1 = Xin (k, if a != 0), 2 = W (k, if present)
     int iX, iW;         // stream index of Xin / W, -1 if absent
+    int iP;             // stream index of P (-1 when kp == 0: out = a Xin + w W)
     int kp, k, cw;      // cw = columns per thread (1, 2 or 4)
     double a, s, w_host;
     const double* w_dev;
@@ -276,12 +277,12 @@ __global__ void __launch_bounds__(NC + 32, 2) upd_stream_kernel(const UpdStream 
         const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
         if (!s_direct[s]) {
             const unsigned char* st = smem + s * STAGE_BYTES;
-            const double* Pt = reinterpret_cast<const double*>(st + U.S.off[0]);
+            const double* Pt = U.iP >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iP]) : nullptr;
             const double* Xt = U.iX >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iX]) : nullptr;
             const double* Wt = U.iW >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iW]) : nullptr;
             upd_tile<CW>(U, Pt, Xt, Wt, sC, nr, r0, wv);
         } else {
-            const double* Pt = U.S.p[0] + r0 * U.kp;
+            const double* Pt = U.iP >= 0 ? U.S.p[U.iP] + r0 * U.kp : nullptr;
             const double* Xt = U.iX >= 0 ? U.S.p[U.iX] + r0 * U.k : nullptr;
             const double* Wt = U.iW >= 0 ? U.S.p[U.iW] + r0 * U.k : nullptr;
             upd_tile<CW>(U, Pt, Xt, Wt, sC, nr, r0, wv);
@@ -623,15 +624,17 @@ size_t stream_part_doubles(int num_sms) { return (size_t)(2 * num_sms + 40) * 10
 
 bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
     // contiguous operands only, kp and k <= 32, out not aliasing P/Xin/W rows in other tiles is fine
-    if (u.kp < 1 || u.kp > 32 || u.k > 32 || u.ldp != u.kp || u.ldo != u.k) return false;
-    if ((const double*)u.out == u.P) return false;   // in-place X <- X C: rows are read whole first (blas.cu)
+    if (u.kp < 0 || u.kp > 32 || u.k > 32 || (u.kp > 0 && u.ldp != u.kp) || u.ldo != u.k) return false;
+    if (u.kp > 0 && (const double*)u.out == u.P) return false;   // in-place X <- X C: blas.cu reads rows first
     if (u.a != 0.0 && (u.ldxin != u.k || !u.Xin)) return false;
     if (u.W && u.ldw != u.k) return false;
-    if (((uintptr_t)u.out & 15) || ((uintptr_t)u.P & 15)) return false;
+    if (u.kp == 0 && u.a == 0.0 && !u.W) return false;
+    if (((uintptr_t)u.out & 15) || (u.kp > 0 && ((uintptr_t)u.P & 15))) return false;
     const int cw = (u.k % 4 == 0) ? 4 : ((u.k % 2 == 0) ? 2 : 1);
     UpdStream U{};
     int nin = 0;
-    U.S.p[nin] = u.P; U.S.w[nin] = u.kp; ++nin;
+    U.iP = -1;
+    if (u.kp > 0) { U.iP = nin; U.S.p[nin] = u.P; U.S.w[nin] = u.kp; ++nin; }
     U.iX = -1; U.iW = -1;
     if (u.a != 0.0) { U.iX = nin; U.S.p[nin] = u.Xin; U.S.w[nin] = u.k; ++nin; }
     if (u.W) { U.iW = nin; U.S.p[nin] = u.W; U.S.w[nin] = u.k; ++nin; }
@@ -656,7 +659,7 @@ bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
         const char* e = getenv("BK_UPD");
         mma = (e && strcmp(e, "fma") == 0) ? 0 : 1;
     }
-    if (mma && u.k % 8 == 0 && u.kp % 4 == 0) {
+    if (mma && u.kp > 0 && u.k % 8 == 0 && u.kp % 4 == 0) {
         const int nq = u.kp / 4, nk = u.k / 8;
 #define BK_UM(Q, K)                                                                            \
     if (nq == Q && nk == K) {                                                                  \
