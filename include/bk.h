@@ -102,6 +102,9 @@ typedef struct bk_csr_info {
     int64_t n_send_rows;      /* rows sent to other ranks per apply         */
     int     n_neighbors;
     int     interior_contiguous; /* interior rows form one contiguous range */
+    int     n_bands;          /* diagonal bands of the windowed apply
+                                 (bk_plan_bands; 0: unstaged gathers)        */
+    int     band_extra_rows;  /* window rows per tile beyond n_bands * T      */
 } bk_csr_info;
 int bk_csr_get_info(const bk_csr *A, bk_csr_info *info);
 
@@ -201,6 +204,32 @@ int bk_plan_halo(int nranks, int rank, const int64_t *rank_begin,
                  int64_t n_local, const int32_t *row_ptr, const int32_t *col_global,
                  int64_t nnz, int64_t *n_ghost, int64_t *ghost_ids, int32_t *ghost_owner,
                  int32_t *col_local, uint8_t *is_boundary);
+
+/* Band plan of the windowed apply (pure host code, run by
+ * bk_csr_create on the contiguous (interior) row range, exported for CPU
+ * tests).  The paper's BOP streams the matrix once for all k columns
+ * (P:666-667); on B200 the X rows a tile of rows needs are moved into shared
+ * memory by TMA bulk copies so the gathers become shared-memory loads.  For a
+ * structured-grid operator every nonzero lies on a few diagonals d = col - row
+ * (5-point: 0, +-1, +-nx; 7-point: also +-nx*ny).  The distinct offsets are
+ * merged into BANDS (gaps <= 4); band g = offsets [dmin, dmax].  For a tile of
+ * rows [r0, r0 + T) (r0, T even) band g needs X rows [r0 + lo, r0 + T + hi)
+ * with lo = dmin rounded down and hi = dmax + 1 rounded up to even (16-byte
+ * aligned TMA copies for any k).  The matrix is band structured (nbands > 0)
+ * when there are <= BK_BAND_MAX bands and sum(hi - lo) <= max_extra;
+ * otherwise nbands = 0 and the apply uses the unstaged gather kernel.
+ * row_ptr: n_rows + 1 offsets into col (any base); row i of the range has
+ * local index i (d = col - i).  Returns BK_OK or BK_ERR_ARG.                */
+#define BK_BAND_MAX 7
+typedef struct bk_band_plan {
+    int32_t nbands;                 /* 0 = not band structured               */
+    int32_t extra_rows;             /* sum(hi - lo): window = nbands*T + this */
+    int32_t max_row_nnz;            /* sum of band widths (>= nnz of any row) */
+    int32_t dmin[BK_BAND_MAX], dmax[BK_BAND_MAX], width[BK_BAND_MAX];
+    int32_t lo[BK_BAND_MAX], hi[BK_BAND_MAX];
+} bk_band_plan;
+int bk_plan_bands(int64_t n_rows, const int32_t *row_ptr, const int32_t *col, int max_extra,
+                  bk_band_plan *out);
 
 #ifdef __cplusplus
 }

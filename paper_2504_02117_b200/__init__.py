@@ -37,7 +37,8 @@ CONV = {"all": 0, "first": 1}
 EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last_error", "bk_ctx_create", "bk_ctx_set_stream",
             "bk_ctx_synchronize", "bk_ctx_destroy", "bk_get_nccl_unique_id", "bk_ctx_set_comm",
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
-            "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo"]
+            "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo",
+            "bk_plan_bands"]
 
 
 class SolveOpts(ctypes.Structure):
@@ -59,7 +60,8 @@ class CsrInfo(ctypes.Structure):
     _fields_ = [("n_global", ctypes.c_int64), ("row_begin", ctypes.c_int64), ("n_local", ctypes.c_int64),
                 ("nnz", ctypes.c_int64), ("n_ghost", ctypes.c_int64), ("n_boundary_rows", ctypes.c_int64),
                 ("n_send_rows", ctypes.c_int64), ("n_neighbors", ctypes.c_int),
-                ("interior_contiguous", ctypes.c_int)]
+                ("interior_contiguous", ctypes.c_int), ("n_bands", ctypes.c_int),
+                ("band_extra_rows", ctypes.c_int)]
 
 
 _P, _I, _I64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
@@ -85,6 +87,7 @@ _sig = {
     "block_krylov_solve": ([_P, _P, _I, _P, _I64, _P, _I64, ctypes.POINTER(SolveOpts),
                             ctypes.POINTER(SolveReport)], _I),
     "bk_plan_halo": ([_I, _I, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P], _I),
+    "bk_plan_bands": ([_I64, _P, _P, _I, _P], _I),
 }
 for _n, (_a, _r) in _sig.items():
     _f = getattr(_lib, _n)
@@ -352,3 +355,28 @@ def plan_halo(nranks: int, rank: int, rank_begin, row_ptr, col_global):
         raise BkError(st, "bk_plan_halo")
     g = ng.value
     return {"ghost_ids": gid[:g], "ghost_owner": gown[:g], "col_local": cl[:nnz], "is_boundary": bnd[:n_local]}
+
+
+BK_BAND_MAX = 7
+
+
+class BandPlan(ctypes.Structure):
+    _fields_ = [("nbands", ctypes.c_int32), ("extra_rows", ctypes.c_int32), ("max_row_nnz", ctypes.c_int32),
+                ("dmin", ctypes.c_int32 * BK_BAND_MAX), ("dmax", ctypes.c_int32 * BK_BAND_MAX),
+                ("width", ctypes.c_int32 * BK_BAND_MAX), ("lo", ctypes.c_int32 * BK_BAND_MAX),
+                ("hi", ctypes.c_int32 * BK_BAND_MAX)]
+
+
+def plan_bands(row_ptr, col, max_extra: int = 96) -> dict:
+    """Host-only band plan of the windowed apply (bk_plan_bands): diagonal bands
+    [dmin, dmax] of d = col - row and their even-rounded segment bounds lo/hi."""
+    rp = np.ascontiguousarray(row_ptr, dtype=np.int32)
+    c = np.ascontiguousarray(col, dtype=np.int32)
+    pl = BandPlan()
+    st = _lib.bk_plan_bands(len(rp) - 1, _P(rp.ctypes.data), _P(c.ctypes.data), max_extra, ctypes.byref(pl))
+    if st:
+        raise BkError(st, "bk_plan_bands")
+    g = pl.nbands
+    return {"nbands": g, "extra_rows": pl.extra_rows, "max_row_nnz": pl.max_row_nnz,
+            "dmin": list(pl.dmin[:g]), "dmax": list(pl.dmax[:g]), "width": list(pl.width[:g]),
+            "lo": list(pl.lo[:g]), "hi": list(pl.hi[:g])}

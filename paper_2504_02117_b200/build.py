@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "lib", "libbk.so")
-SOURCES = ["spmm.cu", "blas.cu", "gram_mma.cu", "stream.cu", "dense.cu", "dense_warp.cu", "abi.cpp", "solve.cpp", "comm.cpp"]
+SOURCES = ["spmm.cu", "blas.cu", "gram_mma.cu", "stream.cu", "dense.cu", "dense_warp.cu", "abi.cpp", "solve.cpp", "comm.cpp", "window.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         common += ["-I", inc]
     else:
         common += ["-DBK_NO_NCCL"]
-    headers = [os.path.join(CSRC, "bk_internal.h"), os.path.join(ROOT, "include", "bk.h")]
+    headers = [os.path.join(CSRC, "bk_internal.h"), os.path.join(CSRC, "ptx.cuh"), os.path.join(ROOT, "include", "bk.h")]
     hdr_mtime = max(os.path.getmtime(h) for h in headers)
     nvcc = _nvcc()
 

@@ -344,6 +344,32 @@ extern "C" int bk_csr_create(bk_ctx* ctx, bk_csr** out, int64_t n_global, int64_
         cudaMemcpyAsync(A->d_col, col_local.data(), sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st);
         cudaMemcpyAsync(A->d_val, val, sizeof(double) * nnz, cudaMemcpyDefault, st);
     }
+    // band plan of the contiguous (interior) row range (window.cpp)
+    if (A->interior_contig && A->n_interior > 0 && nnz > 0) {
+        const int64_t ib = A->interior_begin, ni = A->n_interior;
+        bk_band_plan bp;
+        // rows of the range are numbered from 0 by the planner: offsets d = col - (row - ib)
+        std::vector<int32_t> rp_range(rp.begin() + ib, rp.begin() + ib + ni + 1);
+        std::vector<int32_t> col_shift;
+        const int32_t* cols = col_local.data();
+        if (ib != 0) {   // shift to range-local row numbering: d = col - row
+            col_shift.resize(nnz);
+            for (int64_t i = 0; i < ni; ++i)
+                for (int32_t p = rp_range[i]; p < rp_range[i + 1]; ++p) col_shift[p] = col_local[p] - (int32_t)ib;
+            cols = col_shift.data();
+        }
+        if (bk_plan_bands(ni, rp_range.data(), cols, 96, &bp) == BK_OK && bp.nbands > 0) {
+            A->band.nbands = bp.nbands;
+            A->band.extra = bp.extra_rows;
+            A->band.max_row_nnz = bp.max_row_nnz;
+            for (int g = 0; g < bp.nbands; ++g) {
+                A->band.lo[g] = bp.lo[g];
+                A->band.hi[g] = bp.hi[g];
+            }
+            A->band.row0 = ib;
+            A->band.nrows = ni;
+        }
+    }
     // Jacobi diagonal (local numbering: diagonal column of row i is i)
     launch_extract_diag_inv(n_local, 0, A->d_rp, A->d_col, A->d_val, A->d_dinv, st);
     int rr = post_launch(ctx, "bk_csr_create");
@@ -385,6 +411,8 @@ extern "C" int bk_csr_get_info(const bk_csr* A, bk_csr_info* info) {
     info->n_send_rows = A->n_send_total;
     info->n_neighbors = (int)A->nbs.size();
     info->interior_contiguous = A->interior_contig;
+    info->n_bands = A->band.nbands;
+    info->band_extra_rows = A->band.extra;
     return BK_OK;
 }
 
@@ -409,7 +437,7 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
     if (ctx->nranks == 1 || A->n_ghost == 0) {
         a.row0 = 0;
         a.nrows = A->n_local;
-        launch_bspmm(a, ctx->stream);
+        if (!launch_bspmm_win(a, A->band, ctx->stream)) launch_bspmm(a, ctx->stream);
         return post_launch(ctx, "bspmm_apply");
     }
     // p > 1: halo exchange on the comm stream overlapped with the interior rows
@@ -423,7 +451,7 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
         a.rows = A->d_interior_rows;
         a.nrows = A->n_interior;
     }
-    launch_bspmm(a, ctx->stream);
+    if (!launch_bspmm_win(a, A->band, ctx->stream)) launch_bspmm(a, ctx->stream);
     cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
     a.rows = A->d_boundary_rows;
     a.nrows = A->n_boundary;

@@ -77,6 +77,15 @@ struct UpdArgs {
 };
 
 void launch_bspmm(const SpmmArgs& a, cudaStream_t st);
+// Windowed apply (X rows of each diagonal band staged in shared memory by
+// TMA) over the planned contiguous row range; false = not
+// applicable (the caller then uses launch_bspmm).
+struct BandPlan {
+    int nbands = 0, extra = 0, max_row_nnz = 0;
+    int lo[BK_BAND_MAX] = {}, hi[BK_BAND_MAX] = {};
+    int64_t row0 = 0, nrows = 0;     // planned contiguous row range
+};
+bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& b, cudaStream_t st);
 void launch_update(const UpdArgs& a, cudaStream_t st);
 // G (ka x kb, row-major, device) = X^T Y; `partials` workspace of gram_ws_doubles().
 size_t gram_ws_doubles(int64_t n, int ka, int kb, int num_sms);
@@ -192,6 +201,7 @@ struct bk_csr {
     std::vector<bk_neighbor> nbs;
     int64_t n_send_total = 0;
     bk_buf ghost, sendbuf;
+    bk::BandPlan band;                    // band plan of the contiguous interior range
 };
 
 // workspace slots used by the ABI and the solvers

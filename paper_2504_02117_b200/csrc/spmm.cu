@@ -20,10 +20,13 @@
 // A simpler one-tile-per-CTA kernel (load, sync, compute) is kept as the
 // `BK_SPMM_KERNEL=tile` variant for A/B measurements; row lists (boundary rows
 // of a partitioned matrix) use a direct, unstaged kernel.
+#include <algorithm>
+#include <climits>
 #include <cstdlib>
 #include <cstring>
 
 #include "bk_internal.h"
+#include "ptx.cuh"
 
 namespace bk {
 namespace {
@@ -36,44 +39,6 @@ template <int VEC>
 struct Batch { static constexpr int B = VEC >= 8 ? 2 : (VEC >= 4 ? 4 : 8); };
 
 // ------------------------------------------------------------------ PTX helpers
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    while (!mbar_try(bar, parity)) {
-    }
-}
-__device__ __forceinline__ uint64_t evict_first_policy() {
-    uint64_t pol;
-    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-    return pol;
-}
-// TMA bulk copy global -> shared (1-D), completion counted on `bar`
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-            "r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-        : "memory");
-}
 
 __device__ __forceinline__ void ld_x(const double* p, double (&x)[1]) { x[0] = __ldg(p); }
 template <int VEC>
@@ -461,10 +426,7 @@ int variant() {
         const char* e = getenv("BK_SPMM_KERNEL");
         // default = 3 CTAs/SM x 8 consumer warps, 2 stages, 256-row tiles (A/B: tools/ab_spmm.sh)
         v = 0;
-        const char* names[] = {"pipe", "tile", "pipe2x3", "pipe3x2", "pipe4x2", "pipe4x3t128", "pipe8x3t128n128",
-                               "pipe3x2n384", "pipe3x2pair", "pipe2x2pair"};
-        for (int i = 0; e && i < 10; ++i)
-            if (strcmp(e, names[i]) == 0) v = i;
+        if (e && strcmp(e, "tile") == 0) v = 1;
     }
     return v;
 }
@@ -497,17 +459,8 @@ void launch_t(const SpmmArgs& a, cudaStream_t st) {
                 return;
             }
         }
-        const int ns = num_sms_cached();
-        switch (variant()) {
-            case 2: launch_pipe<KP, VEC, HAS_C, 256, 3, 2, 256, 2304>(a, ns, st); break;
-            case 4: launch_pipe<KP, VEC, HAS_C, 256, 2, 4, 256, 2048>(a, ns, st); break;
-            case 5: launch_pipe<KP, VEC, HAS_C, 256, 3, 4, 128, 1152>(a, ns, st); break;
-            case 6: launch_pipe<KP, VEC, HAS_C, 128, 3, 8, 128, 1152>(a, ns, st); break;
-            case 7: launch_pipe<KP, VEC, HAS_C, 384, 2, 3, 256, 2304>(a, ns, st); break;
-            case 8: launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304, true>(a, ns, st); break;
-            case 9: launch_pipe<KP, VEC, HAS_C, 256, 2, 2, 256, 2304, true>(a, ns, st); break;
-            default: launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304>(a, ns, st); break;
-        }
+        // (round-1 A/B of ring depth / CTAs per SM / tile size: DESIGN.md §4.1)
+        launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304>(a, num_sms_cached(), st);
     }
 }
 
@@ -548,6 +501,364 @@ void launch_k(const SpmmArgs& a, cudaStream_t st, bool vec2) {
     launch_kv<KP, 1>(a, st);
 }
 
+
+// ------------------------------------------------------------------ windowed pipeline (X staged in shared memory)
+// DESIGN.md §4.1.  For a band-structured matrix (every nonzero on a few
+// diagonals d = col - row, bk_plan_bands) the X rows a tile of rows [r0, r0+T)
+// needs are one contiguous segment per band, [r0 + lo_g, r0 + T + hi_g).  The
+// producer warp moves the tile's CSR ranges AND those segments into a shared-
+// memory ring with TMA bulk copies (no per-tile plan: addresses follow from r0;
+// only the tile's two row-pointer bounds are prefetched, several tiles ahead,
+// with cp.async); the consumers' gathers become shared-memory loads.  Column-
+// chunk order alternates between rows so the 16-byte LDS of a warp spread over
+// all 32 banks.
+struct BandArgs {
+    SpmmArgs a;
+    int lo[BK_BAND_MAX], hi[BK_BAND_MAX], wb[BK_BAND_MAX];   // segment bounds, window row base
+    int G;              // bands
+    int TR, cap, ns;    // rows per tile, staged nonzeros per tile, ring stages
+    int stage_bytes, off_col, off_val, off_rp;
+    int ntiles;
+    int64_t ncols;      // rows of X
+    int dbg;            // diagnostics (BK_WIN_DEBUG, timing only; results invalid):
+                        // 1 consumers skip the rows, 2 only the top band is copied
+};
+constexpr int kMetaDepth = 8;   // tiles whose row-pointer bounds are in flight
+
+// One X row chunk (VEC doubles at column c0) of window row `wr`.
+template <int VEC>
+__device__ __forceinline__ void win_load(const double* xp, int sw, double (&x)[VEC]) {
+    if constexpr (VEC == 4) {
+        const double2 lo = reinterpret_cast<const double2*>(xp)[sw];
+        const double2 hi = reinterpret_cast<const double2*>(xp)[1 - sw];
+        x[0] = lo.x; x[1] = lo.y; x[2] = hi.x; x[3] = hi.y;
+    } else if constexpr (VEC == 2) {
+        const double2 q = *reinterpret_cast<const double2*>(xp);
+        x[0] = q.x; x[1] = q.y;
+    } else {
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) x[t] = xp[t];
+    }
+}
+
+// acc += sum_{p in [s,e)} val[p] X[col[p], c0 : c0+VEC] with X from the staged
+// window (window row of column c: c + fo[g] for the last band g with
+// c >= thr[g]).  MR > 0: every row has <= MR nonzeros (the plan's bound), one
+// branch-free pass with clamped indices and zero weights; MR == 0: batches of 4.
+// Lanes with c0 >= k compute on in-bounds garbage that is never stored.
+template <int VEC, int NB, int MR>
+__device__ __forceinline__ void band_accumulate(const double* s_win, const int* col, const double* val, int s, int e,
+                                                const int (&thr)[NB], const int (&fo)[NB], int kk, int c0, int sw,
+                                                double (&acc)[VEC]) {
+    constexpr int B = MR > 0 ? MR : 4;
+    for (int p = s; p < e; p += B) {
+        double x[B][VEC];
+        double v[B];
+#pragma unroll
+        for (int u = 0; u < B; ++u) {
+            const int q = (p + u < e) ? p + u : e - 1;
+            const int c = col[q];
+            v[u] = (p + u < e) ? val[q] : 0.0;
+            int f = fo[0];
+#pragma unroll
+            for (int g = 1; g < NB; ++g) f = (c >= thr[g]) ? fo[g] : f;
+            win_load<VEC>(s_win + (c + f) * kk + c0, sw, x[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < B; ++u)
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) acc[t] = fma(v[u], x[u][t], acc[t]);
+        if constexpr (MR > 0) break;
+    }
+    if constexpr (VEC == 4) {
+        if (sw) {   // chunks were accumulated in swapped order
+            const double t0 = acc[0], t1 = acc[1];
+            acc[0] = acc[2]; acc[1] = acc[3]; acc[2] = t0; acc[3] = t1;
+        }
+    }
+}
+
+template <int KP, int VEC, bool HAS_C, int NC, int NB, int MR, bool KEXACT>
+__global__ void __launch_bounds__(NC + 32, 1)
+bspmm_win_kernel(const BandArgs w) {
+    const SpmmArgs& a = w.a;
+    constexpr int LANES = KP / VEC;
+    constexpr int RPP = NC / LANES;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + w.ns * w.stage_bytes);
+    uint64_t* empty = full + 8;
+    int2* s_pp = reinterpret_cast<int2*>(empty + 8);           // kMetaDepth row-pointer bounds
+    double* s_C = reinterpret_cast<double*>(s_pp + kMetaDepth);
+    double* s_t = s_C + KP * KP;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
+    if (tid == 0) {
+        for (int s = 0; s < w.ns; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC / 32);
+        }
+        mbar_fence_init();
+    }
+    if (tid < NC) load_C<KP, HAS_C>(a, s_C, tid, NC);
+    __syncthreads();
+
+    const int k = a.k;
+    if (warp == NC / 32) {
+        // ------------------------------------------------ producer (one thread)
+        if (lane32 != 0) return;
+        const uint64_t pol_once = evict_first_policy();    // CSR: read once
+        const uint64_t pol_x = evict_normal_policy();      // X rows: re-read by the neighbouring tiles
+        const int64_t rend = a.row0 + a.nrows;
+        auto fetch = [&](int tile, int slot) {
+            if (tile < w.ntiles) {
+                const int64_t r0 = a.row0 + (int64_t)tile * w.TR;
+                const int64_t r1 = (rend - r0) < w.TR ? rend : r0 + w.TR;
+                const uint32_t dst = smem_u32(s_pp + slot);
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(a.rp + r0) : "memory");
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4), "l"(a.rp + r1) : "memory");
+            }
+            asm volatile("cp.async.commit_group;" ::: "memory");
+        };
+        for (int d = 0; d < kMetaDepth; ++d) fetch(blockIdx.x + d * gridDim.x, d);
+        const uint32_t kb = (uint32_t)k * 8u;
+        int s = 0, slot = 0;
+        uint32_t ph = 0;
+        int i = 0;
+        for (int tile = blockIdx.x; tile < w.ntiles; tile += gridDim.x, ++i) {
+            asm volatile("cp.async.wait_group %0;" ::"n"(kMetaDepth - 1) : "memory");
+            const int2 pp = s_pp[slot];
+            fetch(tile + kMetaDepth * gridDim.x, slot);
+            slot = (slot + 1 == kMetaDepth) ? 0 : slot + 1;
+            if (i >= w.ns) mbar_wait(&empty[s], ph ^ 1u);
+            unsigned char* st = smem + s * w.stage_bytes;
+            double* s_win = reinterpret_cast<double*>(st);
+            const int64_t r0 = a.row0 + (int64_t)tile * w.TR;
+            const int nr = (int)((rend - r0) < w.TR ? (rend - r0) : w.TR);
+            const int p0 = pp.x, p1 = pp.y;
+            const int64_t ra = r0 & ~(int64_t)3;
+            const uint32_t rp_bytes = (uint32_t)((((r0 - ra) + nr + 1 + 3) & ~3) * 4);
+            const int pc = p0 & ~3, pv = p0 & ~1;
+            const uint32_t col_bytes = p1 > p0 ? (uint32_t)(((p1 - pc + 3) & ~3) * 4) : 0u;
+            const uint32_t val_bytes = p1 > p0 ? (uint32_t)(((p1 - pv + 1) & ~1) * 8) : 0u;
+            uint32_t bytes = rp_bytes + col_bytes + val_bytes;
+            int64_t sa[NB];
+            uint32_t sb[NB];
+#pragma unroll
+            for (int g = 0; g < NB; ++g) {
+                sb[g] = 0;
+                sa[g] = 0;
+                if (g < w.G && (!(w.dbg & 2) || g == w.G - 1)) {
+                    const int64_t lo = r0 + w.lo[g];
+                    const int64_t a0 = lo < 0 ? 0 : lo;
+                    int64_t b0 = r0 + nr + w.hi[g];
+                    if (b0 > w.ncols) b0 = w.ncols;
+                    if (b0 > a0) {
+                        uint32_t b = (uint32_t)(b0 - a0) * kb;
+                        double* dst = s_win + (int64_t)(w.wb[g] + (a0 - lo)) * k;
+                        if (b & 15u) {   // odd k and X ends at an odd row: last row by hand
+                            b -= kb;
+                            const double* src = a.X + (b0 - 1) * k;
+                            double* d1 = dst + (b0 - 1 - a0) * k;
+                            for (int t = 0; t < k; ++t) d1[t] = src[t];
+                        }
+                        sa[g] = a0;
+                        sb[g] = b;
+                        bytes += b;
+                    }
+                }
+            }
+            mbar_expect_tx(&full[s], bytes);
+            bulk_g2s(st + w.off_rp, a.rp + ra, rp_bytes, &full[s], pol_once);
+            if (col_bytes) {
+                bulk_g2s(st + w.off_col, a.col + pc, col_bytes, &full[s], pol_once);
+                bulk_g2s(st + w.off_val, a.val + pv, val_bytes, &full[s], pol_once);
+            }
+#pragma unroll
+            for (int g = 0; g < NB; ++g) {
+                if (sb[g]) {
+                    const int64_t lo = r0 + w.lo[g];
+                    bulk_g2s(s_win + (int64_t)(w.wb[g] + (sa[g] - lo)) * k, a.X + sa[g] * k, sb[g], &full[s], pol_x);
+                }
+            }
+            if (++s == w.ns) {
+                s = 0;
+                ph ^= 1u;
+            }
+        }
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        return;
+    }
+    // ---------------------------------------------------- consumer warps
+    const int grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
+    const int kk = KEXACT ? KP : k;
+    double* t_row = s_t + grp * (KP + 1);
+    const int passes = (w.TR + RPP - 1) / RPP;
+    int s = 0;
+    uint32_t ph = 0;
+    for (int tile = blockIdx.x; tile < w.ntiles; tile += gridDim.x) {
+        mbar_wait(&full[s], ph);
+        const unsigned char* st = smem + s * w.stage_bytes;
+        const int64_t r0 = a.row0 + (int64_t)tile * w.TR;
+        const int nr = (int)((a.row0 + a.nrows - r0) < w.TR ? (a.row0 + a.nrows - r0) : w.TR);
+        const int* s_rp = reinterpret_cast<const int*>(st + w.off_rp) + (int)(r0 & 3);
+        const int p0 = s_rp[0];
+        const int* scol = reinterpret_cast<const int*>(st + w.off_col) + (p0 & 3) - p0;
+        const double* sval = reinterpret_cast<const double*>(st + w.off_val) + (p0 & 1) - p0;
+        const double* s_win = reinterpret_cast<const double*>(st);
+        // window row of column c: c + fo[g] for the last band g with c >= thr[g]
+        int thr[NB], fo[NB];
+#pragma unroll
+        for (int g = 0; g < NB; ++g) {
+            const bool on = g < w.G;
+            thr[g] = on ? (int)(r0 + w.lo[g]) : INT_MAX;
+            fo[g] = on ? (int)(w.wb[g] - (r0 + w.lo[g])) : 0;
+        }
+#pragma unroll 1
+        for (int pass = 0; pass < (w.dbg & 1 ? 0 : passes); ++pass) {
+            const int r = pass * RPP + grp;
+            const bool active = r < nr;
+            double acc[VEC];
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
+            if (active) {
+                const int rs = s_rp[r], re = s_rp[r + 1];
+                if (re > rs) {
+                    const int gr = (int)(r0 + r);
+                    const int sw = (kk <= 16) ? (((gr * kk) >> 4) & 1) : (gr & 1);
+                    band_accumulate<VEC, NB, MR>(s_win, scol, sval, rs, re, thr, fo, kk, c0, sw, acc);
+                }
+            }
+            row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
+        }
+        __syncwarp();
+        if (lane32 == 0) mbar_arrive(&empty[s]);
+        if (++s == w.ns) {
+            s = 0;
+            ph ^= 1u;
+        }
+    }
+}
+
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
+template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT, int NC>
+bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int ctas) {
+    constexpr int LANES = KP / VEC;
+    constexpr int RPP = NC / LANES;
+    static const int tr_env = env_int("BK_WIN_TR", 0);
+    BandArgs w{};
+    w.a = a;
+    w.G = p.nbands;
+    auto r16 = [](int64_t x) { return (x + 15) & ~(int64_t)15; };
+    auto layout = [&](int TR) {
+        w.TR = TR;
+        w.cap = TR * p.max_row_nnz;
+        int wrows = 0;
+        for (int g = 0; g < p.nbands; ++g) {
+            w.lo[g] = p.lo[g];
+            w.hi[g] = p.hi[g];
+            w.wb[g] = wrows;
+            wrows += TR + p.hi[g] - p.lo[g];
+        }
+        const int64_t win = (int64_t)wrows * a.k * 8;
+        w.off_col = (int)r16(win);
+        w.off_val = w.off_col + (int)r16((int64_t)(w.cap + 4) * 4);
+        w.off_rp = w.off_val + (int)r16((int64_t)(w.cap + 2) * 8);
+        w.stage_bytes = (int)((w.off_rp + r16((TR + 8) * 4) + 127) & ~(int64_t)127);
+    };
+    int TR = RPP < 64 ? 64 : RPP;
+    if (tr_env > 0) TR = std::max(2, tr_env & ~1);
+    layout(TR);
+    const int fixed = 16 * 8 + kMetaDepth * 8 + (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
+    const int budget = (ctas == 1 ? 227 * 1024 : 113 * 1024) - fixed;
+    while (budget / w.stage_bytes < 2 && TR > 2 * 2) {   // huge windows: smaller tiles
+        TR = (TR / 2) & ~1;
+        layout(TR);
+    }
+    int ns = budget / w.stage_bytes;
+    if (ns > 8) ns = 8;
+    if (ns < 2) return false;
+    w.ns = ns;
+    const int64_t ntiles = (a.nrows + w.TR - 1) / w.TR;
+    if (ntiles >= (1ll << 31)) return false;
+    w.ntiles = (int)ntiles;
+    w.ncols = a.ncol_local;
+    static const int dbg = env_int("BK_WIN_DEBUG", 0);
+    w.dbg = dbg;
+    const int smem = ns * w.stage_bytes + fixed;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             227 * 1024);
+        attr = true;
+    }
+    const int64_t cap = (int64_t)ctas * num_sms_cached();
+    const int64_t grid = ntiles < cap ? ntiles : cap;
+    BK_KERNEL(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT><<<(unsigned)grid, NC + 32, smem, st>>>(w));
+    return true;
+}
+
+// CTA shape: two 256-consumer CTAs per SM when each still gets >= 3 ring
+// stages in half the shared memory, else one CTA with 512 consumers (more
+// warps for latency hiding, full shared memory for the window).  Env
+// BK_WIN_CTAS=1|2 forces it (A/B).
+template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT>
+bool launch_win_shape(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
+    static const int force = env_int("BK_WIN_CTAS", 0);
+    int ctas = force;
+    if (ctas != 1 && ctas != 2) {
+        // stage bytes at the 2-CTA tile size (RPP rows, >= 64)
+        const int rpp = 256 / (KP / VEC), tr = rpp < 64 ? 64 : rpp;
+        int64_t wrows = 0;
+        for (int g = 0; g < p.nbands; ++g) wrows += tr + p.hi[g] - p.lo[g];
+        const int64_t stage = wrows * a.k * 8 + (int64_t)tr * p.max_row_nnz * 12 + tr * 4 + 256;
+        ctas = (3 * stage <= 100 * 1024) ? 2 : 1;
+    }
+    if (ctas == 1 && KP >= 4) return launch_win_t<KP, VEC, HAS_C, NB, MR, KEXACT, 512>(a, p, st, 1);
+    return launch_win_t<KP, VEC, HAS_C, NB, MR, KEXACT, 256>(a, p, st, ctas);
+}
+
+template <int KP, int VEC, bool HAS_C, int NB, int MR>
+bool launch_win_ke(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
+    return a.k == KP ? launch_win_shape<KP, VEC, HAS_C, NB, MR, true>(a, p, st)
+                     : launch_win_shape<KP, VEC, HAS_C, NB, MR, false>(a, p, st);
+}
+
+// 2-D 5-point (3 bands, <= 5 nonzeros per row), 3-D 7-point (5 bands, <= 7),
+// anything else band structured: 7 bands, batched rows
+template <int KP, int VEC, bool HAS_C>
+bool launch_win_nb(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
+    if (p.nbands <= 3 && p.max_row_nnz <= 5) return launch_win_ke<KP, VEC, HAS_C, 3, 5>(a, p, st);
+    if (p.nbands <= 5 && p.max_row_nnz <= 7) return launch_win_ke<KP, VEC, HAS_C, 5, 7>(a, p, st);
+    return launch_win_ke<KP, VEC, HAS_C, BK_BAND_MAX, 0>(a, p, st);
+}
+
+template <int KP, int VEC>
+bool launch_win_kv(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
+    return a.C ? launch_win_nb<KP, VEC, true>(a, p, st) : launch_win_nb<KP, VEC, false>(a, p, st);
+}
+
+template <int KP>
+bool launch_win_k(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, bool vec2) {
+    if constexpr (KP >= 4) {
+        if (vec2 && a.k % 4 == 0 && a.kout % 4 == 0) return launch_win_kv<KP, 4>(a, p, st);
+    }
+    if constexpr (KP >= 2) {
+        if (vec2) return launch_win_kv<KP, 2>(a, p, st);
+    }
+    if constexpr (KP <= 8) return launch_win_kv<KP, 1>(a, p, st);   // odd k: one column per lane
+    return false;
+}
+
+bool win_enabled() {
+    static const int v = env_int("BK_SPMM_WIN", 1);
+    return v != 0;
+}
+
 }  // namespace
 
 void launch_bspmm(const SpmmArgs& a, cudaStream_t st) {
@@ -562,6 +873,21 @@ void launch_bspmm(const SpmmArgs& a, cudaStream_t st) {
     else if (kmax <= 8) launch_k<8>(a, st, vec2);
     else if (kmax <= 16) launch_k<16>(a, st, vec2);
     else launch_k<32>(a, st, vec2);
+}
+
+bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
+    if (!win_enabled() || p.nbands <= 0 || a.rows || a.Xg) return false;
+    if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
+    // the window copies contiguous X rows: packed X (ldx == k), 16-byte aligned
+    if (a.ldx != a.k || ((uintptr_t)a.X % 16) != 0) return false;
+    const int kmax = a.k > a.kout ? a.k : a.kout;
+    const bool vec2 = (a.k % 2 == 0) && (a.kout % 2 == 0) && (a.ldy % 2 == 0) && ((uintptr_t)a.Y % 16 == 0);
+    if (kmax <= 1) return launch_win_k<1>(a, p, st, false);
+    if (kmax <= 2) return launch_win_k<2>(a, p, st, vec2);
+    if (kmax <= 4) return launch_win_k<4>(a, p, st, vec2);
+    if (kmax <= 8) return launch_win_k<8>(a, p, st, vec2);
+    if (kmax <= 16) return launch_win_k<16>(a, p, st, vec2);
+    return launch_win_k<32>(a, p, st, vec2);
 }
 
 }  // namespace bk

@@ -104,3 +104,69 @@ def test_halo_plan_rejects_bad_input():
         bk.plan_halo(2, 0, [0, 3, 2], [0, 1], [0])          # decreasing bounds
     with pytest.raises(bk.BkError):
         bk.plan_halo(2, 0, [0, 1, 2], [0, 1], [5])          # column out of range
+
+
+# ---------------------------------------------------------------- band plan (bk_plan_bands)
+def _check_bands(A, plan, max_extra=96):
+    """Every nonzero lies in exactly one band; bands are sorted, disjoint (gap > 4),
+    lo/hi even with lo <= dmin and hi >= dmax + 1, and extra = sum(hi - lo)."""
+    rp = A.row_ptr.numpy().astype(np.int64)
+    col = A.col.numpy().astype(np.int64)
+    rows = np.repeat(np.arange(A.n_rows), np.diff(rp))
+    d = col - rows
+    g = plan["nbands"]
+    assert 1 <= g <= 7
+    dmin, dmax = np.array(plan["dmin"]), np.array(plan["dmax"])
+    lo, hi = np.array(plan["lo"]), np.array(plan["hi"])
+    assert np.all(dmin <= dmax) and np.all(dmin[1:] > dmax[:-1] + 4)
+    assert np.all(lo % 2 == 0) and np.all(hi % 2 == 0) and np.all(lo <= dmin) and np.all(hi >= dmax + 1)
+    assert np.all(lo > dmin - 2) and np.all(hi < dmax + 3)
+    assert plan["extra_rows"] == int((hi - lo).sum()) <= max_extra
+    assert plan["width"] == list(dmax - dmin + 1) and plan["max_row_nnz"] == int((dmax - dmin + 1).sum())
+    inband = (d[:, None] >= dmin[None, :]) & (d[:, None] <= dmax[None, :])
+    assert np.all(inband.sum(axis=1) == 1)
+    assert np.diff(rp).max() <= plan["max_row_nnz"]
+    # every distinct offset is covered and each band's ends are attained offsets
+    assert set(dmin) | set(dmax) <= set(np.unique(d))
+
+
+def test_band_plan_2d_3d_stencils():
+    """5-point: bands {-nx}, {-1,0,1}, {+nx}; 7-point: also {-nx ny}, {+nx ny}."""
+    import paper_2504_02117_b200 as bk
+    A = synth.convdiff2d(128)
+    p = bk.plan_bands(A.row_ptr, A.col)
+    _check_bands(A, p)
+    assert p["dmin"] == [-128, -1, 128] and p["dmax"] == [-128, 1, 128]
+    assert p["lo"] == [-128, -2, 128] and p["hi"] == [-126, 2, 130] and p["extra_rows"] == 8
+    B = synth.diffreact3d(20)
+    p = bk.plan_bands(B.row_ptr, B.col)
+    _check_bands(B, p)
+    assert p["dmin"] == [-400, -20, -1, 20, 400] and p["max_row_nnz"] == 7
+    C = synth.richards3d(24, 24, 12)
+    _check_bands(C, bk.plan_bands(C.row_ptr, C.col))
+    # odd offsets: the +-nx bands of an odd-width grid round outward to even bounds
+    O = synth.convdiff2d(25)
+    p = bk.plan_bands(O.row_ptr, O.col)
+    _check_bands(O, p)
+    assert p["lo"] == [-26, -2, 24] and p["hi"] == [-24, 2, 26]
+
+
+def test_band_plan_rejects_unstructured_and_bad_args():
+    import paper_2504_02117_b200 as bk
+    R = synth.random_csr(300, 5000, 6, 7, empty_rows=(3, 4))
+    assert bk.plan_bands(R.row_ptr, R.col)["nbands"] == 0            # thousands of offsets
+    A = synth.convdiff2d(64)
+    assert bk.plan_bands(A.row_ptr, A.col, max_extra=4)["nbands"] == 0   # window too wide
+    # 9 isolated diagonals -> more than BK_BAND_MAX bands
+    n = 200
+    offs = [-160, -120, -80, -40, 0, 40, 80, 120, 160]
+    rp = [0]; cols = []
+    for i in range(n):
+        c = [i + o for o in offs if 0 <= i + o < n]
+        cols += c; rp.append(len(cols))
+    assert bk.plan_bands(rp, cols)["nbands"] == 0
+    assert bk.plan_bands([0], [])["nbands"] == 0                       # empty
+    with pytest.raises(bk.BkError):
+        bk.plan_bands([0, 2, 1], [0, 1])                               # decreasing row_ptr
+    with pytest.raises(bk.BkError):
+        bk.plan_bands(A.row_ptr, A.col, max_extra=-1)

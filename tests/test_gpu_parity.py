@@ -123,6 +123,67 @@ def test_spmm_edge_cases(ctx, bk):
         assert np.all(Yh[[5, 102, 199]] == 0.0)
 
 
+def _mixed_structure_csr(n_grid=40, bad=range(500, 540), seed=0):
+    """Integer 5-point stencil with a band of rows given far-away random columns: not
+    band structured, so the apply uses the gather kernel."""
+    A = synth.convdiff2d(n_grid, integer=True)
+    rp = A.row_ptr.numpy(); col = A.col.numpy(); val = A.val.numpy()
+    g = np.random.default_rng(seed)
+    nrp = [0]; ncol = []; nval = []
+    for i in range(A.n_rows):
+        if i in bad:
+            c = np.sort(g.choice(A.n_cols, 6, replace=False)); v = g.integers(-3, 4, 6).astype(np.float64)
+        else:
+            c = col[rp[i]:rp[i + 1]]; v = val[rp[i]:rp[i + 1]]
+        ncol.append(c); nval.append(v); nrp.append(nrp[-1] + len(c))
+    return synth.Csr(A.n_rows, A.n_cols, torch.tensor(nrp, dtype=torch.int32),
+                     torch.tensor(np.concatenate(ncol), dtype=torch.int32), torch.tensor(np.concatenate(nval)))
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 6, 8, 12, 16, 20, 32])
+def test_spmm_windowed_paths_bitwise(ctx, bk, k):
+    """Windowed apply (X rows of each diagonal band staged in shared memory, DESIGN.md
+    §4.1): stencils are band structured; odd n_cols (clipped last segment, odd k:
+    hand-copied last row), 3-D 5-band windows, an unstructured matrix (gather
+    kernel), coupled epilogue -- all bitwise equal to the oracle on integer inputs."""
+    cases = [synth.convdiff2d(25, integer=True),            # 625 rows: odd n_cols
+             synth.diffreact3d(12, integer=True),           # 1728 rows, 5 segments
+             _mixed_structure_csr()]
+    for A in cases:
+        M = bk.Matrix.from_csr(ctx, A)
+        info = M.info()
+        if A.name and A.name.startswith(("convdiff", "diffreact")):
+            assert info["n_bands"] in (3, 5), info
+        else:
+            assert info["n_bands"] == 0, info
+        X = synth.multivector(A.n_rows, k, 3, integer=True)
+        Y = torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
+        bk.bspmm_apply(ctx, M, cu(X), Y)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().numpy(), oracle.spmm(A, X)), (A.name, k)
+        C = synth.small_dense(k, k, 6, integer=True)
+        Y0 = synth.multivector(A.n_rows, k, 4, integer=True)
+        Y2 = cu(Y0)
+        bk.bspmm_apply(ctx, M, cu(X), Y2, C=cu(C), alpha=-2.0, beta=3.0)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y2.cpu().numpy(), oracle.spmm(A, X, C, alpha=-2.0, beta=3.0, Y=Y0)), (A.name, k)
+
+
+def test_spmm_unaligned_x_falls_back(ctx, bk):
+    """X not 16-byte aligned (the window copies need it): generic kernel, same result."""
+    A = synth.convdiff2d(40, integer=True)
+    k = 3
+    X = synth.multivector(A.n_rows, k, 3, integer=True)
+    buf = torch.zeros(A.n_rows * k + 1, dtype=torch.float64, device="cuda")
+    Xv = buf[1:].view(A.n_rows, k)
+    Xv.copy_(cu(X))
+    M = bk.Matrix.from_csr(ctx, A)
+    Y = torch.empty(A.n_rows, k, dtype=torch.float64, device="cuda")
+    bk.bspmm_apply(ctx, M, Xv, Y)
+    torch.cuda.synchronize()
+    assert np.array_equal(Y.cpu().numpy(), oracle.spmm(A, X))
+
+
 def test_spmm_rejects_bad_arguments(ctx, bk):
     A = synth.make_matrix("c1")
     M = bk.Matrix.from_csr(ctx, A)
