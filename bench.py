@@ -181,6 +181,15 @@ def run_ours(args):
     for _ in range(args.warmup):
         one_step()
     torch.cuda.synchronize()
+    if getattr(args, "profile_step", False):
+        # one step between cudaProfilerStart/Stop, for `ncu --profile-from-start off`
+        flush.fill_(1.0)
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
+        one_step()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
+        return
 
     keys = [(c, k) for k in KS for c in ("spmm", "gram", "update")] + [("solve", SOLVE_K)]
     durs = {kk: [] for kk in keys}
@@ -477,6 +486,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--profile-step", action="store_true", help="one step inside cudaProfilerStart/Stop (ncu --profile-from-start off)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=2)

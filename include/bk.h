@@ -93,6 +93,8 @@ int bk_ctx_comm_info(const bk_ctx *ctx, int *nranks, int *rank);
 int bk_csr_create(bk_ctx *ctx, bk_csr **out, int64_t n_global, int64_t row_begin,
                   int64_t n_local, const int32_t *row_ptr, const int32_t *col_global,
                   const double *val, int64_t nnz);
+/* Destroying a ctx detaches its matrices (their handles stay valid for
+ * bk_csr_destroy, which then only frees memory; any other use is an error). */
 int bk_csr_destroy(bk_csr *A);
 
 typedef struct bk_csr_info {

@@ -203,6 +203,7 @@ extern "C" int bk_ctx_destroy(bk_ctx* ctx) {
     if (!ctx) return BK_OK;
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
+    for (bk_csr* A : ctx->mats) A->ctx = nullptr;   // still valid handles; destroy frees their memory
     for (auto& b : ctx->ws)
         if (b.p) cudaFree(b.p);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
@@ -375,6 +376,7 @@ extern "C" int bk_csr_create(bk_ctx* ctx, bk_csr** out, int64_t n_global, int64_
     int rr = post_launch(ctx, "bk_csr_create");
     if (!rr) rr = cuda_check(ctx, cudaStreamSynchronize(st), "bk_csr_create sync");
     if (rr) { bk_csr_destroy(A); return rr; }
+    ctx->mats.push_back(A);
     *out = A;
     return BK_OK;
     BK_CATCH(ctx)
@@ -385,6 +387,8 @@ extern "C" int bk_csr_destroy(bk_csr* A) {
     if (A->ctx) {
         cudaSetDevice(A->ctx->device);
         cudaStreamSynchronize(A->ctx->stream);
+        auto& v = A->ctx->mats;
+        v.erase(std::remove(v.begin(), v.end(), A), v.end());
     }
     cudaFree(A->d_rp);
     cudaFree(A->d_col);

@@ -33,7 +33,9 @@ struct DevStatus {
     int breakdown_col;   // -1 if none
     int iter;            // completed (un-halted) iterations
     int gm_steps;        // GMRES: completed inner steps in the current cycle
-    int pad[3];
+    int pending_bd;      // deferred breakdown (column + 1) of an LU solve whose
+                         // result is only needed if the next convergence test fails
+    int pad[2];
     double relres[BK_MAX_K];
     double r0[BK_MAX_K];
     double omega;        // BiCGStab scalar
@@ -106,6 +108,19 @@ bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const 
                           const double* Y2, int64_t ldy2, double* d, double* d2, double* part, int* ticket,
                           int num_sms, cudaStream_t st);
 bool use_stream_kernels();
+// Fused block-BiCGStab passes (stream.cu; false = not applicable):
+// multi-operand Gram: X = [arrays[xs[0]] ..], Y = [arrays[ys[0]] ..], all kw wide
+// (kw <= 16); k x k block (i, j) of X^T Y is written to blk[i][j] (null = dropped).
+// ndot (<= 2) column dots dots[q][c] = sum_r A_q[r,c] B_q[r,c], A_q = arrays[dpair[q][0]],
+// B_q = arrays[dpair[q][1]] (kw | 32), computed in the same pass.
+bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya, const int* ys, int nin,
+                              const double* const* arrays, double* const (*blk)[2], double* part, int* ticket,
+                              int num_sms, cudaStream_t st, int ndot = 0, const int (*dpair)[2] = nullptr,
+                              double* const* dots = nullptr);
+// X += P al + w S; R = S - w T; P = R + (P - w V) be; rr_c = ||R_c||^2 (w = *w_dev); k % 8 == 0
+bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
+                            const double* V, const double* al, const double* be, const double* w_dev, double* rr,
+                            const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st);
 // d[c] = sum_i X[i,c] Y[i,c] for c < k (and optionally d2 with Y2); deterministic.
 size_t coldot_ws_doubles(int64_t n, int k, int num_sms);
 void launch_coldot(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,
@@ -123,9 +138,16 @@ void launch_pack_rows(int64_t nrows, int k, const int32_t* rows, const double* X
 // Out(k x nrhs) = G^{-1} Rhs by Cholesky; breakdown -> st->breakdown_col, st->halt.
 void sd_chol_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double tol,
                    DevStatus* st, cudaStream_t s);
-// Out = G^{-1} (sign * Rhs) by LU with partial pivoting.
+// Out = G^{-1} (sign * Rhs) by LU with partial pivoting.  defer: a breakdown
+// only records st->pending_bd (acted on by the next sd_conv_check if that test
+// does not converge) instead of halting.
+// LUo / pivo (optional, k x k and k ints): keep the factors for sd_lu_resolve.
 void sd_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign,
-                 double tol, DevStatus* st, cudaStream_t s);
+                 double tol, DevStatus* st, cudaStream_t s, int defer = 0, double* LUo = nullptr,
+                 int* pivo = nullptr);
+// Out = G^{-1} (sign Rhs) reusing sd_lu_solve's factors of G (no breakdown possible).
+void sd_lu_resolve(const double* LU, const int* piv, const double* Rhs, double* Out, int k, int nrhs, double sign,
+                   DevStatus* st, cudaStream_t s);
 // R upper (G = R^T R) and Rinv; also Racc <- R * Racc_in if Racc_in != null (Racc = R2 R1).
 void sd_chol_qr(const double* G, double* R, double* Rinv, const double* Rprev, double* Rprod,
                 int k, double tol, DevStatus* st, cudaStream_t s);
@@ -133,8 +155,9 @@ void sd_chol_qr(const double* G, double* R, double* Rinv, const double* Rprev, d
 // init != 0: store r0_c = sqrt(g_c) instead.
 void sd_conv_check(const double* g, int gstride, int k, double rtol, int conv_mode, int init,
                    DevStatus* st, cudaStream_t s);
-// BiCGStab omega = sum(ts) / sum(tt) into st->omega (breakdown if tt == 0).
-void sd_omega(const double* ts, const double* tt, int k, DevStatus* st, cudaStream_t s);
+// BiCGStab omega = sum(ts) / sum(tt) into st->omega (breakdown if tt == 0);
+// ts[c * stride], tt[c * stride] (stride k + 1: diagonals of k x k Grams).
+void sd_omega(const double* ts, const double* tt, int k, DevStatus* st, cudaStream_t s, int stride = 1);
 // Copy a k x k matrix (device) (used to roll RZ <- RZn).
 void sd_copy(const double* src, double* dst, int n, cudaStream_t s);
 // GMRES: apply stored rotations Q_0..Q_{j-1} to the new block column, QR the
@@ -169,6 +192,7 @@ struct bk_ctx {
     int* d_tickets = nullptr;     // zeroed device counters for last-CTA reductions
     size_t h_pinned_bytes = 0;
     int nranks = 1, rank = 0;
+    std::vector<bk_csr*> mats;    // live matrices (detached when the ctx is destroyed)
 #ifndef BK_NO_NCCL
     ncclComm_t comm = nullptr;
 #endif

@@ -87,7 +87,7 @@ __global__ void chol_solve_kernel(const double* __restrict__ G, const double* __
     for (int t = tid; t < k * nrhs; t += nt) Out[t] = b[(t / nrhs) * LD + t % nrhs];
 }
 
-__global__ void lu_solve_kernel(const double* __restrict__ G, const double* __restrict__ Rhs,
+__global__ void lu_solve_kernel(int defer, const double* __restrict__ G, const double* __restrict__ Rhs,
                                 double* __restrict__ Out, int k, int nrhs, double sign, double tol,
                                 DevStatus* st) {
     __shared__ double s[KM * LD];
@@ -127,7 +127,10 @@ __global__ void lu_solve_kernel(const double* __restrict__ G, const double* __re
         }
         __syncthreads();
         if (s_fail >= 0) {
-            if (tid == 0 && st) { st->breakdown_col = s_fail; st->halt = 1; }
+            if (tid == 0 && st) {
+                if (defer) st->pending_bd = s_fail + 1;
+                else { st->breakdown_col = s_fail; st->halt = 1; }
+            }
             return;
         }
         const int p = s_piv;
@@ -219,12 +222,13 @@ __global__ void conv_check_kernel(const double* __restrict__ g, int gstride, int
     }
     st->iter += 1;
     if (ok) { st->converged = 1; st->halt = 1; }
+    else if (st->pending_bd) { st->breakdown_col = st->pending_bd - 1; st->halt = 1; }
 }
 
-__global__ void omega_kernel(const double* ts, const double* tt, int k, DevStatus* st) {
+__global__ void omega_kernel(const double* ts, const double* tt, int k, int stride, DevStatus* st) {
     if (threadIdx.x != 0 || st->halt) return;
     double a = 0.0, b = 0.0;
-    for (int c = 0; c < k; ++c) { a += ts[c]; b += tt[c]; }
+    for (int c = 0; c < k; ++c) { a += ts[c * stride]; b += tt[c * stride]; }
     if (!(b > 0.0)) { st->breakdown_col = 0; st->halt = 1; return; }
     st->omega = a / b;
     st->neg_omega = -(a / b);
@@ -379,7 +383,8 @@ __global__ void gmres_backsolve_kernel(const double* __restrict__ Rtri, int ldr,
 
 // single-warp register versions (dense_warp.cu) are the default; BK_DENSE=cta
 // selects the shared-memory CTA kernels above (A/B and cross-check)
-void sdw_lu_solve(const double*, const double*, double*, int, int, double, double, DevStatus*, cudaStream_t);
+void sdw_lu_solve(const double*, const double*, double*, int, int, double, double, DevStatus*, cudaStream_t, int,
+                  double*, int*);
 void sdw_chol_solve(const double*, const double*, double*, int, int, double, DevStatus*, cudaStream_t);
 void sdw_chol_qr(const double*, double*, double*, const double*, double*, int, double, DevStatus*, cudaStream_t);
 
@@ -398,9 +403,9 @@ void sd_chol_solve(const double* G, const double* Rhs, double* Out, int k, int n
     BK_KERNEL(chol_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, tol, st));
 }
 void sd_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign, double tol,
-                 DevStatus* st, cudaStream_t s) {
-    if (!dense_cta()) return sdw_lu_solve(G, Rhs, Out, k, nrhs, sign, tol, st, s);
-    BK_KERNEL(lu_solve_kernel<<<1, 256, 0, s>>>(G, Rhs, Out, k, nrhs, sign, tol, st));
+                 DevStatus* st, cudaStream_t s, int defer, double* LUo, int* pivo) {
+    if (!dense_cta() || LUo) return sdw_lu_solve(G, Rhs, Out, k, nrhs, sign, tol, st, s, defer, LUo, pivo);
+    BK_KERNEL(lu_solve_kernel<<<1, 256, 0, s>>>(defer, G, Rhs, Out, k, nrhs, sign, tol, st));
 }
 void sd_chol_qr(const double* G, double* R, double* Rinv, const double* Rprev, double* Rprod, int k, double tol,
                 DevStatus* st, cudaStream_t s) {
@@ -411,8 +416,8 @@ void sd_conv_check(const double* g, int gstride, int k, double rtol, int conv_mo
                    cudaStream_t s) {
     BK_KERNEL(conv_check_kernel<<<1, 32, 0, s>>>(g, gstride, k, rtol, conv_mode, init, st));
 }
-void sd_omega(const double* ts, const double* tt, int k, DevStatus* st, cudaStream_t s) {
-    BK_KERNEL(omega_kernel<<<1, 32, 0, s>>>(ts, tt, k, st));
+void sd_omega(const double* ts, const double* tt, int k, DevStatus* st, cudaStream_t s, int stride) {
+    BK_KERNEL(omega_kernel<<<1, 32, 0, s>>>(ts, tt, k, stride, st));
 }
 void sd_copy(const double* src, double* dst, int n, cudaStream_t s) { BK_KERNEL(copy_kernel<<<1, 256, 0, s>>>(src, dst, n)); }
 void sd_add(const double* a, const double* b, double* out, int n, cudaStream_t s) {

@@ -21,20 +21,35 @@ __device__ __forceinline__ double wmax(double v) {
 }
 
 // LU with partial pivoting (explicit row swaps), Out = G^{-1} (sign Rhs).
-__global__ void __launch_bounds__(32) lu_solve_w(const double* __restrict__ G, const double* __restrict__ Rhs,
+// rows < k of a k x ncols row-major matrix (scaled) into smem, all loads in flight first
+__device__ __forceinline__ void load_rows_w(const double* __restrict__ src, double* dst, int k, int ncols, double scale) {
+    const int l = threadIdx.x;
+    double v[KM];
+#pragma unroll
+    for (int r = 0; r < KM; ++r) v[r] = (r < k && l < ncols) ? src[r * ncols + l] : 0.0;
+#pragma unroll
+    for (int r = 0; r < KM; ++r)
+        if (r < k && l < ncols) dst[r * LD + l] = scale * v[r];
+}
+
+// LU with partial pivoting (explicit row swaps), Out = G^{-1} (sign Rhs).
+// LUo / pivo (optional): the factors (P G = L U, unit L below the diagonal,
+// getrf layout) and the pivot row of each step, for lu_resolve_w.
+__global__ void __launch_bounds__(32) lu_solve_w(int defer, const double* __restrict__ G, const double* __restrict__ Rhs,
                                                  double* __restrict__ Out, int k, int nrhs, double sign, double tol,
-                                                 DevStatus* st) {
+                                                 DevStatus* st, double* __restrict__ LUo, int* __restrict__ pivo) {
     __shared__ double A[KM * LD], B[KM * LD];
+    __shared__ int s_piv[KM];
     if (st && st->halt) return;
     const int l = threadIdx.x;
+    load_rows_w(G, A, k, k, 1.0);
+    load_rows_w(Rhs, B, k, nrhs, sign);
+    __syncwarp();
     double mx = 0.0;
-    for (int r = 0; r < k; ++r) {
-        if (l < k) { const double g = G[r * k + l]; A[r * LD + l] = g; mx = fmax(mx, fabs(g)); }
-        if (l < nrhs) B[r * LD + l] = sign * Rhs[r * nrhs + l];
-    }
+    for (int r = 0; r < k; ++r)
+        if (l < k) mx = fmax(mx, fabs(A[r * LD + l]));
     mx = wmax(mx);
     if (!(mx > 0.0)) mx = 2.2250738585072014e-308;
-    __syncwarp();
 #pragma unroll 1
     for (int j = 0; j < k; ++j) {
         double v = (l >= j && l < k) ? fabs(A[l * LD + j]) : -1.0;
@@ -46,9 +61,13 @@ __global__ void __launch_bounds__(32) lu_solve_w(const double* __restrict__ G, c
             if (ov > v || (ov == v && op < p)) { v = ov; p = op; }
         }
         if (!(v > tol * mx)) {
-            if (l == 0 && st) { st->breakdown_col = j; st->halt = 1; }
+            if (l == 0 && st) {
+                if (defer) st->pending_bd = j + 1;
+                else { st->breakdown_col = j; st->halt = 1; }
+            }
             return;
         }
+        if (l == 0) s_piv[j] = p;
         if (p != j) {   // lane l swaps column l of rows j and p
             if (l < k) { const double t = A[j * LD + l]; A[j * LD + l] = A[p * LD + l]; A[p * LD + l] = t; }
             if (l < nrhs) { const double t = B[j * LD + l]; B[j * LD + l] = B[p * LD + l]; B[p * LD + l] = t; }
@@ -60,11 +79,47 @@ __global__ void __launch_bounds__(32) lu_solve_w(const double* __restrict__ G, c
             for (int c = j + 1; c < k; ++c) A[l * LD + c] = fma(-f, A[j * LD + c], A[l * LD + c]);
 #pragma unroll 4
             for (int c = 0; c < nrhs; ++c) B[l * LD + c] = fma(-f, B[j * LD + c], B[l * LD + c]);
+            A[l * LD + j] = f;   // L multiplier (getrf layout)
         }
         __syncwarp();
     }
     // back substitution, lane = right-hand-side column (solution overwrites B)
     if (l < nrhs) {
+#pragma unroll 1
+        for (int i = k - 1; i >= 0; --i) {
+            double v = B[i * LD + l];
+#pragma unroll 4
+            for (int q = i + 1; q < k; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
+            B[i * LD + l] = v / A[i * LD + i];
+        }
+        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
+    }
+    if (LUo && l < k)
+        for (int r = 0; r < k; ++r) LUo[r * k + l] = A[r * LD + l];
+    if (pivo && l < k) pivo[l] = s_piv[l];
+}
+
+// Out = G^{-1} (sign Rhs) from lu_solve_w's factors (getrs): b <- P b, L y = b, U x = y.
+__global__ void __launch_bounds__(32) lu_resolve_w(const double* __restrict__ LU, const int* __restrict__ piv,
+                                                   const double* __restrict__ Rhs, double* __restrict__ Out, int k,
+                                                   int nrhs, double sign, DevStatus* st) {
+    __shared__ double A[KM * LD], B[KM * LD];
+    if (st && st->halt) return;
+    const int l = threadIdx.x;
+    load_rows_w(LU, A, k, k, 1.0);
+    load_rows_w(Rhs, B, k, nrhs, sign);
+    __syncwarp();
+    if (l < nrhs) {
+#pragma unroll 1
+        for (int j = 0; j < k; ++j) {   // b <- P b (all interchanges, in order: getrs)
+            const int p = piv[j];
+            if (p != j) { const double t = B[j * LD + l]; B[j * LD + l] = B[p * LD + l]; B[p * LD + l] = t; }
+        }
+#pragma unroll 1
+        for (int j = 0; j < k; ++j) {   // L y = b (unit lower, final row order)
+            const double bj = B[j * LD + l];
+            for (int i = j + 1; i < k; ++i) B[i * LD + l] = fma(-A[i * LD + j], bj, B[i * LD + l]);
+        }
 #pragma unroll 1
         for (int i = k - 1; i >= 0; --i) {
             double v = B[i * LD + l];
@@ -177,8 +232,13 @@ __global__ void __launch_bounds__(32) chol_qr_w(const double* __restrict__ G, do
 }  // namespace
 
 void sdw_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign, double tol,
-                  DevStatus* st, cudaStream_t s) {
-    BK_KERNEL(lu_solve_w<<<1, 32, 0, s>>>(G, Rhs, Out, k, nrhs, sign, tol, st));
+                  DevStatus* st, cudaStream_t s, int defer, double* LUo, int* pivo) {
+    BK_KERNEL(lu_solve_w<<<1, 32, 0, s>>>(defer, G, Rhs, Out, k, nrhs, sign, tol, st, LUo, pivo));
+}
+
+void sd_lu_resolve(const double* LU, const int* piv, const double* Rhs, double* Out, int k, int nrhs, double sign,
+                   DevStatus* st, cudaStream_t s) {
+    BK_KERNEL(lu_resolve_w<<<1, 32, 0, s>>>(LU, piv, Rhs, Out, k, nrhs, sign, st));
 }
 
 void sdw_chol_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double tol, DevStatus* st,

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <vector>
@@ -88,6 +89,28 @@ struct Solver {
             r = allreduce_sum(ctx, d, k);
             if (!r && d2) r = allreduce_sum(ctx, d2, k);
         }
+        return r;
+    }
+    // fused multi-operand Gram (k x k blocks of [arrays[xs..]]^T [arrays[ys..]]), summed over ranks
+    int gram_multi(int nxa, const int* xs, int nya, const int* ys, int nin, const double* const* arrays,
+                   double* const (*blk)[2], int ndot = 0, const int (*dp)[2] = nullptr, double* const* dots = nullptr) {
+        rep->n_gram++;
+        double* spart = (double*)ws_get(ctx, WS_GRAM_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double));
+        if (!launch_gram_multi_stream(n, k, nxa, xs, nya, ys, nin, arrays, blk, spart, ctx->d_tickets,
+                                      ctx->num_sms, st, ndot, dp, dots))
+            return set_error(ctx, BK_ERR_UNSUPPORTED, "fused gram not applicable");
+        int r = launched("gram_multi");
+        for (int i = 0; i < nxa && !r; ++i)
+            for (int j = 0; j < nya && !r; ++j)
+                if (allred && blk[i][j]) {
+                    rep->n_allreduce++;
+                    r = allreduce_sum(ctx, blk[i][j], (int64_t)k * k);
+                }
+        for (int q = 0; q < ndot && !r; ++q)
+            if (allred) {
+                rep->n_allreduce++;
+                r = allreduce_sum(ctx, dots[q], k);
+            }
         return r;
     }
     // out = a Xin + s P C (+ w W), optionally halted
@@ -206,6 +229,25 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
 }
 
 // ---------------------------------------------------------------- O6 block BiCGStab
+// Fused pass structure, same steps and order of the O6 recurrences:
+//   V = A P                          (windowed apply)
+//   [M1 RR] = Rt^T [V R]             (one pass over Rt, V, R)
+//   al = M1^-1 RR ; S = R - V al
+//   T = A S
+//   RtT = Rt^T T, ts = <T_c,S_c>, tt = <T_c,T_c>   (one pass: DMMA Gram + FMA column dots)
+//   w = sum ts / sum tt ; be = -M1^-1 RtT (M1's LU factors from the al solve)
+//   X += P al + w S ; R = S - w T ; P = R + (P - w V) be ; rr = ||R_c||^2   (one pass)
+//   convergence test on rr
+// 21 N x k passes per iteration instead of 28 for the unfused sequence.
+static bool fused_bicgstab_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("BK_FUSED");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
     const int k = S.k;
     double* R = S.vec();
@@ -217,7 +259,8 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     double* Tmp = S.vec();
     double* sm = S.small(8 * 32 * 32);
     double *M1 = sm, *RR = sm + 1024, *al = sm + 2048, *RtT = sm + 3072, *be = sm + 4096, *ts = sm + 5120,
-           *tt = sm + 5120 + 32, *nr = sm + 5120 + 64;
+           *tt = sm + 5120 + 32, *nr = sm + 5120 + 64, *LUf = sm + 6144;
+    int* piv = reinterpret_cast<int*>(sm + 7168);
     TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
     TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
     sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
@@ -226,24 +269,58 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     const double tol = S.o->breakdown_tol;
     const double* om = &S.ds->omega;
     const double* nom = &S.ds->neg_omega;
+    const bool fused = fused_bicgstab_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
+                       ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
     for (int it = 0; it < S.o->max_iters; ++it) {
         TRY(S.spmm(P, k, V, k));
-        TRY(S.gram(Rt, k, k, V, k, M1));
-        TRY(S.gram(Rt, k, k, R, k, RR));
-        sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st);
+        if (fused) {
+            const double* arr[3] = {Rt, V, R};
+            const int xs[1] = {0}, ys[2] = {1, 2};
+            double* const blk[3][2] = {{M1, RR}, {nullptr, nullptr}, {nullptr, nullptr}};
+            TRY(S.gram_multi(1, xs, 2, ys, 3, arr, blk));
+        } else {
+            TRY(S.gram(Rt, k, k, V, k, M1));
+            TRY(S.gram(Rt, k, k, R, k, RR));
+        }
+        if (fused) sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st, 0, LUf, piv);   // factors kept for be
+        else sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st);
         TRY(S.upd(Sv, k, 1.0, R, k, -1.0, V, k, k, al));
         TRY(S.spmm(Sv, k, T, k));
-        TRY(S.coldot(T, k, Sv, k, T, k, ts, tt));
-        sd_omega(ts, tt, k, S.ds, S.st);
-        TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al, Sv, k, 1.0, om));
-        TRY(S.upd(R, k, 1.0, Sv, k, 0.0, nullptr, k, 0, nullptr, T, k, 1.0, nom));
-        TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
-        sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
-        TRY(S.gram(Rt, k, k, T, k, RtT));
-        sd_lu_solve(M1, RtT, be, k, k, -1.0, tol, S.ds, S.st);
-        S.rep->n_small += 4;
-        TRY(S.upd(Tmp, k, 1.0, P, k, 0.0, nullptr, k, 0, nullptr, V, k, 1.0, nom));
-        TRY(S.upd(P, k, 1.0, R, k, 1.0, Tmp, k, k, be));
+        if (fused) {
+            const double* arr[3] = {Rt, Sv, T};
+            const int xs[1] = {0}, ys[1] = {2};
+            double* const blk[3][2] = {{RtT, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+            const int dp[2][2] = {{2, 1}, {2, 2}};   // <T,S>, <T,T> per column
+            double* const dots[2] = {ts, tt};
+            TRY(S.gram_multi(1, xs, 1, ys, 3, arr, blk, 2, dp, dots));
+            sd_omega(ts, tt, k, S.ds, S.st);
+            sd_lu_resolve(LUf, piv, RtT, be, k, k, -1.0, S.ds, S.st);   // same M1: no new breakdown
+            S.rep->n_update += 3;
+            S.rep->n_gram++;
+            double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
+            if (!launch_bcg_tail_stream(S.n, k, X, R, P, Sv, T, V, al, be, om, nr, &S.ds->halt, spart,
+                                        S.ctx->d_tickets, S.ctx->num_sms, S.st))
+                return set_error(S.ctx, BK_ERR_UNSUPPORTED, "fused BiCGStab tail not applicable");
+            TRY(S.launched("bcg_tail"));
+            if (S.allred) {
+                S.rep->n_allreduce++;
+                TRY(allreduce_sum(S.ctx, nr, k));
+            }
+            sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
+            S.rep->n_small += 4;
+        } else {
+            TRY(S.coldot(T, k, Sv, k, T, k, ts, tt));
+            sd_omega(ts, tt, k, S.ds, S.st);
+            TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al, Sv, k, 1.0, om));
+            TRY(S.upd(R, k, 1.0, Sv, k, 0.0, nullptr, k, 0, nullptr, T, k, 1.0, nom));
+            TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
+            sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
+            TRY(S.gram(Rt, k, k, T, k, RtT));
+            sd_lu_solve(M1, RtT, be, k, k, -1.0, tol, S.ds, S.st);
+            S.rep->n_small += 4;
+            TRY(S.upd(Tmp, k, 1.0, P, k, 0.0, nullptr, k, 0, nullptr, V, k, 1.0, nom));
+            TRY(S.upd(P, k, 1.0, R, k, 1.0, Tmp, k, k, be));
+        }
         if ((it + 1) % S.o->check_every == 0 || it + 1 == S.o->max_iters) {
             TRY(S.poll());
             if (S.hs->halt) break;

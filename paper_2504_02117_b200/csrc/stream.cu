@@ -37,10 +37,11 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
 }
 
 // Up to 3 contiguous row-major operands streamed tile by tile.
+constexpr int MAXS = 5;            // operands per stream tile
 struct Streams {
-    const double* p[3];
-    int w[3];        // doubles per row (0 = unused)
-    int off[3];      // byte offset of the operand inside a stage
+    const double* p[MAXS];
+    int w[MAXS];     // doubles per row (0 = unused)
+    int off[MAXS];   // byte offset of the operand inside a stage
     int nin;
     int T;           // rows per tile
     int64_t n;
@@ -266,6 +267,16 @@ struct GramStream {
     int* ticket;
     double* G;          // gram: ka x kb; coldot: d[k]
     double* G2;         // coldot second output
+    // multi-operand Gram (mode 2): X = [S.p[xs[0]] ... ], Y = [S.p[ys[0]] ...], every
+    // array kw wide; output block (i, j) (kw x kw) goes to blk[i][j] (null = dropped)
+    int mode;           // 0 gram, 1 coldot, 2 multi-operand gram
+    int kw, nxa, nya;
+    int xs[3], ys[2];
+    double* blk[3][2];
+    // mode 2 extra: column dots dots[q][c] = sum_r S.p[da[q]][r,c] * S.p[db[q]][r,c] (FMA, q < ndot)
+    int ndot;
+    int da[2], db[2];
+    double* dots[2];
 };
 
 // NSET independent accumulator sets (quads alternate between them) so the
@@ -355,6 +366,19 @@ __device__ __forceinline__ void finish_reduce(const GramStream& Gs, double* s_re
             idx = which * 32 + c;
             dst = c;
             G = which ? Gs.G2 : Gs.G;
+        } else if (Gs.mode == 2) {
+            if (o < Gs.ka * Gs.kb) {
+                const int a = o / kb_real, b = o % kb_real;
+                idx = a * ld_out + b;
+                dst = (a % Gs.kw) * Gs.kw + (b % Gs.kw);
+                G = Gs.blk[a / Gs.kw][b / Gs.kw];
+            } else {   // column dots after the Gram block (NOUT - 64 + q * 32 + c)
+                const int o2 = o - Gs.ka * Gs.kb, q = o2 / Gs.kw, c = o2 % Gs.kw;
+                idx = NOUT - 64 + q * 32 + c;
+                dst = c;
+                G = Gs.dots[q];
+            }
+            if (!G) continue;
         } else {
             const int a = o / kb_real, b = o % kb_real;
             idx = a * ld_out + b;
@@ -583,6 +607,232 @@ void gram_stream_t(const GramStream& Gs, int grid, cudaStream_t st) {
 
 }  // namespace
 
+// ------------------------------------------------------------------ fused block-BiCGStab passes
+// Multi-operand Gram on the FP64 tensor cores: G = [X_0 X_1 ..]^T [Y_0 Y_1 ..]
+// with every X_i / Y_j one kw-wide stream of the tile (an array read once even
+// if it appears in X and Y).  Column c of X is column c % kw of array c / kw.
+template <int NA, int NB>
+__device__ __forceinline__ void gram_tile_multi(const GramStream& Gs, const double* const (&base)[MAXS], int nr,
+                                                double (&acc)[NA][NB][2]) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int kq = lane & 3, mg = lane >> 2;
+    const int kw = Gs.kw, ka = Gs.ka, kb = Gs.kb;
+    const double* xb[NA];
+    const double* yb[NB];
+#pragma unroll
+    for (int i = 0; i < NA; ++i) {
+        const int c = 8 * i + mg;
+        xb[i] = c < ka ? base[Gs.xs[c / kw]] + (c % kw) : nullptr;
+    }
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+        const int c = 8 * j + mg;
+        yb[j] = c < kb ? base[Gs.ys[c / kw]] + (c % kw) : nullptr;
+    }
+    for (int q0 = 4 * warp; q0 < nr; q0 += 4 * (NC / 32)) {
+        const int r = q0 + kq;
+        const bool rin = r < nr;
+        double av[NA], bv[NB];
+#pragma unroll
+        for (int i = 0; i < NA; ++i) av[i] = (rin && xb[i]) ? xb[i][(int64_t)r * kw] : 0.0;
+#pragma unroll
+        for (int j = 0; j < NB; ++j) bv[j] = (rin && yb[j]) ? yb[j][(int64_t)r * kw] : 0.0;
+#pragma unroll
+        for (int i = 0; i < NA; ++i)
+#pragma unroll
+            for (int j = 0; j < NB; ++j) dmma(acc[i][j][0], acc[i][j][1], av[i], bv[j]);
+    }
+}
+
+template <int NA, int NB>
+__global__ void __launch_bounds__(NC + 32, 2) gram_multi_stream_kernel(const GramStream Gs) {
+    constexpr int KAP = 8 * NA, KBP = 8 * NB, NOUT = KAP * KBP + 64;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(Gs.S, smem, full, empty, s_direct);
+        return;
+    }
+    double acc[NA][NB][2];
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    // column dots: flattened walk over the tile (kw | 32: thread t sees column t % kw)
+    const int kw = Gs.kw;
+    double dd[2] = {0.0, 0.0};
+    int it = 0;
+    for (int tile = blockIdx.x; tile < Gs.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * Gs.S.T;
+        const int nr = (int)((Gs.S.n - r0) < Gs.S.T ? (Gs.S.n - r0) : Gs.S.T);
+        const unsigned char* st = smem + s * STAGE_BYTES;
+        const double* base[MAXS];
+#pragma unroll
+        for (int q = 0; q < MAXS; ++q)
+            base[q] = q < Gs.S.nin ? (s_direct[s] ? Gs.S.p[q] + r0 * Gs.S.w[q]
+                                                  : reinterpret_cast<const double*>(st + Gs.S.off[q]))
+                                   : nullptr;
+        gram_tile_multi<NA, NB>(Gs, base, nr, acc);
+        if (Gs.ndot > 0) {
+            const int ne = nr * kw;
+            const double *a0 = base[Gs.da[0]], *b0 = base[Gs.db[0]];
+            const double *a1 = Gs.ndot > 1 ? base[Gs.da[1]] : a0, *b1 = Gs.ndot > 1 ? base[Gs.db[1]] : b0;
+            for (int e = threadIdx.x; e < ne; e += NC) {
+                dd[0] = fma(a0[e], b0[e], dd[0]);
+                dd[1] = fma(a1[e], b1[e], dd[1]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    for (int m = 16; m >= kw; m >>= 1) {   // lanes l, l + kw, ... share a column: fixed xor tree
+        dd[0] += __shfl_xor_sync(0xffffffffu, dd[0], m);
+        dd[1] += __shfl_xor_sync(0xffffffffu, dd[1], m);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    double* s_red = reinterpret_cast<double*>(smem);
+    if (lane < kw) {
+        s_red[warp * NOUT + NOUT - 64 + lane] = dd[0];
+        s_red[warp * NOUT + NOUT - 32 + lane] = dd[1];
+    }
+    const int kq = lane & 3, mg = lane >> 2;
+#pragma unroll
+    for (int i = 0; i < NA; ++i)
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + 8 * j + 2 * kq;
+            d[0] = acc[i][j][0];
+            d[1] = acc[i][j][1];
+        }
+    finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb + Gs.ndot * kw, Gs.kb, KBP, false);
+}
+
+// BiCGStab tail, one pass (O6 steps in order):
+//   X <- X + P al + w S ;  R <- S - w T ;  P <- R + (P - w V) be ;  rr_c = sum_r R[r,c]^2
+// al, be: k x k (B fragments in registers); w = *w_dev.  Streams: 0 X, 1 P, 2 S, 3 T, 4 V.
+struct BcgTail {
+    Streams S;
+    int k;
+    const double* al;
+    const double* be;
+    const double* w_dev;
+    double* X;
+    double* R;
+    double* P;
+    const int* halt;
+    GramStream red;     // coldot-mode reduction of rr (part, ticket, G = rr)
+};
+
+template <int NQ, int NK>
+__global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTail U) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    if (U.halt && *U.halt) return;
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(U.S, smem, full, empty, s_direct);
+        return;
+    }
+    const int k = U.k, kq = lane & 3, mg = lane >> 2;
+    // B fragments: lane holds al / be [4 ks + kq][8 nb + mg]
+    double ba[NQ][NK], bb[NQ][NK];
+#pragma unroll
+    for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+        for (int nb = 0; nb < NK; ++nb) {
+            ba[ks][nb] = U.al[(4 * ks + kq) * k + 8 * nb + mg];
+            bb[ks][nb] = U.be[(4 * ks + kq) * k + 8 * nb + mg];
+        }
+    const double w = *U.w_dev;
+    double rr[NK][2];
+#pragma unroll
+    for (int nb = 0; nb < NK; ++nb) rr[nb][0] = rr[nb][1] = 0.0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < U.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * U.S.T;
+        const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
+        const unsigned char* st = smem + s * STAGE_BYTES;
+        const double* b[5];
+#pragma unroll
+        for (int q = 0; q < 5; ++q)
+            b[q] = s_direct[s] ? U.S.p[q] + r0 * k : reinterpret_cast<const double*>(st + U.S.off[q]);
+        const double *Xt = b[0], *Pt = b[1], *St = b[2], *Tt = b[3], *Vt = b[4];
+        for (int rb = 8 * warp; rb < nr; rb += 8 * (NC / 32)) {
+            const int r = rb + mg;
+            const bool rin = r < nr;
+            double ap[NQ], aq[NQ];   // A fragments: P and P - w V (row mg, col 4 ks + kq)
+#pragma unroll
+            for (int ks = 0; ks < NQ; ++ks) {
+                const double p = rin ? Pt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+                const double v = rin ? Vt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+                ap[ks] = p;
+                aq[ks] = fma(-w, v, p);
+            }
+#pragma unroll
+            for (int nb = 0; nb < NK; ++nb) {
+                const int c = 8 * nb + 2 * kq;
+                double x0 = 0.0, x1 = 0.0, r0v = 0.0, r1v = 0.0;
+                if (rin) {
+                    const double2 xv = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
+                    const double2 sv = *reinterpret_cast<const double2*>(St + (int64_t)r * k + c);
+                    const double2 tv = *reinterpret_cast<const double2*>(Tt + (int64_t)r * k + c);
+                    x0 = fma(w, sv.x, xv.x);
+                    x1 = fma(w, sv.y, xv.y);
+                    r0v = fma(-w, tv.x, sv.x);
+                    r1v = fma(-w, tv.y, sv.y);
+                }
+                double p0 = r0v, p1 = r1v;
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) {
+                    dmma(x0, x1, ap[ks], ba[ks][nb]);
+                    dmma(p0, p1, aq[ks], bb[ks][nb]);
+                }
+                if (rin) {
+                    const int64_t o = (r0 + r) * k + c;
+                    *reinterpret_cast<double2*>(U.X + o) = make_double2(x0, x1);
+                    *reinterpret_cast<double2*>(U.R + o) = make_double2(r0v, r1v);
+                    *reinterpret_cast<double2*>(U.P + o) = make_double2(p0, p1);
+                    rr[nb][0] = fma(r0v, r0v, rr[nb][0]);
+                    rr[nb][1] = fma(r1v, r1v, rr[nb][1]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // column sums over the 8 row groups (lanes with equal kq): fixed xor tree
+#pragma unroll
+    for (int nb = 0; nb < NK; ++nb)
+#pragma unroll
+        for (int m = 4; m <= 16; m <<= 1) {
+            rr[nb][0] += __shfl_xor_sync(0xffffffffu, rr[nb][0], m);
+            rr[nb][1] += __shfl_xor_sync(0xffffffffu, rr[nb][1], m);
+        }
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    double* s_red = reinterpret_cast<double*>(smem);
+    if (mg == 0) {
+#pragma unroll
+        for (int nb = 0; nb < NK; ++nb) {
+            s_red[warp * 64 + 8 * nb + 2 * kq] = rr[nb][0];
+            s_red[warp * 64 + 8 * nb + 2 * kq + 1] = rr[nb][1];
+        }
+    }
+    finish_reduce<64>(U.red, s_red, k, k, 32, true);
+}
+
 // ------------------------------------------------------------------ launchers (return false = not applicable)
 // CTA partials + group partials (<= 32 groups of 16), NOUT <= 1024 each
 size_t stream_part_doubles(int num_sms) { return (size_t)(2 * num_sms + 40) * 1024; }
@@ -722,6 +972,89 @@ bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const 
     if (!a) { set_smem((const void*)coldot_stream_kernel, smem); a = true; }
     BK_KERNEL(coldot_stream_kernel<<<grid, NC + 32, smem, st>>>(Gs));
     return true;
+}
+
+// Stream geometry shared by the fused launchers: nin operands of width w each.
+static void stream_geom(Streams& S, int nin, int64_t n) {
+    int bpr = 0;
+    for (int j = 0; j < nin; ++j) bpr += S.w[j] * 8;
+    S.nin = nin;
+    S.T = tile_rows_for(bpr);
+    auto lay = [&]() {
+        int off = 0;
+        for (int j = 0; j < nin; ++j) { S.off[j] = off; off += S.T * S.w[j] * 8; off = (off + 127) & ~127; }
+        return off;
+    };
+    while (lay() > STAGE_BYTES && S.T > 8) S.T = (S.T / 2) & ~7;
+    S.n = n;
+    S.ntiles = (int)((n + S.T - 1) / S.T);
+}
+
+bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya, const int* ys, int nin,
+                              const double* const* arrays, double* const (*blk)[2], double* part, int* ticket,
+                              int num_sms, cudaStream_t st, int ndot, const int (*dpair)[2], double* const* dots) {
+    if (kw < 1 || kw > 16 || n <= 0 || nin < 1 || nin > MAXS || nxa < 1 || nxa > 3 || nya < 1 || nya > 2) return false;
+    if (ndot < 0 || ndot > 2 || (ndot > 0 && 32 % kw != 0)) return false;
+    GramStream Gs{};
+    for (int q = 0; q < nin; ++q) {
+        if ((uintptr_t)arrays[q] & 15) return false;
+        Gs.S.p[q] = arrays[q];
+        Gs.S.w[q] = kw;
+    }
+    stream_geom(Gs.S, nin, n);
+    Gs.mode = 2; Gs.kw = kw; Gs.nxa = nxa; Gs.nya = nya;
+    for (int i = 0; i < nxa; ++i) Gs.xs[i] = xs[i];
+    for (int j = 0; j < nya; ++j) Gs.ys[j] = ys[j];
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 2; ++j) Gs.blk[i][j] = (i < nxa && j < nya) ? blk[i][j] : nullptr;
+    Gs.ka = nxa * kw; Gs.kb = nya * kw; Gs.part = part; Gs.ticket = ticket;
+    Gs.ndot = ndot;
+    for (int q = 0; q < ndot; ++q) { Gs.da[q] = dpair[q][0]; Gs.db[q] = dpair[q][1]; Gs.dots[q] = dots[q]; }
+    const int grid = grid_for(Gs.S.ntiles, num_sms);
+    const int na = (Gs.ka + 7) / 8, nb = (Gs.kb + 7) / 8;
+    const int smem = NSTAGE * STAGE_BYTES + 128;
+#define BK_GM(A, B)                                                                              \
+    if (na == A && nb == B) {                                                                    \
+        static_assert((NC / 32) * (64 * A * B + 64) * 8 <= NSTAGE * STAGE_BYTES, "combine buffer"); \
+        static bool at = false;                                                                  \
+        if (!at) { set_smem((const void*)gram_multi_stream_kernel<A, B>, smem); at = true; }     \
+        BK_KERNEL(gram_multi_stream_kernel<A, B><<<grid, NC + 32, smem, st>>>(Gs));               \
+        return true;                                                                             \
+    }
+    // kw <= 8: (1..3) x (1..2) blocks of 8; kw = 16: (2..6) x (2..4)
+    BK_GM(1, 1) BK_GM(1, 2) BK_GM(2, 1) BK_GM(3, 1) BK_GM(2, 2) BK_GM(3, 2)
+    BK_GM(2, 4) BK_GM(4, 2) BK_GM(6, 2) BK_GM(4, 4)
+#undef BK_GM
+    return false;
+}
+
+bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
+                            const double* V, const double* al, const double* be, const double* w_dev, double* rr,
+                            const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st) {
+    if (n <= 0 || k % 8 != 0 || k > 32) return false;
+    const double* arr[5] = {X, P, S, T, V};
+    BcgTail U{};
+    for (int q = 0; q < 5; ++q) {
+        if ((uintptr_t)arr[q] & 15) return false;
+        U.S.p[q] = arr[q];
+        U.S.w[q] = k;
+    }
+    if ((uintptr_t)R & 15) return false;
+    stream_geom(U.S, 5, n);
+    U.k = k; U.al = al; U.be = be; U.w_dev = w_dev; U.X = X; U.R = R; U.P = P; U.halt = halt;
+    U.red.part = part; U.red.ticket = ticket; U.red.G = rr; U.red.G2 = nullptr;
+    const int grid = grid_for(U.S.ntiles, num_sms);
+    const int smem = NSTAGE * STAGE_BYTES + 128;
+#define BK_BT(Q, K)                                                                              \
+    if (k == 8 * K) {                                                                            \
+        static bool at = false;                                                                  \
+        if (!at) { set_smem((const void*)bcg_tail_stream_kernel<Q, K>, smem); at = true; }       \
+        BK_KERNEL(bcg_tail_stream_kernel<Q, K><<<grid, NC + 32, smem, st>>>(U));                  \
+        return true;                                                                             \
+    }
+    BK_BT(2, 1) BK_BT(4, 2) BK_BT(6, 3) BK_BT(8, 4)
+#undef BK_BT
+    return false;
 }
 
 }  // namespace bk

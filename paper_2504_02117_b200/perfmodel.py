@@ -72,8 +72,22 @@ def coldot_bytes(n: int, k: int, n_y: int = 1) -> int:
     return D * n * k * (1 + n_y)
 
 
-def bicgstab_iter_bytes(n: int, nnz: int, k: int) -> int:
-    """One block BiCGStab iteration as enqueued by solve.cpp (DESIGN.md §3 O6)."""
+def bicgstab_fused(k: int) -> bool:
+    """Whether solve.cpp takes the fused BiCGStab passes (k % 8 == 0, k <= 16)."""
+    return k % 8 == 0 and k <= 16
+
+
+def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> int:
+    """One block BiCGStab iteration as enqueued by solve.cpp (DESIGN.md §3 O6, §4.4).
+
+    Fused (default where solve.cpp fuses): 2 applies + [Rt V R] Gram pass (3 N x k reads)
+    + S = R - V alpha (2 reads, 1 write) + [Rt S T] Gram pass (3 reads) + the tail
+    X, R, P update with ||R|| (5 reads, 3 writes) = 21 N x k passes + 2 CSR streams."""
+    if fused is None:
+        fused = bicgstab_fused(k)
+    if fused:
+        v = 8 * n * k
+        return 2 * spmm_bytes(n, nnz, k) + 3 * v + update_bytes(n, k, k) + 3 * v + 8 * v
     b = 2 * spmm_bytes(n, nnz, k)                     # V = A P, T = A S
     b += 3 * gram_bytes(n, k, k)                      # Rt^T V, Rt^T R, Rt^T T
     b += coldot_bytes(n, k, 2) + coldot_bytes(n, k, 1)  # <T,S>, <T,T>; ||R||

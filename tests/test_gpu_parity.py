@@ -265,10 +265,13 @@ def test_update_integer_bitwise_and_inplace(ctx, bk):
 # ----------------------------------------------------------------------------- a6 solve
 SOLVES = [("cg", "c1s", {}), ("gmres", "c1", {"restart": 100}), ("gmres", "c1", {"restart": 20}),
           ("bicgstab", "c1", {}), ("cg", "c1s", {"precond": "jacobi"})]
+# k = 8, 16 take the fused BiCGStab passes; k = 1, 4 the unfused ones.
+# (GMRES(20) at k = 16 stagnates on c1 in the oracle as well: not a parity case.)
+SOLVE_CASES = [(m, c, kw, k) for (m, c, kw) in SOLVES for k in (1, 4, 8, 16)
+               if not (m == "gmres" and kw.get("restart") == 20 and k == 16)]
 
 
-@pytest.mark.parametrize("method,cfg,kw", SOLVES)
-@pytest.mark.parametrize("k", [1, 4])
+@pytest.mark.parametrize("method,cfg,kw,k", SOLVE_CASES)
 def test_solve_matches_oracle(ctx, bk, method, cfg, kw, k):
     A = synth.make_matrix(cfg)
     B = synth.multivector(A.n_rows, k, 2)
@@ -314,6 +317,22 @@ def test_solve_duplicated_rhs_breakdown_status(ctx, bk):
     _, rr = oracle.block_cg(A, B)
     assert st == bk.BK_BREAKDOWN and rep["status"] == "breakdown"
     assert rep["breakdown_column"] == rr.breakdown_column == 2
+    assert torch.all(torch.isfinite(X))
+
+
+@pytest.mark.parametrize("k", [3, 8])
+def test_bicgstab_duplicated_rhs_breakdown_status(ctx, bk, k):
+    """Rt^T V singular (a duplicated right-hand side): breakdown status and column as
+    the oracle, on the unfused (k = 3) and the fused (k = 8) pass structure."""
+    A = synth.make_matrix("c1")
+    b = synth.multivector(A.n_rows, k - 1, 2)
+    B = torch.cat([b, b[:, :1]], dim=1)
+    X = torch.zeros(A.n_rows, k, dtype=torch.float64, device="cuda")
+    st, rep = bk.block_krylov_solve(ctx, bk.Matrix.from_csr(ctx, A), cu(B), X, method="bicgstab",
+                                    x0_is_zero=True)
+    _, rr = oracle.block_bicgstab(A, B)
+    assert st == bk.BK_BREAKDOWN and rep["status"] == "breakdown"
+    assert rep["breakdown_column"] == rr.breakdown_column == k - 1
     assert torch.all(torch.isfinite(X))
 
 
