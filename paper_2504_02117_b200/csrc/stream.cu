@@ -277,12 +277,16 @@ struct GramStream {
     int ndot;
     int da[2], db[2];
     double* dots[2];
+    // panel Gram (16-column panels): X panel p = columns [xpo[p], xpo[p] + 16) of stream xps[p]
+    int nxp, nyp;
+    int xps[4], xpo[4], yps[4], ypo[4];
 };
 
 // NSET independent accumulator sets (quads alternate between them) so the
 // DMMA accumulation is not one long dependent chain per warp.
+// (register cap 96 at 2 CTAs x 288 threads: more sets spill in the hot loop)
 template <int NA, int NB>
-struct GramSets { static constexpr int NSET = (NA * NB <= 4) ? 4 : ((NA * NB <= 9) ? 2 : 1); };
+struct GramSets { static constexpr int NSET = (NA * NB <= 2) ? 4 : ((NA * NB <= 4) ? 2 : 1); };
 
 template <int NA, int NB>
 __device__ __forceinline__ void gram_tile(const GramStream& Gs, const double* Xt, const double* Yt, int nr,
@@ -714,6 +718,123 @@ __global__ void __launch_bounds__(NC + 32, 2) gram_multi_stream_kernel(const Gra
     finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb + Gs.ndot * kw, Gs.kb, KBP, false);
 }
 
+// Panel Gram: X and Y are lists of 16-column panels.  Lane (mg, kq) loads the
+// 16-byte chunk mg (columns 2mg, 2mg+1) of row q0 + kq of each panel with one
+// LDS.128 -- 4 rows x 8 chunks = 512 bytes, conflict-free (the 8-byte
+// fragment loads of 16-wide rows were 4-way conflicted) -- and the two columns
+// feed two PARITY blocks (even / odd columns of the panel) as m8n8k4 DMMA
+// fragments; only the output index mapping changes:
+// block (2p + e, 2q + f), fragment (m, n) -> G[16p + 2m + e][16q + 2n + f].
+template <int NXP, int NYP>
+struct PanelSets { static constexpr int NSET = (NXP * NYP <= 1) ? 2 : 1; };
+
+template <int NXP, int NYP>
+__global__ void __launch_bounds__(NC + 32, 2) gram_panel_stream_kernel(const GramStream Gs) {
+    constexpr int KA = 16 * NXP, KB = 16 * NYP, NOUT = KA * KB + 64;
+    constexpr int NSET = PanelSets<NXP, NYP>::NSET;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(Gs.S, smem, full, empty, s_direct);
+        return;
+    }
+    const int kq = lane & 3, mg = lane >> 2;
+    double acc[NSET][2 * NXP][2 * NYP][2];
+#pragma unroll
+    for (int t = 0; t < NSET; ++t)
+#pragma unroll
+        for (int i = 0; i < 2 * NXP; ++i)
+#pragma unroll
+            for (int j = 0; j < 2 * NYP; ++j) acc[t][i][j][0] = acc[t][i][j][1] = 0.0;
+    const int kw = Gs.kw;
+    double dd[2] = {0.0, 0.0};
+    int it = 0;
+    for (int tile = blockIdx.x; tile < Gs.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * Gs.S.T;
+        const int nr = (int)((Gs.S.n - r0) < Gs.S.T ? (Gs.S.n - r0) : Gs.S.T);
+        const unsigned char* st = smem + s * STAGE_BYTES;
+        const double* base[MAXS];
+#pragma unroll
+        for (int q = 0; q < MAXS; ++q)
+            base[q] = q < Gs.S.nin ? (s_direct[s] ? Gs.S.p[q] + r0 * Gs.S.w[q]
+                                                  : reinterpret_cast<const double*>(st + Gs.S.off[q]))
+                                   : nullptr;
+        const double* xb[NXP];
+        const double* yb[NYP];
+        int xw[NXP], yw[NYP];
+#pragma unroll
+        for (int p = 0; p < NXP; ++p) { xb[p] = base[Gs.xps[p]] + Gs.xpo[p] + 2 * mg; xw[p] = Gs.S.w[Gs.xps[p]]; }
+#pragma unroll
+        for (int p = 0; p < NYP; ++p) { yb[p] = base[Gs.yps[p]] + Gs.ypo[p] + 2 * mg; yw[p] = Gs.S.w[Gs.yps[p]]; }
+        for (int q0 = 4 * warp; q0 < nr; q0 += 4 * (NC / 32) * NSET) {
+            double2 a[NSET][NXP], b[NSET][NYP];
+#pragma unroll
+            for (int t = 0; t < NSET; ++t) {
+                const int r = q0 + 4 * (NC / 32) * t + kq;
+                const bool rin = r < nr;
+#pragma unroll
+                for (int p = 0; p < NXP; ++p)
+                    a[t][p] = rin ? *reinterpret_cast<const double2*>(xb[p] + (int64_t)r * xw[p]) : make_double2(0.0, 0.0);
+#pragma unroll
+                for (int p = 0; p < NYP; ++p)
+                    b[t][p] = rin ? *reinterpret_cast<const double2*>(yb[p] + (int64_t)r * yw[p]) : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int t = 0; t < NSET; ++t)
+#pragma unroll
+                for (int p = 0; p < NXP; ++p)
+#pragma unroll
+                    for (int q = 0; q < NYP; ++q) {
+                        dmma(acc[t][2 * p][2 * q][0], acc[t][2 * p][2 * q][1], a[t][p].x, b[t][q].x);
+                        dmma(acc[t][2 * p][2 * q + 1][0], acc[t][2 * p][2 * q + 1][1], a[t][p].x, b[t][q].y);
+                        dmma(acc[t][2 * p + 1][2 * q][0], acc[t][2 * p + 1][2 * q][1], a[t][p].y, b[t][q].x);
+                        dmma(acc[t][2 * p + 1][2 * q + 1][0], acc[t][2 * p + 1][2 * q + 1][1], a[t][p].y, b[t][q].y);
+                    }
+        }
+        if (Gs.ndot > 0) {
+            const int ne = nr * kw;
+            const double *a0 = base[Gs.da[0]], *b0 = base[Gs.db[0]];
+            const double *a1 = Gs.ndot > 1 ? base[Gs.da[1]] : a0, *b1 = Gs.ndot > 1 ? base[Gs.db[1]] : b0;
+            for (int e = threadIdx.x; e < ne; e += NC) {
+                dd[0] = fma(a0[e], b0[e], dd[0]);
+                dd[1] = fma(a1[e], b1[e], dd[1]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    for (int m = 16; m >= kw; m >>= 1) {
+        dd[0] += __shfl_xor_sync(0xffffffffu, dd[0], m);
+        dd[1] += __shfl_xor_sync(0xffffffffu, dd[1], m);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    double* s_red = reinterpret_cast<double*>(smem);
+    if (lane < kw && kw <= 32) {
+        s_red[warp * NOUT + NOUT - 64 + lane] = dd[0];
+        s_red[warp * NOUT + NOUT - 32 + lane] = dd[1];
+    }
+#pragma unroll
+    for (int i = 0; i < 2 * NXP; ++i)
+#pragma unroll
+        for (int j = 0; j < 2 * NYP; ++j) {
+            double v0 = acc[0][i][j][0], v1 = acc[0][i][j][1];
+#pragma unroll
+            for (int t = 1; t < NSET; ++t) { v0 += acc[t][i][j][0]; v1 += acc[t][i][j][1]; }   // fixed order
+            const int a = 16 * (i >> 1) + 2 * mg + (i & 1);
+            const int b = 16 * (j >> 1) + 4 * kq + (j & 1);
+            s_red[warp * NOUT + a * KB + b] = v0;
+            s_red[warp * NOUT + a * KB + b + 2] = v1;
+        }
+    finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb + (Gs.mode == 2 ? Gs.ndot * kw : 0), Gs.kb, KB, false);
+}
+
 // BiCGStab tail, one pass (O6 steps in order):
 //   X <- X + P al + w S ;  R <- S - w T ;  P <- R + (P - w V) be ;  rr_c = sum_r R[r,c]^2
 // al, be: k x k (B fragments in registers); w = *w_dev.  Streams: 0 X, 1 P, 2 S, 3 T, 4 V.
@@ -745,15 +866,18 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
         return;
     }
     const int k = U.k, kq = lane & 3, mg = lane >> 2;
-    // B fragments: lane holds al / be [4 ks + kq][8 nb + mg]
-    double ba[NQ][NK], bb[NQ][NK];
+    // B fragments of al / be in shared memory, [ks][nb][lane] (conflict-free LDS.64;
+    // keeping them in registers spilled at the 96-register cap)
+    double* s_ba = reinterpret_cast<double*>(smem + NSTAGE * STAGE_BYTES + 128);
+    double* s_bb = s_ba + NQ * NK * 32;
 #pragma unroll
     for (int ks = 0; ks < NQ; ++ks)
 #pragma unroll
         for (int nb = 0; nb < NK; ++nb) {
-            ba[ks][nb] = U.al[(4 * ks + kq) * k + 8 * nb + mg];
-            bb[ks][nb] = U.be[(4 * ks + kq) * k + 8 * nb + mg];
+            s_ba[(ks * NK + nb) * 32 + lane] = U.al[(4 * ks + kq) * k + 8 * nb + mg];
+            s_bb[(ks * NK + nb) * 32 + lane] = U.be[(4 * ks + kq) * k + 8 * nb + mg];
         }
+    __syncwarp();
     const double w = *U.w_dev;
     double rr[NK][2];
 #pragma unroll
@@ -797,8 +921,8 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
                 double p0 = r0v, p1 = r1v;
 #pragma unroll
                 for (int ks = 0; ks < NQ; ++ks) {
-                    dmma(x0, x1, ap[ks], ba[ks][nb]);
-                    dmma(p0, p1, aq[ks], bb[ks][nb]);
+                    dmma(x0, x1, ap[ks], s_ba[(ks * NK + nb) * 32 + lane]);
+                    dmma(p0, p1, aq[ks], s_bb[(ks * NK + nb) * 32 + lane]);
                 }
                 if (rin) {
                     const int64_t o = (r0 + r) * k + c;
@@ -833,9 +957,34 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
     finish_reduce<64>(U.red, s_red, k, k, 32, true);
 }
 
+int panel_mode() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("BK_GRAM_PANEL");
+        v = e ? atoi(e) : 1;
+    }
+    return v;
+}
+bool panel_enabled() { return panel_mode() != 0; }
+
+bool launch_panel(const GramStream& Gs, int grid, cudaStream_t st) {
+    const int smem = NSTAGE * STAGE_BYTES + 128;
+#define BK_GP(A, B)                                                                              \
+    if (Gs.nxp == A && Gs.nyp == B) {                                                            \
+        static_assert((NC / 32) * (256 * A * B + 64) * 8 <= NSTAGE * STAGE_BYTES, "combine");    \
+        static bool at = false;                                                                  \
+        if (!at) { set_smem((const void*)gram_panel_stream_kernel<A, B>, smem); at = true; }     \
+        BK_KERNEL(gram_panel_stream_kernel<A, B><<<grid, NC + 32, smem, st>>>(Gs));               \
+        return true;                                                                             \
+    }
+    BK_GP(1, 1) BK_GP(1, 2) BK_GP(2, 1) BK_GP(2, 2) BK_GP(3, 1)
+#undef BK_GP
+    return false;
+}
+
 // ------------------------------------------------------------------ launchers (return false = not applicable)
-// CTA partials + group partials (<= 32 groups of 16), NOUT <= 1024 each
-size_t stream_part_doubles(int num_sms) { return (size_t)(2 * num_sms + 40) * 1024; }
+// CTA partials + group partials (<= 32 groups of 16), NOUT <= 2048 each
+size_t stream_part_doubles(int num_sms) { return (size_t)(2 * num_sms + 40) * 2048; }
 
 bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
     // contiguous operands only, kp and k <= 32, out not aliasing P/Xin/W rows in other tiles is fine
@@ -924,6 +1073,15 @@ bool launch_gram_stream(int64_t n, int ka, int kb, const double* X, int64_t ldx,
     Gs.S.ntiles = (int)((n + Gs.S.T - 1) / Gs.S.T);
     Gs.ka = ka; Gs.kb = kb; Gs.part = part; Gs.ticket = ticket; Gs.G = G; Gs.G2 = nullptr;
     const int grid = grid_for(Gs.S.ntiles, num_sms);
+    // (measured: the 8-byte fragment kernel is faster for the plain Gram once it does not
+    // spill -- k = 16: 49 vs 52 us, k = 32: 96 vs 113 us; BK_GRAM_PANEL=2 forces panels)
+    if (ka % 16 == 0 && kb % 16 == 0 && panel_mode() == 2) {
+        Gs.kw = 16;
+        Gs.nxp = ka / 16; Gs.nyp = kb / 16;
+        for (int p = 0; p < Gs.nxp; ++p) { Gs.xps[p] = 0; Gs.xpo[p] = 16 * p; }
+        for (int p = 0; p < Gs.nyp; ++p) { Gs.yps[p] = Gs.same ? 0 : 1; Gs.ypo[p] = 16 * p; }
+        if (launch_panel(Gs, grid, st)) return true;
+    }
     if (ka <= 4 && kb <= 4) {
         const int smem = NSTAGE * STAGE_BYTES + 128;
         static bool a = false;
@@ -1011,6 +1169,12 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
     Gs.ndot = ndot;
     for (int q = 0; q < ndot; ++q) { Gs.da[q] = dpair[q][0]; Gs.db[q] = dpair[q][1]; Gs.dots[q] = dots[q]; }
     const int grid = grid_for(Gs.S.ntiles, num_sms);
+    if (kw == 16 && panel_enabled()) {   // conflict-free 16-byte fragment loads (parity blocks)
+        Gs.nxp = nxa; Gs.nyp = nya;
+        for (int i = 0; i < nxa; ++i) { Gs.xps[i] = xs[i]; Gs.xpo[i] = 0; }
+        for (int j = 0; j < nya; ++j) { Gs.yps[j] = ys[j]; Gs.ypo[j] = 0; }
+        if (launch_panel(Gs, grid, st)) return true;
+    }
     const int na = (Gs.ka + 7) / 8, nb = (Gs.kb + 7) / 8;
     const int smem = NSTAGE * STAGE_BYTES + 128;
 #define BK_GM(A, B)                                                                              \
@@ -1044,7 +1208,7 @@ bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, c
     U.k = k; U.al = al; U.be = be; U.w_dev = w_dev; U.X = X; U.R = R; U.P = P; U.halt = halt;
     U.red.part = part; U.red.ticket = ticket; U.red.G = rr; U.red.G2 = nullptr;
     const int grid = grid_for(U.S.ntiles, num_sms);
-    const int smem = NSTAGE * STAGE_BYTES + 128;
+    const int smem = NSTAGE * STAGE_BYTES + 128 + 2 * (k / 4) * (k / 8) * 32 * 8;
 #define BK_BT(Q, K)                                                                              \
     if (k == 8 * K) {                                                                            \
         static bool at = false;                                                                  \
