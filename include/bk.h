@@ -168,10 +168,17 @@ typedef struct bk_solve_opts {
     int    conv_mode;       /* enum bk_conv                                   */
     int    x0_is_zero;      /* 1: ignore X on entry                           */
     int    check_every;     /* host-side convergence poll period (>= 1)       */
-    int    use_graphs;      /* 1: replay iterations as CUDA graphs            */
+    int    use_graphs;      /* reserved (ignored): iterations are enqueued    */
     double rtol;
     double breakdown_tol;   /* relative pivot threshold (default 1e-13)       */
+    int    timing;          /* 1: CUDA events around every N x k kernel on the
+                               ctx stream -> rep->t_class_ms / n_class       */
 } bk_solve_opts;
+
+/* kernel classes of bk_solve_report.t_class_ms / n_class */
+enum bk_kclass { BK_K_SPMM = 0, BK_K_GRAM = 1, BK_K_UPDATE = 2, BK_K_FUSED_TAIL = 3,
+                 BK_K_FUSED_GRAM = 4 /* Rt^T [V R] */, BK_K_COPY = 5,
+                 BK_K_FUSED_DOTS = 6 /* Rt^T T, <T,S>, <T,T> */, BK_NKCLASS = 7 };
 
 typedef struct bk_solve_report {
     int     status;           /* BK_OK / BK_NOT_CONVERGED / BK_BREAKDOWN      */
@@ -182,6 +189,8 @@ typedef struct bk_solve_report {
     double  true_relres[BK_MAX_K]; /* ||B - A X|| / initial, recomputed       */
     double  t_total_ms;
     int64_t n_spmm, n_gram, n_update, n_small, n_allreduce;
+    double  t_class_ms[BK_NKCLASS];  /* opts->timing: summed event time per kernel class */
+    int64_t n_class[BK_NKCLASS];     /* launches timed per class                        */
 } bk_solve_report;
 
 void bk_solve_opts_default(bk_solve_opts *opts);

@@ -45,7 +45,10 @@ class SolveOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int), ("max_iters", ctypes.c_int), ("restart", ctypes.c_int),
                 ("precond", ctypes.c_int), ("conv_mode", ctypes.c_int), ("x0_is_zero", ctypes.c_int),
                 ("check_every", ctypes.c_int), ("use_graphs", ctypes.c_int), ("rtol", ctypes.c_double),
-                ("breakdown_tol", ctypes.c_double)]
+                ("breakdown_tol", ctypes.c_double), ("timing", ctypes.c_int)]
+
+
+KCLASSES = ["spmm", "gram", "update", "fused_tail", "fused_gram", "copy", "fused_dots"]
 
 
 class SolveReport(ctypes.Structure):
@@ -53,7 +56,8 @@ class SolveReport(ctypes.Structure):
                 ("breakdown_column", ctypes.c_int), ("relres", ctypes.c_double * BK_MAX_K),
                 ("true_relres", ctypes.c_double * BK_MAX_K), ("t_total_ms", ctypes.c_double),
                 ("n_spmm", ctypes.c_int64), ("n_gram", ctypes.c_int64), ("n_update", ctypes.c_int64),
-                ("n_small", ctypes.c_int64), ("n_allreduce", ctypes.c_int64)]
+                ("n_small", ctypes.c_int64), ("n_allreduce", ctypes.c_int64),
+                ("t_class_ms", ctypes.c_double * 7), ("n_class", ctypes.c_int64 * 7)]
 
 
 class CsrInfo(ctypes.Structure):
@@ -298,7 +302,7 @@ def block_update(ctx: Context, X, P, C, a: float = 1.0, s: float = 1.0, n=None, 
 
 
 def solve_opts(method="cg", rtol=1e-10, max_iters=1000, restart=30, precond="none", conv_mode="all",
-               x0_is_zero=False, check_every=1, breakdown_tol=1e-13, use_graphs=False) -> SolveOpts:
+               x0_is_zero=False, check_every=1, breakdown_tol=1e-13, use_graphs=False, timing=False) -> SolveOpts:
     o = SolveOpts()
     _lib.bk_solve_opts_default(ctypes.byref(o))
     o.method = METHODS[method]
@@ -311,6 +315,7 @@ def solve_opts(method="cg", rtol=1e-10, max_iters=1000, restart=30, precond="non
     o.check_every = check_every
     o.breakdown_tol = breakdown_tol
     o.use_graphs = int(bool(use_graphs))
+    o.timing = int(bool(timing))
     return o
 
 
@@ -332,7 +337,9 @@ def block_krylov_solve(ctx: Context, A: Matrix, B, X, **opts):
            "breakdown_column": rep.breakdown_column, "relres": np.array(rep.relres[:k]),
            "true_relres": np.array(rep.true_relres[:k]), "t_total_ms": rep.t_total_ms,
            "n_spmm": rep.n_spmm, "n_gram": rep.n_gram, "n_update": rep.n_update, "n_small": rep.n_small,
-           "n_allreduce": rep.n_allreduce}
+           "n_allreduce": rep.n_allreduce,
+           "t_class_ms": {c: rep.t_class_ms[i] for i, c in enumerate(KCLASSES)},
+           "n_class": {c: rep.n_class[i] for i, c in enumerate(KCLASSES)}}
     return st, out
 
 

@@ -204,6 +204,7 @@ extern "C" int bk_ctx_destroy(bk_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaStreamSynchronize(ctx->stream);
     for (bk_csr* A : ctx->mats) A->ctx = nullptr;   // still valid handles; destroy frees their memory
+    for (cudaEvent_t e : ctx->tev) cudaEventDestroy(e);
     for (auto& b : ctx->ws)
         if (b.p) cudaFree(b.p);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);

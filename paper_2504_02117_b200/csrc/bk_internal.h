@@ -108,6 +108,26 @@ bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const 
                           const double* Y2, int64_t ldy2, double* d, double* d2, double* part, int* ticket,
                           int num_sms, cudaStream_t st);
 bool use_stream_kernels();
+// k x k epilogue of a fused reduction pass, run by the CTA that produced the
+// final result (dense_dev.cuh run_small_epi): 1 Out = G^{-1}(sign Rhs) by LU,
+// factors kept in LU/piv; 2 BiCGStab omega from ts, tt then Out = G^{-1}(sign Rhs)
+// from LU/piv; 3 convergence test on column norms g.
+struct SmallEpi {
+    int kind = 0;
+    int k = 0;
+    DevStatus* st = nullptr;
+    const double* G = nullptr;
+    const double* Rhs = nullptr;
+    double* Out = nullptr;
+    double sign = 1.0, tol = 0.0;
+    double* LU = nullptr;
+    int* piv = nullptr;
+    const double* ts = nullptr;
+    const double* tt = nullptr;
+    const double* g = nullptr;
+    double rtol = 0.0;
+    int conv_mode = 0;
+};
 // Fused block-BiCGStab passes (stream.cu; false = not applicable):
 // multi-operand Gram: X = [arrays[xs[0]] ..], Y = [arrays[ys[0]] ..], all kw wide
 // (kw <= 16); k x k block (i, j) of X^T Y is written to blk[i][j] (null = dropped).
@@ -116,11 +136,12 @@ bool use_stream_kernels();
 bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya, const int* ys, int nin,
                               const double* const* arrays, double* const (*blk)[2], double* part, int* ticket,
                               int num_sms, cudaStream_t st, int ndot = 0, const int (*dpair)[2] = nullptr,
-                              double* const* dots = nullptr);
+                              double* const* dots = nullptr, const SmallEpi* epi = nullptr);
 // X += P al + w S; R = S - w T; P = R + (P - w V) be; rr_c = ||R_c||^2 (w = *w_dev); k % 8 == 0
 bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
                             const double* V, const double* al, const double* be, const double* w_dev, double* rr,
-                            const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st);
+                            const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st,
+                            const SmallEpi* epi = nullptr);
 // d[c] = sum_i X[i,c] Y[i,c] for c < k (and optionally d2 with Y2); deterministic.
 size_t coldot_ws_doubles(int64_t n, int k, int num_sms);
 void launch_coldot(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,
@@ -193,6 +214,7 @@ struct bk_ctx {
     size_t h_pinned_bytes = 0;
     int nranks = 1, rank = 0;
     std::vector<bk_csr*> mats;    // live matrices (detached when the ctx is destroyed)
+    std::vector<cudaEvent_t> tev; // event pool of the solver's per-kernel timing (opts.timing)
 #ifndef BK_NO_NCCL
     ncclComm_t comm = nullptr;
 #endif

@@ -7,128 +7,31 @@
 // 256-thread CTA versions in dense.cu spend ~100 block barriers per call).
 // Breakdown is a status (DevStatus), never a crash (R6).
 #include "bk_internal.h"
+#include "dense_dev.cuh"
 
 namespace bk {
 namespace {
 
-constexpr int KM = BK_MAX_K;
-constexpr int LD = KM + 1;
+using dd::KM;
+using dd::LD;
+using dd::wmax;
 
-__device__ __forceinline__ double wmax(double v) {
-#pragma unroll
-    for (int m = 16; m >= 1; m >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, m));
-    return v;
-}
-
-// LU with partial pivoting (explicit row swaps), Out = G^{-1} (sign Rhs).
-// rows < k of a k x ncols row-major matrix (scaled) into smem, all loads in flight first
-__device__ __forceinline__ void load_rows_w(const double* __restrict__ src, double* dst, int k, int ncols, double scale) {
-    const int l = threadIdx.x;
-    double v[KM];
-#pragma unroll
-    for (int r = 0; r < KM; ++r) v[r] = (r < k && l < ncols) ? src[r * ncols + l] : 0.0;
-#pragma unroll
-    for (int r = 0; r < KM; ++r)
-        if (r < k && l < ncols) dst[r * LD + l] = scale * v[r];
-}
-
-// LU with partial pivoting (explicit row swaps), Out = G^{-1} (sign Rhs).
-// LUo / pivo (optional): the factors (P G = L U, unit L below the diagonal,
-// getrf layout) and the pivot row of each step, for lu_resolve_w.
+// LU with partial pivoting (explicit row swaps), Out = G^{-1} (sign Rhs)
+// (dense_dev.cuh lu_solve_warp); LUo / pivo keep the factors for lu_resolve_w.
 __global__ void __launch_bounds__(32) lu_solve_w(int defer, const double* __restrict__ G, const double* __restrict__ Rhs,
                                                  double* __restrict__ Out, int k, int nrhs, double sign, double tol,
                                                  DevStatus* st, double* __restrict__ LUo, int* __restrict__ pivo) {
     __shared__ double A[KM * LD], B[KM * LD];
     __shared__ int s_piv[KM];
-    if (st && st->halt) return;
-    const int l = threadIdx.x;
-    load_rows_w(G, A, k, k, 1.0);
-    load_rows_w(Rhs, B, k, nrhs, sign);
-    __syncwarp();
-    double mx = 0.0;
-    for (int r = 0; r < k; ++r)
-        if (l < k) mx = fmax(mx, fabs(A[r * LD + l]));
-    mx = wmax(mx);
-    if (!(mx > 0.0)) mx = 2.2250738585072014e-308;
-#pragma unroll 1
-    for (int j = 0; j < k; ++j) {
-        double v = (l >= j && l < k) ? fabs(A[l * LD + j]) : -1.0;
-        int p = l;
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, v, m);
-            const int op = __shfl_xor_sync(0xffffffffu, p, m);
-            if (ov > v || (ov == v && op < p)) { v = ov; p = op; }
-        }
-        if (!(v > tol * mx)) {
-            if (l == 0 && st) {
-                if (defer) st->pending_bd = j + 1;
-                else { st->breakdown_col = j; st->halt = 1; }
-            }
-            return;
-        }
-        if (l == 0) s_piv[j] = p;
-        if (p != j) {   // lane l swaps column l of rows j and p
-            if (l < k) { const double t = A[j * LD + l]; A[j * LD + l] = A[p * LD + l]; A[p * LD + l] = t; }
-            if (l < nrhs) { const double t = B[j * LD + l]; B[j * LD + l] = B[p * LD + l]; B[p * LD + l] = t; }
-        }
-        __syncwarp();
-        if (l > j && l < k) {
-            const double f = A[l * LD + j] / A[j * LD + j];
-#pragma unroll 4
-            for (int c = j + 1; c < k; ++c) A[l * LD + c] = fma(-f, A[j * LD + c], A[l * LD + c]);
-#pragma unroll 4
-            for (int c = 0; c < nrhs; ++c) B[l * LD + c] = fma(-f, B[j * LD + c], B[l * LD + c]);
-            A[l * LD + j] = f;   // L multiplier (getrf layout)
-        }
-        __syncwarp();
-    }
-    // back substitution, lane = right-hand-side column (solution overwrites B)
-    if (l < nrhs) {
-#pragma unroll 1
-        for (int i = k - 1; i >= 0; --i) {
-            double v = B[i * LD + l];
-#pragma unroll 4
-            for (int q = i + 1; q < k; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
-            B[i * LD + l] = v / A[i * LD + i];
-        }
-        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
-    }
-    if (LUo && l < k)
-        for (int r = 0; r < k; ++r) LUo[r * k + l] = A[r * LD + l];
-    if (pivo && l < k) pivo[l] = s_piv[l];
+    dd::lu_solve_warp(defer, G, Rhs, Out, k, nrhs, sign, tol, st, LUo, pivo, A, B, s_piv);
 }
 
-// Out = G^{-1} (sign Rhs) from lu_solve_w's factors (getrs): b <- P b, L y = b, U x = y.
+// Out = G^{-1} (sign Rhs) from lu_solve_w's factors (getrs).
 __global__ void __launch_bounds__(32) lu_resolve_w(const double* __restrict__ LU, const int* __restrict__ piv,
                                                    const double* __restrict__ Rhs, double* __restrict__ Out, int k,
                                                    int nrhs, double sign, DevStatus* st) {
     __shared__ double A[KM * LD], B[KM * LD];
-    if (st && st->halt) return;
-    const int l = threadIdx.x;
-    load_rows_w(LU, A, k, k, 1.0);
-    load_rows_w(Rhs, B, k, nrhs, sign);
-    __syncwarp();
-    if (l < nrhs) {
-#pragma unroll 1
-        for (int j = 0; j < k; ++j) {   // b <- P b (all interchanges, in order: getrs)
-            const int p = piv[j];
-            if (p != j) { const double t = B[j * LD + l]; B[j * LD + l] = B[p * LD + l]; B[p * LD + l] = t; }
-        }
-#pragma unroll 1
-        for (int j = 0; j < k; ++j) {   // L y = b (unit lower, final row order)
-            const double bj = B[j * LD + l];
-            for (int i = j + 1; i < k; ++i) B[i * LD + l] = fma(-A[i * LD + j], bj, B[i * LD + l]);
-        }
-#pragma unroll 1
-        for (int i = k - 1; i >= 0; --i) {
-            double v = B[i * LD + l];
-#pragma unroll 4
-            for (int q = i + 1; q < k; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
-            B[i * LD + l] = v / A[i * LD + i];
-        }
-        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
-    }
+    dd::lu_resolve_warp(LU, piv, Rhs, Out, k, nrhs, sign, st, A, B);
 }
 
 // Cholesky of A (lower part, lane = row); returns breakdown column or -1.

@@ -32,6 +32,34 @@ struct Solver {
     DevStatus* hs = nullptr;   // pinned readback
     int slot = WS_SOLVE_BASE;
     bool allred;
+    // opts.timing: (start, end) event index pairs per kernel class, events from ctx->tev
+    std::vector<int> tcls;
+    int tnext = 0;
+    cudaEvent_t tev(int i) {
+        while ((int)ctx->tev.size() <= i) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ctx->tev.push_back(e);
+        }
+        return ctx->tev[i];
+    }
+    void tb() {
+        if (o->timing) cudaEventRecord(tev(tnext), st);
+    }
+    void te(int cls) {
+        if (!o->timing) return;
+        cudaEventRecord(tev(tnext + 1), st);
+        tnext += 2;
+        tcls.push_back(cls);
+    }
+    void tsum() {   // after the stream is synchronized
+        for (size_t i = 0; i < tcls.size(); ++i) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, ctx->tev[2 * i], ctx->tev[2 * i + 1]);
+            rep->t_class_ms[tcls[i]] += ms;
+            rep->n_class[tcls[i]] += 1;
+        }
+    }
 
     double* vec(int ld_cols = 0) {
         const int cols = ld_cols ? ld_cols : k;
@@ -59,15 +87,28 @@ struct Solver {
 
     int spmm(const double* X, int64_t ldx, double* Y, int64_t ldy, double alpha = 1.0, double beta = 0.0) {
         rep->n_spmm++;
-        return spmm_dev(ctx, A, k, X, ldx, nullptr, k, alpha, beta, Y, ldy);
+        tb();
+        const int r = spmm_dev(ctx, A, k, X, ldx, nullptr, k, alpha, beta, Y, ldy);
+        te(BK_K_SPMM);
+        return r;
     }
     int gram(const double* X, int64_t ldx, int ka, const double* Y, int64_t ldy, double* G) {
         rep->n_gram++;
         if (allred) rep->n_allreduce++;
-        return gram_dev(ctx, n, ka, k, X, ldx, Y, ldy, G, allred);
+        tb();
+        const int r = gram_dev(ctx, n, ka, k, X, ldx, Y, ldy, G, allred);
+        te(BK_K_GRAM);
+        return r;
     }
     int coldot(const double* X, int64_t ldx, const double* Y, int64_t ldy, const double* Y2, int64_t ldy2,
                double* d, double* d2) {
+        tb();
+        const int r = coldot_(X, ldx, Y, ldy, Y2, ldy2, d, d2);
+        te(BK_K_GRAM);
+        return r;
+    }
+    int coldot_(const double* X, int64_t ldx, const double* Y, int64_t ldy, const double* Y2, int64_t ldy2,
+                double* d, double* d2) {
         rep->n_gram++;
         double* part = (double*)ws_get(ctx, WS_COLDOT_PART, coldot_ws_doubles(n, k, ctx->num_sms) * sizeof(double));
         double* spart = use_stream_kernels()
@@ -93,12 +134,15 @@ struct Solver {
     }
     // fused multi-operand Gram (k x k blocks of [arrays[xs..]]^T [arrays[ys..]]), summed over ranks
     int gram_multi(int nxa, const int* xs, int nya, const int* ys, int nin, const double* const* arrays,
-                   double* const (*blk)[2], int ndot = 0, const int (*dp)[2] = nullptr, double* const* dots = nullptr) {
+                   double* const (*blk)[2], int ndot = 0, const int (*dp)[2] = nullptr, double* const* dots = nullptr,
+                   const SmallEpi* epi = nullptr, int cls = BK_K_FUSED_GRAM) {
         rep->n_gram++;
         double* spart = (double*)ws_get(ctx, WS_GRAM_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double));
+        tb();
         if (!launch_gram_multi_stream(n, k, nxa, xs, nya, ys, nin, arrays, blk, spart, ctx->d_tickets,
-                                      ctx->num_sms, st, ndot, dp, dots))
+                                      ctx->num_sms, st, ndot, dp, dots, epi))
             return set_error(ctx, BK_ERR_UNSUPPORTED, "fused gram not applicable");
+        te(cls);
         int r = launched("gram_multi");
         for (int i = 0; i < nxa && !r; ++i)
             for (int j = 0; j < nya && !r; ++j)
@@ -125,11 +169,22 @@ struct Solver {
         u.W = W; u.ldw = ldw; u.w_host = w_host; u.w_dev = w_dev;
         u.out = out; u.ldo = ldo;
         u.halt = halted ? &ds->halt : nullptr;
+        tb();
         launch_update(u, st);
+        te(BK_K_UPDATE);
         return launched("update");
     }
     int copy(double* dst, int64_t ldd, const double* src, int64_t lds) {
+        tb();
+        const int r = copy_(dst, ldd, src, lds);
+        te(BK_K_COPY);
+        return r;
+    }
+    int copy_(double* dst, int64_t ldd, const double* src, int64_t lds) {
         if (n == 0) return BK_OK;
+        if (ldd == k && lds == k)   // contiguous: one linear copy (a 2-D copy of k*8-byte rows is far slower)
+            return cuda_check(ctx, cudaMemcpyAsync(dst, src, (size_t)n * k * sizeof(double), cudaMemcpyDeviceToDevice, st),
+                              "copy");
         return cuda_check(ctx,
                           cudaMemcpy2DAsync(dst, ldd * sizeof(double), src, lds * sizeof(double), k * sizeof(double),
                                             n, cudaMemcpyDeviceToDevice, st),
@@ -165,6 +220,7 @@ int finish(Solver& S, const double* B, int64_t ldb, const double* X, int64_t ldx
     cudaEventCreate(&e1);
     cudaEventRecord(e1, S.st);
     TRY(cuda_check(ctx, cudaStreamSynchronize(S.st), "finish"));
+    S.tsum();
     float ms = 0.f;
     cudaEventElapsedTime(&ms, e0, e1);
     cudaEventDestroy(e1);
@@ -251,7 +307,7 @@ static bool fused_bicgstab_enabled() {
 int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
     const int k = S.k;
     double* R = S.vec();
-    double* Rt = S.vec();
+    double* Rt_buf = S.vec();
     double* P = S.vec();
     double* V = S.vec();
     double* Sv = S.vec();
@@ -264,26 +320,38 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
     TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
     sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
-    TRY(S.copy(Rt, k, R, k));
+    // Rt = R0 is never written: with X0 = 0 it is B itself (no copy)
+    const double* Rt = Rt_buf;
+    if (S.o->x0_is_zero && ldb == k && ((uintptr_t)B % 16) == 0) Rt = B;
+    else TRY(S.copy(Rt_buf, k, R, k));
     TRY(S.copy(P, k, R, k));
     const double tol = S.o->breakdown_tol;
     const double* om = &S.ds->omega;
     const double* nom = &S.ds->neg_omega;
     const bool fused = fused_bicgstab_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
                        ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
+    // one rank: the k x k steps run in the epilogue of the pass that produces their
+    // input (no separate small-kernel launches); p > 1: after the allreduce
+    const bool epi = fused && !S.allred;
+    SmallEpi e_al, e_be, e_cv;
+    e_al.kind = 1; e_al.k = k; e_al.st = S.ds; e_al.G = M1; e_al.Rhs = RR; e_al.Out = al; e_al.sign = 1.0;
+    e_al.tol = tol; e_al.LU = LUf; e_al.piv = piv;
+    e_be.kind = 2; e_be.k = k; e_be.st = S.ds; e_be.ts = ts; e_be.tt = tt; e_be.Rhs = RtT; e_be.Out = be;
+    e_be.sign = -1.0; e_be.LU = LUf; e_be.piv = piv;
+    e_cv.kind = 3; e_cv.k = k; e_cv.st = S.ds; e_cv.g = nr; e_cv.rtol = S.o->rtol; e_cv.conv_mode = S.o->conv_mode;
     for (int it = 0; it < S.o->max_iters; ++it) {
         TRY(S.spmm(P, k, V, k));
         if (fused) {
             const double* arr[3] = {Rt, V, R};
             const int xs[1] = {0}, ys[2] = {1, 2};
             double* const blk[3][2] = {{M1, RR}, {nullptr, nullptr}, {nullptr, nullptr}};
-            TRY(S.gram_multi(1, xs, 2, ys, 3, arr, blk));
+            TRY(S.gram_multi(1, xs, 2, ys, 3, arr, blk, 0, nullptr, nullptr, epi ? &e_al : nullptr));
+            if (!epi) sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st, 0, LUf, piv);   // factors kept for be
         } else {
             TRY(S.gram(Rt, k, k, V, k, M1));
             TRY(S.gram(Rt, k, k, R, k, RR));
+            sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st);
         }
-        if (fused) sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st, 0, LUf, piv);   // factors kept for be
-        else sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st);
         TRY(S.upd(Sv, k, 1.0, R, k, -1.0, V, k, k, al));
         TRY(S.spmm(Sv, k, T, k));
         if (fused) {
@@ -292,21 +360,25 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
             double* const blk[3][2] = {{RtT, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
             const int dp[2][2] = {{2, 1}, {2, 2}};   // <T,S>, <T,T> per column
             double* const dots[2] = {ts, tt};
-            TRY(S.gram_multi(1, xs, 1, ys, 3, arr, blk, 2, dp, dots));
-            sd_omega(ts, tt, k, S.ds, S.st);
-            sd_lu_resolve(LUf, piv, RtT, be, k, k, -1.0, S.ds, S.st);   // same M1: no new breakdown
+            TRY(S.gram_multi(1, xs, 1, ys, 3, arr, blk, 2, dp, dots, epi ? &e_be : nullptr, BK_K_FUSED_DOTS));
+            if (!epi) {
+                sd_omega(ts, tt, k, S.ds, S.st);
+                sd_lu_resolve(LUf, piv, RtT, be, k, k, -1.0, S.ds, S.st);   // same M1: no new breakdown
+            }
             S.rep->n_update += 3;
             S.rep->n_gram++;
             double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
+            S.tb();
             if (!launch_bcg_tail_stream(S.n, k, X, R, P, Sv, T, V, al, be, om, nr, &S.ds->halt, spart,
-                                        S.ctx->d_tickets, S.ctx->num_sms, S.st))
+                                        S.ctx->d_tickets, S.ctx->num_sms, S.st, epi ? &e_cv : nullptr))
                 return set_error(S.ctx, BK_ERR_UNSUPPORTED, "fused BiCGStab tail not applicable");
+            S.te(BK_K_FUSED_TAIL);
             TRY(S.launched("bcg_tail"));
             if (S.allred) {
                 S.rep->n_allreduce++;
                 TRY(allreduce_sum(S.ctx, nr, k));
             }
-            sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
+            if (!epi) sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
             S.rep->n_small += 4;
         } else {
             TRY(S.coldot(T, k, Sv, k, T, k, ts, tt));
@@ -418,7 +490,9 @@ int solve_impl(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb
     cudaEventRecord(e0, S.st);
     int r = S.init_status();
     if (!r && o->x0_is_zero && A->n_local > 0)
-        r = cuda_check(ctx, cudaMemset2DAsync(X, ldx * sizeof(double), 0, k * sizeof(double), A->n_local, S.st),
+        r = cuda_check(ctx,
+                       ldx == k ? cudaMemsetAsync(X, 0, (size_t)A->n_local * k * sizeof(double), S.st)
+                                : cudaMemset2DAsync(X, ldx * sizeof(double), 0, k * sizeof(double), A->n_local, S.st),
                        "zero X");
     if (!r) {
         switch (o->method) {

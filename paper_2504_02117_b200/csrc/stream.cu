@@ -15,6 +15,7 @@
 // be) are read directly from global memory by the consumers.
 #include "bk_internal.h"
 #include "ptx.cuh"
+#include "dense_dev.cuh"
 
 #ifndef BK_STREAM_NSTAGE
 #define BK_STREAM_NSTAGE 2
@@ -280,6 +281,7 @@ struct GramStream {
     // panel Gram (16-column panels): X panel p = columns [xpo[p], xpo[p] + 16) of stream xps[p]
     int nxp, nyp;
     int xps[4], xpo[4], yps[4], ypo[4];
+    SmallEpi epi;       // k x k epilogue run by the CTA that writes the final result
 };
 
 // NSET independent accumulator sets (quads alternate between them) so the
@@ -316,8 +318,9 @@ __device__ __forceinline__ void gram_tile(const GramStream& Gs, const double* Xt
 }
 
 // fixed-order cross-warp combine -> CTA partial -> last CTA sums partials in order
+// returns true in the CTA that wrote the final outputs (after a CTA barrier)
 template <int NOUT>
-__device__ __forceinline__ void finish_reduce(const GramStream& Gs, double* s_red, int nout_real, int kb_real,
+__device__ __forceinline__ bool finish_reduce(const GramStream& Gs, double* s_red, int nout_real, int kb_real,
                                               int ld_out, bool coldot) {
     __shared__ int s_last;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -344,7 +347,7 @@ __device__ __forceinline__ void finish_reduce(const GramStream& Gs, double* s_re
     asm volatile("bar.sync 1, %0;" ::"r"(NC));
     if (tid == 0) s_last = (atomicAdd(Gs.ticket + 1 + g, 1) == gsz - 1);
     asm volatile("bar.sync 1, %0;" ::"r"(NC));
-    if (!s_last) return;
+    if (!s_last) return false;
     __threadfence();
     for (int o = tid; o < NOUT; o += NC) {
         double v[RG];
@@ -360,7 +363,7 @@ __device__ __forceinline__ void finish_reduce(const GramStream& Gs, double* s_re
     asm volatile("bar.sync 1, %0;" ::"r"(NC));
     if (tid == 0) s_last = (atomicAdd(Gs.ticket, 1) == ngrp - 1);
     asm volatile("bar.sync 1, %0;" ::"r"(NC));
-    if (!s_last) return;
+    if (!s_last) return false;
     __threadfence();
     for (int o = tid; o < nout_real; o += NC) {
         int idx, dst;
@@ -399,8 +402,15 @@ __device__ __forceinline__ void finish_reduce(const GramStream& Gs, double* s_re
         G[dst] = s;
     }
     if (tid == 0) *Gs.ticket = 0;
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));   // final outputs visible to the CTA (epilogue)
     (void)lane;
     (void)warp;
+    return true;
+}
+
+// k x k epilogue (warp 0 of the final CTA), scratch = the drained ring
+__device__ __forceinline__ void small_epilogue(const SmallEpi& e, unsigned char* smem) {
+    if (e.kind && (threadIdx.x >> 5) == 0) dd::run_small_epi(e, reinterpret_cast<double*>(smem));
 }
 
 template <int NA, int NB>
@@ -715,7 +725,7 @@ __global__ void __launch_bounds__(NC + 32, 2) gram_multi_stream_kernel(const Gra
             d[0] = acc[i][j][0];
             d[1] = acc[i][j][1];
         }
-    finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb + Gs.ndot * kw, Gs.kb, KBP, false);
+    if (finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb + Gs.ndot * kw, Gs.kb, KBP, false)) small_epilogue(Gs.epi, smem);
 }
 
 // Panel Gram: X and Y are lists of 16-column panels.  Lane (mg, kq) loads the
@@ -832,7 +842,8 @@ __global__ void __launch_bounds__(NC + 32, 2) gram_panel_stream_kernel(const Gra
             s_red[warp * NOUT + a * KB + b] = v0;
             s_red[warp * NOUT + a * KB + b + 2] = v1;
         }
-    finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb + (Gs.mode == 2 ? Gs.ndot * kw : 0), Gs.kb, KB, false);
+    if (finish_reduce<NOUT>(Gs, s_red, Gs.ka * Gs.kb + (Gs.mode == 2 ? Gs.ndot * kw : 0), Gs.kb, KB, false))
+        small_epilogue(Gs.epi, smem);
 }
 
 // BiCGStab tail, one pass (O6 steps in order):
@@ -954,7 +965,7 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
             s_red[warp * 64 + 8 * nb + 2 * kq + 1] = rr[nb][1];
         }
     }
-    finish_reduce<64>(U.red, s_red, k, k, 32, true);
+    if (finish_reduce<64>(U.red, s_red, k, k, 32, true)) small_epilogue(U.red.epi, smem);
 }
 
 int panel_mode() {
@@ -1150,7 +1161,8 @@ static void stream_geom(Streams& S, int nin, int64_t n) {
 
 bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya, const int* ys, int nin,
                               const double* const* arrays, double* const (*blk)[2], double* part, int* ticket,
-                              int num_sms, cudaStream_t st, int ndot, const int (*dpair)[2], double* const* dots) {
+                              int num_sms, cudaStream_t st, int ndot, const int (*dpair)[2], double* const* dots,
+                              const SmallEpi* epi) {
     if (kw < 1 || kw > 16 || n <= 0 || nin < 1 || nin > MAXS || nxa < 1 || nxa > 3 || nya < 1 || nya > 2) return false;
     if (ndot < 0 || ndot > 2 || (ndot > 0 && 32 % kw != 0)) return false;
     GramStream Gs{};
@@ -1168,6 +1180,7 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
     Gs.ka = nxa * kw; Gs.kb = nya * kw; Gs.part = part; Gs.ticket = ticket;
     Gs.ndot = ndot;
     for (int q = 0; q < ndot; ++q) { Gs.da[q] = dpair[q][0]; Gs.db[q] = dpair[q][1]; Gs.dots[q] = dots[q]; }
+    if (epi) Gs.epi = *epi;
     const int grid = grid_for(Gs.S.ntiles, num_sms);
     if (kw == 16 && panel_enabled()) {   // conflict-free 16-byte fragment loads (parity blocks)
         Gs.nxp = nxa; Gs.nyp = nya;
@@ -1194,7 +1207,8 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
 
 bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
                             const double* V, const double* al, const double* be, const double* w_dev, double* rr,
-                            const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st) {
+                            const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st,
+                            const SmallEpi* epi) {
     if (n <= 0 || k % 8 != 0 || k > 32) return false;
     const double* arr[5] = {X, P, S, T, V};
     BcgTail U{};
@@ -1207,6 +1221,7 @@ bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, c
     stream_geom(U.S, 5, n);
     U.k = k; U.al = al; U.be = be; U.w_dev = w_dev; U.X = X; U.R = R; U.P = P; U.halt = halt;
     U.red.part = part; U.red.ticket = ticket; U.red.G = rr; U.red.G2 = nullptr;
+    if (epi) U.red.epi = *epi;
     const int grid = grid_for(U.S.ntiles, num_sms);
     const int smem = NSTAGE * STAGE_BYTES + 128 + 2 * (k / 4) * (k / 8) * 32 * 8;
 #define BK_BT(Q, K)                                                                              \
