@@ -10,7 +10,9 @@ module both sides use is ``synth`` (seeded inputs, no method arithmetic).
 * this file: ctypes marshalling for those, and the block Krylov algorithms O4
   (block CG), O5 (block GMRES(m), BCGS2 + CholQR2), O6 (block BiCGStab), written
   step by step in float64 numpy with numpy/LAPACK for the k x k steps, plus
-  O7 (dense reference solve).  SURVEY.md §8(c) and DESIGN.md §3 give the
+  O7 (dense reference solve) and O8 (the DIRK window of SURVEY.md §8(f) NEXT-1:
+  sequential SDIRK stepping, the all-at-once Kronecker solve, the splitting
+  fixed point).  SURVEY.md §8(c) and DESIGN.md §3 give the
   readings.  Pins live in tests/test_oracle_*.py.
 
 Parity status: every function here is pinned (see DESIGN.md §3 table).
@@ -422,3 +424,81 @@ def dense_solve(A, B):
 
 
 SOLVERS = {"cg": block_cg, "gmres": block_gmres, "bicgstab": block_bicgstab}
+
+
+# ---------------------------------------------------------------------------
+# O8: the DIRK window as one matrix equation.
+# M = mass * I (finite volumes), K: CSR stiffness, A: Butcher matrix of a
+# stiffly accurate DIRK method (m x m, row-major), s time steps per window,
+# k = s m columns.  All dense / tiny N.
+# ---------------------------------------------------------------------------
+def _dense(A):
+    A = CsrNp.of(A)
+    D = np.zeros((A.n_rows, A.n_cols))
+    for i in range(A.n_rows):
+        for p in range(A.row_ptr[i], A.row_ptr[i + 1]):
+            D[i, A.col[p]] += A.val[p]
+    return D
+
+
+def dirk_sequential(K, mass, A_tab, Bcols, y_n, tau, s):
+    """Classical stepping of eq. (stiffly-accurate-DIRK): for step q and stage i
+    (1/tau) M (y^(q,i) - y^q) + sum_{j<=i} a_ij K y^(q,j) = sum_{j<=i} a_ij b(t^(q,j)),
+    y^{q+1} = y^(q,m) (stiffly accurate).  Bcols[:, q m + j] = b(t^(q,j)).
+    Returns Y (N x s m), column q m + i = y^(q,i).  Dense solves (tiny N)."""
+    Kd = _dense(K)
+    N = Kd.shape[0]
+    A = np.asarray(A_tab, dtype=np.float64)
+    m = A.shape[0]
+    Bc = _np(Bcols, np.float64)
+    Y = np.zeros((N, s * m))
+    yq = _np(y_n, np.float64).reshape(N).copy()
+    for q in range(s):
+        for i in range(m):
+            lhs = mass / tau * np.eye(N) + A[i, i] * Kd
+            rhs = mass / tau * yq
+            for j in range(i + 1):
+                rhs = rhs + A[i, j] * Bc[:, q * m + j]
+            for j in range(i):
+                rhs = rhs - A[i, j] * (Kd @ Y[:, q * m + j])
+            Y[:, q * m + i] = np.linalg.solve(lhs, rhs)
+        yq = Y[:, q * m + m - 1].copy()
+    return Y
+
+
+def dirk_all_at_once(K, mass, A1, A2, B, B0):
+    """Eq. (general-system-time-steps), P:104-126 with the window matrices of P:260-288:
+    [A1 (x) M + A2 (x) K] vec(Y) = [A2 (x) I_N] vec(B) + vec(B0), vec = column stacking
+    (X_1^T, ..., X_k^T)^T; i.e. M Y A1^T + K Y A2^T = B A2^T + B0.  Dense Kronecker solve."""
+    Kd = _dense(K)
+    N = Kd.shape[0]
+    A1 = np.asarray(A1, dtype=np.float64)
+    A2 = np.asarray(A2, dtype=np.float64)
+    Md = mass * np.eye(N)
+    lhs = np.kron(A1, Md) + np.kron(A2, Kd)
+    Bm = _np(B, np.float64)
+    rhs = np.kron(A2, np.eye(N)) @ Bm.T.reshape(-1) + _np(B0, np.float64).T.reshape(-1)
+    return np.linalg.solve(lhs, rhs).reshape(A1.shape[0], N).T
+
+
+def dirk_fixed_point(L, K, mass, tau, A1, A2, B, B0, Y0, iters, inner=None):
+    """Splitting fixed point, eq. (matrix-splitting) and (matrix-fixed-point-equation), P:357-395:
+    beta = A2[0,0]; (M/tau + beta K) Y^j = -M Y^{j-1} (A1 - I/tau)^T - K Y^{j-1} (A2 - beta I)^T
+                                           + B A2^T + B0,   j = 1..iters.
+    L = M/tau + beta K (CSR).  inner: None = exact (dense) solves, else a callable
+    inner(L, Rhs, X0) -> Y (e.g. a block Krylov oracle).  Returns (Y, [Y^1, ..., Y^iters])."""
+    A1 = np.asarray(A1, dtype=np.float64)
+    A2 = np.asarray(A2, dtype=np.float64)
+    k = A1.shape[0]
+    beta = A2[0, 0]
+    Y = _np(Y0, np.float64).copy()
+    Bm = _np(B, np.float64)
+    fixed = Bm @ A2.T + _np(B0, np.float64)
+    Ld = _dense(L) if inner is None else None
+    hist = []
+    for _ in range(iters):
+        rhs = (-mass * Y @ (A1 - np.eye(k) / tau).T
+               - spmm(K, Y) @ (A2 - beta * np.eye(k)).T + fixed)
+        Y = np.linalg.solve(Ld, rhs) if inner is None else inner(L, rhs, Y)
+        hist.append(Y.copy())
+    return Y, hist

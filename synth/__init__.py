@@ -424,6 +424,12 @@ def random_csr(n_rows: int, n_cols: int, nnz_per_row: int, seed: int, *, empty_r
 # DESIGN.md R24).  Data only: the builder of C given to bspmm_apply.
 # ---------------------------------------------------------------------------
 SDIRK2 = [[SDIRK2_GAMMA, 0.0], [1.0 - SDIRK2_GAMMA, SDIRK2_GAMMA]]
+# Alexander's 3-stage SDIRK (R10): c = (g, (1+g)/2, 1), b = last row
+_g3 = SDIRK3_GAMMA
+_a21 = (1.0 - _g3) / 2.0
+_b1 = -(6.0 * _g3 * _g3 - 16.0 * _g3 + 1.0) / 4.0
+_b2 = (6.0 * _g3 * _g3 - 20.0 * _g3 + 5.0) / 4.0
+SDIRK3 = [[_g3, 0.0, 0.0], [_a21, _g3, 0.0], [_b1, _b2, _g3]]
 
 
 def window_matrices(A_tab, s: int, tau: float, a_elim=None):

@@ -114,6 +114,7 @@ def test_sdirk_tableaux_order_conditions():
     A3 = np.array([[g3, 0, 0], [a21, g3, 0], [b1, b2, g3]]); b3 = A3[-1]; c3 = A3.sum(1)
     assert math.isclose(b3.sum(), 1.0, abs_tol=1e-14) and math.isclose(b3 @ c3, 0.5, abs_tol=1e-14)
     assert math.isclose(b3 @ c3 ** 2, 1 / 3, abs_tol=1e-14) and math.isclose(b3 @ A3 @ c3, 1 / 6, abs_tol=1e-14)
+    assert np.array_equal(np.array(synth.SDIRK3), A3)                    # the tableau the NEXT-1 driver uses
     assert g == 1 - math.sqrt(2) / 2
 
 
