@@ -199,6 +199,39 @@ int block_krylov_solve(bk_ctx *ctx, const bk_csr *A, int k, const double *B, int
                        double *X, int64_t ldx, const bk_solve_opts *opts,
                        bk_solve_report *rep);
 
+/* ---------------------------------------------------------------- NEXT-1: DIRK window
+ * s time steps x m stages of a stiffly accurate DIRK method as ONE matrix equation
+ * with k = s m columns (§2.1, eq. general-system-time-steps P:104-126,
+ * window matrices P:260-288):
+ *     M Y A1^T + K Y A2^T = B A2^T + B0,          M = mass * I,
+ * solved by the splitting fixed point (eq. matrix-splitting / matrix-fixed-point-
+ * equation), beta = A2[0][0], L = M/tau + beta K:
+ *     L Y^j = -M Y^{j-1} (A1 - I/tau)^T - K Y^{j-1} (A2 - beta I)^T + B A2^T + B0,
+ * one block_krylov_solve per outer iteration (opts `inner`, started from zero:
+ * a warm start leaves already-exact columns with a zero residual, on which the
+ * block method breaks down -- no deflation).  For SDIRK windows both couplings are strictly lower triangular, so
+ * the iteration is exact after k outer steps (column c after c + 1), up to the
+ * inner tolerance.
+ * L, K: matrices of the same row partition (L must equal M/tau + beta K; the
+ *   caller assembles it).  A1, A2: k x k row-major, HOST.  B, B0: N x k (ld ldb),
+ *   host or device.  Y: N x k (ld ldy): Y^0 on entry, the last iterate on return.
+ * outer_tol > 0: stop when ||Y^j - Y^{j-1}||_F <= outer_tol ||Y^j||_F;
+ *   0: run max_outer iterations.
+ * Returns BK_OK, BK_NOT_CONVERGED or BK_BREAKDOWN (of an inner solve; also in
+ * rep->status), or an error status.                                          */
+typedef struct bk_dirk_report {
+    int    status;
+    int    outer_iterations;
+    int    inner_iterations_total;
+    int    last_inner_status;
+    double last_change;      /* ||Y^j - Y^{j-1}||_F / ||Y^j||_F, last outer step */
+    double t_total_ms;
+} bk_dirk_report;
+int bk_dirk_solve(bk_ctx *ctx, const bk_csr *L, const bk_csr *K, double mass, double tau, int k,
+                  const double *A1, const double *A2, const double *B, const double *B0, int64_t ldb,
+                  double *Y, int64_t ldy, int max_outer, double outer_tol,
+                  const bk_solve_opts *inner, bk_dirk_report *rep);
+
 /* ---------------------------------------------------------------- host-only
  * Halo plan of a contiguous row partition (pure host code, no CUDA; exported
  * for CPU tests of the multi-GPU path).  Given this rank's local CSR columns

@@ -38,7 +38,7 @@ EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last
             "bk_ctx_synchronize", "bk_ctx_destroy", "bk_get_nccl_unique_id", "bk_ctx_set_comm",
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
             "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo",
-            "bk_plan_bands"]
+            "bk_plan_bands", "bk_dirk_solve"]
 
 
 class SolveOpts(ctypes.Structure):
@@ -92,6 +92,7 @@ _sig = {
                             ctypes.POINTER(SolveReport)], _I),
     "bk_plan_halo": ([_I, _I, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P], _I),
     "bk_plan_bands": ([_I64, _P, _P, _I, _P], _I),
+    "bk_dirk_solve": ([_P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _I64, _P, _I64, _I, _D, _P, _P], _I),
 }
 for _n, (_a, _r) in _sig.items():
     _f = getattr(_lib, _n)
@@ -387,3 +388,36 @@ def plan_bands(row_ptr, col, max_extra: int = 96) -> dict:
     return {"nbands": g, "extra_rows": pl.extra_rows, "max_row_nnz": pl.max_row_nnz,
             "dmin": list(pl.dmin[:g]), "dmax": list(pl.dmax[:g]), "width": list(pl.width[:g]),
             "lo": list(pl.lo[:g]), "hi": list(pl.hi[:g])}
+
+
+class DirkReport(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int), ("outer_iterations", ctypes.c_int),
+                ("inner_iterations_total", ctypes.c_int), ("last_inner_status", ctypes.c_int),
+                ("last_change", ctypes.c_double), ("t_total_ms", ctypes.c_double)]
+
+
+def dirk_solve(ctx: Context, L: Matrix, K: Matrix, mass: float, tau: float, A1, A2, B, B0, Y, *,
+               max_outer=None, outer_tol=0.0, **inner):
+    """NEXT-1 DIRK window (bk_dirk_solve): M Y A1^T + K Y A2^T = B A2^T + B0 by the splitting
+    fixed point; `inner` = block_krylov_solve options.  Y: initial guess in, solution out.
+    Returns (status, report dict)."""
+    pb, nb, kb, ldb = _mv(B, "B")
+    p0, n0, k0, ld0 = _mv(B0, "B0")
+    py, ny, ky, ldy = _mv(Y, "Y")
+    if not (kb == k0 == ky) or ld0 != ldb:
+        raise ValueError("B, B0, Y must have the same width; B and B0 the same leading dimension")
+    a1 = np.ascontiguousarray(np.asarray(A1, dtype=np.float64))
+    a2 = np.ascontiguousarray(np.asarray(A2, dtype=np.float64))
+    if a1.shape != (kb, kb) or a2.shape != (kb, kb):
+        raise ValueError("A1, A2 must be k x k")
+    o = solve_opts(**inner)
+    rep = DirkReport()
+    st = _lib.bk_dirk_solve(ctx.handle, L.handle, K.handle, float(mass), float(tau), kb, _P(a1.ctypes.data),
+                            _P(a2.ctypes.data), _P(pb), _P(p0), ldb, _P(py), ldy,
+                            kb if max_outer is None else int(max_outer), float(outer_tol), ctypes.byref(o),
+                            ctypes.byref(rep))
+    if st not in (BK_OK, BK_NOT_CONVERGED, BK_BREAKDOWN):
+        ctx.check(st, "bk_dirk_solve")
+    return st, {"status": {0: "ok", 2: "not_converged", 3: "breakdown"}[rep.status],
+                "outer_iterations": rep.outer_iterations, "inner_iterations_total": rep.inner_iterations_total,
+                "last_change": rep.last_change, "t_total_ms": rep.t_total_ms}

@@ -650,3 +650,49 @@ extern "C" int block_krylov_solve(bk_ctx* ctx, const bk_csr* A, int k, const dou
     return r;
     BK_CATCH(ctx)
 }
+
+// ------------------------------------------------------------------ NEXT-1 DIRK window (dirk.cpp)
+extern "C" int bk_dirk_solve(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k,
+                             const double* A1, const double* A2, const double* B, const double* B0, int64_t ldb,
+                             double* Y, int64_t ldy, int max_outer, double outer_tol, const bk_solve_opts* inner,
+                             bk_dirk_report* rep) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, L && K && L->ctx == ctx && K->ctx == ctx, "bk_dirk_solve: matrix NULL or from another ctx");
+    ARG_CHECK(ctx, L->n_local == K->n_local && L->row_begin == K->row_begin && L->n_global == K->n_global,
+              "bk_dirk_solve: L and K must have the same row partition");
+    ARG_CHECK(ctx, k >= 1 && k <= BK_MAX_K, "bk_dirk_solve: need 1 <= k <= 32");
+    ARG_CHECK(ctx, A1 && A2 && inner && rep, "bk_dirk_solve: NULL A1/A2/opts/report");
+    ARG_CHECK(ctx, !is_device_ptr(A1) && !is_device_ptr(A2), "bk_dirk_solve: A1, A2 must be host arrays");
+    ARG_CHECK(ctx, tau > 0.0 && mass >= 0.0 && max_outer >= 0 && outer_tol >= 0.0,
+              "bk_dirk_solve: need tau > 0, mass >= 0, max_outer >= 0, outer_tol >= 0");
+    ARG_CHECK(ctx, ldb >= k && ldy >= k, "bk_dirk_solve: leading dimension too small");
+    ARG_CHECK(ctx, L->n_local == 0 || (B && B0 && Y), "bk_dirk_solve: NULL B/B0/Y");
+    ARG_CHECK(ctx, (const void*)Y != (const void*)B && (const void*)Y != (const void*)B0,
+              "bk_dirk_solve: Y must not alias B or B0");
+    ARG_CHECK(ctx, inner->method >= BK_CG && inner->method <= BK_BICGSTAB && inner->check_every >= 1 &&
+                       inner->max_iters >= 0 && inner->rtol >= 0.0,
+              "bk_dirk_solve: bad inner solver options");
+    ARG_CHECK(ctx, inner->method != BK_GMRES || (inner->restart >= 1 && (int64_t)(inner->restart + 1) * k <= BK_MAX_KA),
+              "bk_dirk_solve: GMRES needs restart >= 1 and (restart+1)*k <= 4096");
+    ARG_CHECK(ctx, inner->precond == BK_PRECOND_NONE || (inner->precond == BK_PRECOND_JACOBI && inner->method == BK_CG),
+              "bk_dirk_solve: JACOBI preconditioning is implemented for CG only");
+    BK_TRY
+    const int64_t n = L->n_local;
+    bool bh, b0h;
+    const double* dB = stage_in(ctx, WS_STAGE_X, B, n, ldb, &bh);
+    const double* dB0 = stage_in(ctx, WS_STAGE_C, B0, n, ldb, &b0h);
+    const bool yh = !is_device_ptr(Y);
+    double* dY = Y;
+    if (yh) {
+        dY = (double*)ws_get(ctx, WS_STAGE_Y, (size_t)n * ldy * sizeof(double));
+        CUDA_OK(ctx, cudaMemcpyAsync(dY, Y, (size_t)n * ldy * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
+    }
+    r = dirk_impl(ctx, L, K, mass, tau, k, A1, A2, dB, dB0, ldb, dY, ldy, max_outer, outer_tol, inner, rep);
+    if (r == BK_ERR_CUDA || r == BK_ERR_NCCL || r == BK_ERR_OOM || r == BK_ERR_ARG) return r;
+    if (yh)
+        CUDA_OK(ctx, cudaMemcpyAsync(Y, dY, (size_t)n * ldy * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    return r;
+    BK_CATCH(ctx)
+}

@@ -364,3 +364,65 @@ def test_full_size_apply_sampled_rows(ctx, bk, cfg, k):
     ref = oracle.spmm_rows(Ac, rows, Xc)
     scale = oracle.spmm_rows(abs_csr(Ac), rows, Xc.abs())
     check_close(Y.cpu().numpy()[rows], ref, scale, what=f"{cfg} k={k}")
+
+
+# ----------------------------------------------------------------------------- NEXT-1 DIRK window
+def _dirk_problem(n, A_tab, s, tau):
+    import math
+    K = synth.convdiff2d(n, tau=float("inf"), gamma=1.0)                  # stiffness (c1 operator family)
+    L = synth.convdiff2d(n, tau=tau, gamma=A_tab[0][0])                   # M/tau + beta K, beta = A2[0,0]
+    mass = (1.0 / n) ** 2
+    m = len(A_tab)
+    k = s * m
+    N = n * n
+    rng = np.random.default_rng(3)
+    f, g, y0 = rng.uniform(-1, 1, N), rng.uniform(-1, 1, N), rng.uniform(-1, 1, N)
+    e = rng.uniform(-0.5, 0.5, (N, k))
+    c = np.array(A_tab).sum(1)
+    B = np.stack([math.sin(1.0 + (q + c[i]) * tau) * f + g + e[:, q * m + i] for q in range(s) for i in range(m)], 1)
+    B0 = np.zeros((N, k))
+    B0[:, :m] = (mass / tau * y0)[:, None]
+    A1, A2 = synth.window_matrices(A_tab, s, tau)
+    return K, L, mass, A1.numpy(), A2.numpy(), B, B0, y0
+
+
+@pytest.mark.parametrize("tab,s,method", [("sdirk2", 2, "gmres"), ("sdirk3", 2, "gmres"),
+                                          ("sdirk2", 8, "bicgstab")])
+def test_dirk_window_matches_sequential_sdirk(ctx, bk, tab, s, method):
+    """bk_dirk_solve (splitting fixed point) after k outer iterations equals classical
+    sequential SDIRK stepping (oracle O8) within the inner tolerance; the iterate after 2 outer
+    iterations equals the oracle fixed point with exact solves (columns 0, 1 exact by then)."""
+    tau = 0.05
+    A_tab = synth.SDIRK2 if tab == "sdirk2" else synth.SDIRK3
+    K, L, mass, A1, A2, B, B0, y0 = _dirk_problem(32, A_tab, s, tau)
+    k = A1.shape[0]
+    Ms, Ks = bk.Matrix.from_csr(ctx, L), bk.Matrix.from_csr(ctx, K)
+    Y = torch.zeros(B.shape, dtype=torch.float64, device="cuda")
+    inner = dict(method=method, rtol=1e-12, max_iters=3000, restart=100, check_every=8)
+    st, rep = bk.dirk_solve(ctx, Ms, Ks, mass, tau, A1, A2, cu(torch.from_numpy(B)), cu(torch.from_numpy(B0)), Y,
+                            **inner)
+    assert st == 0 and rep["outer_iterations"] == k, rep
+    Ys = oracle.dirk_sequential(K, mass, A_tab, B, y0, tau, s)
+    rel = np.linalg.norm(Y.cpu().numpy() - Ys) / np.linalg.norm(Ys)
+    assert rel <= 1e-8, rel
+    Y2 = torch.zeros_like(Y)
+    bk.dirk_solve(ctx, Ms, Ks, mass, tau, A1, A2, B, B0, Y2, max_outer=2, **inner)   # host B, B0
+    _, hist = oracle.dirk_fixed_point(L, K, mass, tau, A1, A2, B, B0, np.zeros_like(B), 2)
+    rel2 = np.linalg.norm(Y2.cpu().numpy() - hist[-1]) / np.linalg.norm(hist[-1])
+    assert rel2 <= 1e-8, rel2
+    assert np.linalg.norm(Y2.cpu().numpy()[:, :2] - Ys[:, :2]) <= 1e-8 * np.linalg.norm(Ys[:, :2])
+
+
+def test_dirk_outer_tolerance_and_arguments(ctx, bk):
+    tau = 0.05
+    K, L, mass, A1, A2, B, B0, _ = _dirk_problem(16, synth.SDIRK2, 2, tau)
+    Ms, Ks = bk.Matrix.from_csr(ctx, L), bk.Matrix.from_csr(ctx, K)
+    Y = torch.zeros(B.shape, dtype=torch.float64, device="cuda")
+    st, rep = bk.dirk_solve(ctx, Ms, Ks, mass, tau, A1, A2, B, B0, Y, max_outer=20, outer_tol=1e-11,
+                            method="gmres", rtol=1e-13, restart=60)
+    assert st == 0 and rep["outer_iterations"] <= 5 and rep["last_change"] <= 1e-11, rep
+    with pytest.raises(bk.BkError):
+        bk.dirk_solve(ctx, Ms, Ks, mass, -1.0, A1, A2, B, B0, Y)          # tau <= 0
+    K2 = bk.Matrix.from_csr(ctx, synth.convdiff2d(8, tau=float("inf"), gamma=1.0))
+    with pytest.raises(bk.BkError):
+        bk.dirk_solve(ctx, Ms, K2, mass, tau, A1, A2, B, B0, Y)           # different partition
