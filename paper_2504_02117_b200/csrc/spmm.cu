@@ -590,6 +590,12 @@ bspmm_win_kernel(const BandArgs w) {
     int2* s_pp = reinterpret_cast<int2*>(empty + 8);           // kMetaDepth row-pointer bounds
     double* s_C = reinterpret_cast<double*>(s_pp + kMetaDepth);
     double* s_t = s_C + KP * KP;
+    // coupled apply on the FP64 tensor cores (TCE): C as m8n8k4 B fragments [ks][nb][lane],
+    // then the tile's (A X) rows (TS doubles per row) for the DMMA epilogue
+    constexpr bool TCE = HAS_C && KP >= 8 && VEC == 4;
+    constexpr int NQ = KP / 4, NKO = KP / 8, TS = KP + 2;
+    double* s_Cf = s_C;
+    double* s_tT = s_Cf + NQ * NKO * 32;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
     if (tid == 0) {
@@ -599,7 +605,15 @@ bspmm_win_kernel(const BandArgs w) {
         }
         mbar_fence_init();
     }
-    if (tid < NC) load_C<KP, HAS_C>(a, s_C, tid, NC);
+    if constexpr (TCE) {
+        for (int i = tid; i < NQ * NKO * 32; i += blockDim.x) {
+            const int l = i & 31, ks = (i >> 5) / NKO, nb = (i >> 5) % NKO;
+            const int r = 4 * ks + (l & 3), c = 8 * nb + (l >> 2);
+            s_Cf[i] = (r < a.k && c < a.kout) ? a.C[r * a.kout + c] : 0.0;
+        }
+    } else {
+        if (tid < NC) load_C<KP, HAS_C>(a, s_C, tid, NC);
+    }
     __syncthreads();
 
     const int k = a.k;
@@ -728,10 +742,47 @@ bspmm_win_kernel(const BandArgs w) {
                     band_accumulate<VEC, NB, MR>(s_win, scol, sval, rs, re, thr, fo, kk, c0, sw, acc);
                 }
             }
-            row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
+            if constexpr (TCE) {   // (A X) row to the tile buffer; padded columns zero
+                double* tp = s_tT + r * TS + c0;
+                const bool keep = active && c0 < a.k;
+                reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
+                reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+            } else {
+                row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
+            }
         }
         __syncwarp();
-        if (lane32 == 0) mbar_arrive(&empty[s]);
+        if (lane32 == 0) mbar_arrive(&empty[s]);   // the stage is no longer read
+        if constexpr (TCE) {
+            // Y(8-row block) = alpha (A X)(block) C + beta Y: DMMA m8n8k4, A = the tile rows,
+            // B = C fragments; fragment D[g][2q..2q+1] -> row rb + g, columns 8 nb + 2q
+            asm volatile("bar.sync 1, %0;" ::"r"(NC));
+            const int mg = lane32 >> 2, kq = lane32 & 3;
+            for (int rb = 8 * warp; rb < nr; rb += 8 * (NC / 32)) {
+                double af[NQ];
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) af[ks] = s_tT[(rb + mg) * TS + 4 * ks + kq];
+                const int row = rb + mg;
+#pragma unroll
+                for (int nb = 0; nb < NKO; ++nb) {
+                    double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                    const int c = 8 * nb + 2 * kq;
+                    if (row < nr && c < a.kout) {
+                        double* yp = a.Y + (r0 + row) * a.ldy + c;
+                        double v0 = a.alpha * d0, v1 = a.alpha * d1;
+                        if (a.beta != 0.0) {
+                            v0 = fma(a.beta, yp[0], v0);
+                            if (c + 1 < a.kout) v1 = fma(a.beta, yp[1], v1);
+                        }
+                        if (c + 1 < a.kout) __stcs(reinterpret_cast<double2*>(yp), make_double2(v0, v1));
+                        else __stcs(yp, v0);
+                    }
+                }
+            }
+            asm volatile("bar.sync 1, %0;" ::"r"(NC));   // tile buffer reused by the next tile
+        }
         if (++s == w.ns) {
             s = 0;
             ph ^= 1u;
@@ -772,11 +823,21 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     int TR = RPP < 64 ? 64 : RPP;
     if (tr_env > 0) TR = std::max(2, tr_env & ~1);
     layout(TR);
-    const int fixed = 16 * 8 + kMetaDepth * 8 + (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
-    const int budget = (ctas == 1 ? 227 * 1024 : 113 * 1024) - fixed;
+    // barriers + row-pointer ring + (C, coupled-apply scratch): with the tensor-core epilogue
+    // (TCE) C fragments and the tile's (A X) rows, else C and one scratch line per row group
+    constexpr bool TCE = HAS_C && KP >= 8 && VEC == 4;
+    auto fixed_for = [&](int tr) {
+        const int cb = TCE ? ((KP / 4) * (KP / 8) * 32 + tr * (KP + 2)) * 8
+                           : (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
+        return 16 * 8 + kMetaDepth * 8 + cb;
+    };
+    int fixed = fixed_for(TR);
+    int budget = (ctas == 1 ? 227 * 1024 : 113 * 1024) - fixed;
     while (budget / w.stage_bytes < 2 && TR > 2 * 2) {   // huge windows: smaller tiles
         TR = (TR / 2) & ~1;
         layout(TR);
+        fixed = fixed_for(TR);
+        budget = (ctas == 1 ? 227 * 1024 : 113 * 1024) - fixed;
     }
     int ns = budget / w.stage_bytes;
     if (ns > 8) ns = 8;

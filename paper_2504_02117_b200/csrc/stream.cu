@@ -31,11 +31,6 @@ constexpr int NC = 256;            // consumer threads
 constexpr int NSTAGE = BK_STREAM_NSTAGE;
 constexpr int STAGE_BYTES = BK_STREAM_STAGE_KB * 1024;
 
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
 
 // Up to 3 contiguous row-major operands streamed tile by tile.
 constexpr int MAXS = 5;            // operands per stream tile
