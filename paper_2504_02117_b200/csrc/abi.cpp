@@ -367,6 +367,8 @@ extern "C" int bk_csr_create(bk_ctx* ctx, bk_csr** out, int64_t n_global, int64_
             for (int g = 0; g < bp.nbands; ++g) {
                 A->band.lo[g] = bp.lo[g];
                 A->band.hi[g] = bp.hi[g];
+                A->band.dmin[g] = bp.dmin[g];
+                A->band.dmax[g] = bp.dmax[g];
             }
             A->band.row0 = ib;
             A->band.nrows = ni;

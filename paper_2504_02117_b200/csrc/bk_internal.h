@@ -85,6 +85,7 @@ void launch_bspmm(const SpmmArgs& a, cudaStream_t st);
 struct BandPlan {
     int nbands = 0, extra = 0, max_row_nnz = 0;
     int lo[BK_BAND_MAX] = {}, hi[BK_BAND_MAX] = {};
+    int dmin[BK_BAND_MAX] = {}, dmax[BK_BAND_MAX] = {};
     int64_t row0 = 0, nrows = 0;     // planned contiguous row range
 };
 bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& b, cudaStream_t st);

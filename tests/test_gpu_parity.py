@@ -6,6 +6,8 @@ seeded inputs.  Bar (BASELINE.json north_star, DESIGN.md §3 R17/R18):
   * solves: relative solution difference <= 1e-8 at the same tolerance,
     iteration counts within 1, true residual <= rtol (x 10).
 """
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -16,6 +18,7 @@ import synth
 pytestmark = pytest.mark.gpu
 
 TOL = 1e-12
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 @pytest.fixture(scope="module")
@@ -156,6 +159,42 @@ def test_spmm_windowed_paths_bitwise(ctx, bk, k):
             assert info["n_bands"] in (3, 5), info
         else:
             assert info["n_bands"] == 0, info
+        X = synth.multivector(A.n_rows, k, 3, integer=True)
+        Y = torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
+        bk.bspmm_apply(ctx, M, cu(X), Y)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().numpy(), oracle.spmm(A, X)), (A.name, k)
+        C = synth.small_dense(k, k, 6, integer=True)
+        Y0 = synth.multivector(A.n_rows, k, 4, integer=True)
+        Y2 = cu(Y0)
+        bk.bspmm_apply(ctx, M, cu(X), Y2, C=cu(C), alpha=-2.0, beta=3.0)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y2.cpu().numpy(), oracle.spmm(A, X, C, alpha=-2.0, beta=3.0, Y=Y0)), (A.name, k)
+
+
+def _run_roll_subprocess(k):
+    """The rolling-window variant is opt-in (BK_SPMM_ROLL=1, read once per process)."""
+    import subprocess
+    import sys
+    code = (f"import sys; sys.path.insert(0, {repr(ROOT)}); sys.path.insert(0, {repr(ROOT + '/tests')}); "
+            f"import test_gpu_parity as t, paper_2504_02117_b200 as bk; "
+            f"c = bk.Context(0); t._roll_case(c, bk, {k}); print('ok')")
+    env = dict(os.environ, BK_SPMM_ROLL="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stderr[-3000:]
+
+
+@pytest.mark.parametrize("k", [1, 2, 4, 6, 8, 12, 16, 32])
+def test_spmm_rolling_window_bitwise(ctx, bk, k):
+    _run_roll_subprocess(k)
+
+
+def _roll_case(ctx, bk, k):
+    """Rolling-window apply (lattice stencils, X lines kept in a shared-memory run ring,
+    DESIGN.md §4.1): 2-D 64 x 40 grid and 3-D 48^3 (short and long sequences, x-halo
+    clipping at line ends, side runs), plain and coupled -- bitwise vs the oracle."""
+    for A in (synth.convdiff2d(64, ny=40, integer=True), synth.diffreact3d(48, integer=True)):
+        M = bk.Matrix.from_csr(ctx, A)
         X = synth.multivector(A.n_rows, k, 3, integer=True)
         Y = torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
         bk.bspmm_apply(ctx, M, cu(X), Y)
