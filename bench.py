@@ -320,6 +320,25 @@ def run_ours(args):
                                  gflops=round(fl / (ms * 1e-3) / 1e9, 1), frac=round(by / (ms * 1e-3) / 1e9 / peak, 4))
             sweep[k] = row
 
+    # ---- the other BASELINE configs (c3, c4, c5), outside the timed region: apply / Gram /
+    # update GB/s at each config's k and block-solver time per iteration (tools/config_sweep.py)
+    configs = None
+    if world == 1 and not args.no_sweep and not args.no_configs:
+        try:
+            r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "config_sweep.py"), "--cfgs", "c3,c4,c5"],
+                               capture_output=True, text=True, timeout=900)
+            configs = {}
+            for ln in r.stdout.splitlines():
+                try:
+                    d = json.loads(ln)
+                    configs[d.pop("cfg")] = d
+                except ValueError:
+                    pass
+            if r.returncode != 0:
+                configs["error"] = r.stderr[-400:]
+        except Exception as e:   # never fail the bench line on the side measurements
+            configs = {"error": str(e)[:400]}
+
     # ---- solve time (full solves, outside the timed region): c1 block GMRES k=4 to 1e-10
     solve_report = None
     if world == 1 and not args.no_sweep:
@@ -404,6 +423,7 @@ def run_ours(args):
             "per_kernel": per,
             "sweep": sweep,
             "solve": solve_report,
+            "configs": configs,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "clocks": cs,
@@ -513,6 +533,7 @@ def main():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--profile-step", action="store_true", help="one step inside cudaProfilerStart/Stop (ncu --profile-from-start off)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c3/c4/c5 side measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=2)
     args = ap.parse_args()
