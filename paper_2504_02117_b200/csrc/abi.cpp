@@ -517,7 +517,13 @@ int gram_dev(bk_ctx* ctx, int64_t n, int ka, int kb, const double* X, int64_t ld
     double* spart = nullptr;
     if (n > 0 && use_stream_kernels())
         spart = (double*)ws_get(ctx, WS_GRAM_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double));
-    if (spart && launch_gram_stream(n, ka, kb, X, ldx, Y, ldy, G, spart, ctx->d_tickets, ctx->num_sms, ctx->stream)) {
+    const bool wide = n > 0 && ka >= 16 && (ka > 32 || ldx != ka || ldy != kb);
+    if (wide && launch_gram_wide(n, ka, kb, X, ldx, Y, ldy, G,
+                                 (double*)ws_get(ctx, WS_GRAM_PART + 33,
+                                                 gram_wide_ws_doubles(ka, kb, ctx->num_sms) * sizeof(double)),
+                                 ctx->num_sms, ctx->stream)) {
+        // strided / wide multi-Gram (GMRES basis): cp.async-staged DMMA
+    } else if (spart && launch_gram_stream(n, ka, kb, X, ldx, Y, ldy, G, spart, ctx->d_tickets, ctx->num_sms, ctx->stream)) {
         // TMA-staged DMMA Gram
     } else if (n > 0 && use_mma && (ka >= 8 || kb >= 8)) {
         double* part = (double*)ws_get(ctx, WS_GRAM_PART, gram_mma_ws_doubles(n, ka, kb, ctx->num_sms) * sizeof(double));

@@ -109,6 +109,11 @@ bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const 
                           const double* Y2, int64_t ldy2, double* d, double* d2, double* part, int* ticket,
                           int num_sms, cudaStream_t st);
 bool use_stream_kernels();
+// Wide / strided multi-Gram and multi-update (wide.cu; GMRES basis, ld = (m+1)k).
+size_t gram_wide_ws_doubles(int ka, int kb, int num_sms);
+bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, const double* W, int64_t ldw,
+                      double* G, double* part, int num_sms, cudaStream_t st);
+bool launch_update_wide(const UpdArgs& u, cudaStream_t st);
 // k x k epilogue of a fused reduction pass, run by the CTA that produced the
 // final result (dense_dev.cuh run_small_epi): 1 Out = G^{-1}(sign Rhs) by LU,
 // factors kept in LU/piv; 2 BiCGStab omega from ts, tt then Out = G^{-1}(sign Rhs)

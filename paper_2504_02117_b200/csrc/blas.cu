@@ -383,6 +383,8 @@ void launch_update(const UpdArgs& a, cudaStream_t st) {
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
     if (use_stream_kernels() && launch_update_stream(a, nsm, st)) return;
+    // strided or wide P (GMRES basis): cp.async-staged DMMA multi-update
+    if (a.kp >= 4 && !a.W && (a.kp > 32 || a.ldp != a.kp || a.ldo != a.k) && launch_update_wide(a, st)) return;
     const int kp = pow2_at_least(a.k);
     switch (kp) {
         case 1: return update_k<1>(a, st);

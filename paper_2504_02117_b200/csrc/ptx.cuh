@@ -41,6 +41,12 @@ __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// spin with test_wait: for barriers completed by cp.async.mbarrier.arrive, which (measured)
+// does not wake threads suspended in try_wait before its time limit
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+    while (!mbar_test(bar, parity)) {
+    }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try(bar, parity)) {
     }

@@ -21,6 +21,8 @@ ap.add_argument("--k", type=int, default=16)
 ap.add_argument("--method", default="bicgstab")
 ap.add_argument("--iters", default="5,10,20")
 ap.add_argument("--reps", type=int, default=5)
+ap.add_argument("--check-every", type=int, default=0, help="0: = iteration count (one poll)")
+ap.add_argument("--restart", type=int, default=30)
 a = ap.parse_args()
 ctx = bk.Context(0)
 A = synth.make_matrix(a.cfg, device="cuda")
@@ -35,7 +37,7 @@ for it in [int(x) for x in a.iters.split(",")]:
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         bk.block_krylov_solve(ctx, M, B, X, method=a.method, rtol=0.0, max_iters=it, x0_is_zero=True,
-                              check_every=it)
+                              check_every=a.check_every or it, restart=a.restart)
         e1.record()
         torch.cuda.synchronize()
         if r:
