@@ -117,7 +117,9 @@ bool launch_update_wide(const UpdArgs& u, cudaStream_t st);
 // k x k epilogue of a fused reduction pass, run by the CTA that produced the
 // final result (dense_dev.cuh run_small_epi): 1 Out = G^{-1}(sign Rhs) by LU,
 // factors kept in LU/piv; 2 BiCGStab omega from ts, tt then Out = G^{-1}(sign Rhs)
-// from LU/piv; 3 convergence test on column norms g.
+// from LU/piv; 3 convergence test on column norms g; 4 Out = G^{-1} Rhs by
+// Cholesky (block CG alpha); 5 block CG: convergence test on diag(g), then
+// Out = Rhs^{-1} g by Cholesky (beta) and Rhs <- g.
 struct SmallEpi {
     int kind = 0;
     int k = 0;
@@ -143,6 +145,10 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
                               const double* const* arrays, double* const (*blk)[2], double* part, int* ticket,
                               int num_sms, cudaStream_t st, int ndot = 0, const int (*dpair)[2] = nullptr,
                               double* const* dots = nullptr, const SmallEpi* epi = nullptr);
+// block CG tail: X += P al; R -= Q al; G = R^T R (new R); k % 8 == 0
+bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double* P, const double* Q,
+                           const double* al, double* G, const int* halt, double* part, int* ticket, int num_sms,
+                           cudaStream_t st, const SmallEpi* epi = nullptr);
 // X += P al + w S; R = S - w T; P = R + (P - w V) be; rr_c = ||R_c||^2 (w = *w_dev); k % 8 == 0
 bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
                             const double* V, const double* al, const double* be, const double* w_dev, double* rr,

@@ -130,6 +130,63 @@ __device__ __forceinline__ void lu_resolve_warp(const double* __restrict__ LU, c
     }
 }
 
+// Cholesky of A (lower part, lane = row) in place; returns the breakdown column or -1.
+__device__ __forceinline__ int chol_warp(double* A, int k, double tol) {
+    const int l = threadIdx.x & 31;
+    double scale = wmax(l < k ? fabs(A[l * LD + l]) : 0.0);
+    if (!(scale > 0.0)) scale = 2.2250738585072014e-308;
+#pragma unroll 1
+    for (int j = 0; j < k; ++j) {
+        const double d = A[j * LD + j];
+        if (!(d > tol * scale)) return j;
+        const double ljj = sqrt(d);
+        __syncwarp();
+        if (l == j) A[j * LD + j] = ljj;
+        if (l > j && l < k) A[l * LD + j] /= ljj;
+        __syncwarp();
+        if (l > j && l < k) {
+            const double lij = A[l * LD + j];
+#pragma unroll 4
+            for (int c = j + 1; c <= l; ++c) A[l * LD + c] = fma(-lij, A[c * LD + j], A[l * LD + c]);
+        }
+        __syncwarp();
+    }
+    return -1;
+}
+
+// Out = G^{-1} Rhs by Cholesky (G SPD k x k, Rhs k x nrhs); breakdown -> status
+__device__ __forceinline__ void chol_solve_warp(const double* __restrict__ G, const double* __restrict__ Rhs,
+                                                double* __restrict__ Out, int k, int nrhs, double tol,
+                                                DevStatus* st, double* A, double* B) {
+    if (st && st->halt) return;
+    const int l = threadIdx.x & 31;
+    load_rows_w(G, A, k, k, 1.0);
+    load_rows_w(Rhs, B, k, nrhs, 1.0);
+    __syncwarp();
+    const int fail = chol_warp(A, k, tol);
+    if (fail >= 0) {
+        if (l == 0 && st) { st->breakdown_col = fail; st->halt = 1; }
+        return;
+    }
+    if (l < nrhs) {
+#pragma unroll 1
+        for (int i = 0; i < k; ++i) {
+            double v = B[i * LD + l];
+#pragma unroll 4
+            for (int q = 0; q < i; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
+            B[i * LD + l] = v / A[i * LD + i];
+        }
+#pragma unroll 1
+        for (int i = k - 1; i >= 0; --i) {
+            double v = B[i * LD + l];
+#pragma unroll 4
+            for (int q = i + 1; q < k; ++q) v = fma(-A[q * LD + i], B[q * LD + l], v);
+            B[i * LD + l] = v / A[i * LD + i];
+        }
+        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
+    }
+}
+
 // BiCGStab omega = sum ts / sum tt (lane 0); tt <= 0 is a breakdown
 __device__ __forceinline__ void omega_dev(const double* ts, const double* tt, int k, int stride, DevStatus* st) {
     if ((threadIdx.x & 31) != 0 || st->halt) return;
@@ -176,6 +233,15 @@ __device__ __forceinline__ void run_small_epi(const SmallEpi& e, double* scratch
         lu_resolve_warp(e.LU, e.piv, e.Rhs, e.Out, e.k, e.k, e.sign, e.st, A, B);
     } else if (e.kind == 3) {
         conv_check_dev(e.g, 1, e.k, e.rtol, e.conv_mode, 0, e.st);
+    } else if (e.kind == 4) {   // block CG alpha: Out = G^{-1} Rhs (Cholesky)
+        chol_solve_warp(e.G, e.Rhs, e.Out, e.k, e.k, e.tol, e.st, A, B);
+    } else if (e.kind == 5) {   // block CG: test on diag(g = R^T R new), beta = Rhs^{-1} g, Rhs <- g
+        conv_check_dev(e.g, e.k + 1, e.k, e.rtol, e.conv_mode, 0, e.st);
+        __syncwarp();
+        chol_solve_warp(e.Rhs, e.g, e.Out, e.k, e.k, e.tol, e.st, A, B);
+        __syncwarp();
+        double* rz = const_cast<double*>(e.Rhs);   // roll R^T R for the next iteration
+        for (int t = threadIdx.x & 31; t < e.k * e.k; t += 32) rz[t] = e.g[t];
     }
 }
 

@@ -236,6 +236,16 @@ int finish(Solver& S, const double* B, int64_t ldb, const double* X, int64_t ldx
 }
 
 // ---------------------------------------------------------------- O4 block CG
+// BK_FUSED=0 selects the unfused kernel sequences (A/B comparisons, tests)
+static bool fused_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("BK_FUSED");
+        v = e ? atoi(e) : 1;
+    }
+    return v != 0;
+}
+
 int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
     const int k = S.k;
     const bool jac = S.o->precond == BK_PRECOND_JACOBI;
@@ -256,7 +266,49 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
         sd_conv_check(RZ, k + 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
     }
     const double tol = S.o->breakdown_tol;
-    for (int it = 0; it < S.o->max_iters; ++it) {
+    // fused pass structure: Q = A P ; PQ = P^T Q (al solve in its epilogue) ;
+    // X += P al, R -= Q al, RZn = R^T R in one pass (test, be solve, RZ roll-over in its
+    // epilogue) ; P = R + P be.  13 N x k passes per iteration instead of 14, 4 launches instead of 9.
+    const bool fused = !jac && fused_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
+                       ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
+    const bool epi = fused && !S.allred;
+    SmallEpi e_al, e_be;
+    e_al.kind = 4; e_al.k = k; e_al.st = S.ds; e_al.G = PQ; e_al.Rhs = RZ; e_al.Out = al; e_al.tol = tol;
+    e_be.kind = 5; e_be.k = k; e_be.st = S.ds; e_be.g = RZn; e_be.Rhs = RZ; e_be.Out = be; e_be.tol = tol;
+    e_be.rtol = S.o->rtol; e_be.conv_mode = S.o->conv_mode;
+    for (int it = 0; fused && it < S.o->max_iters; ++it) {
+        TRY(S.spmm(P, k, Q, k));
+        const double* arr[2] = {P, Q};
+        const int xs[1] = {0}, ys[1] = {1};
+        double* const blk[3][2] = {{PQ, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+        TRY(S.gram_multi(1, xs, 1, ys, 2, arr, blk, 0, nullptr, nullptr, epi ? &e_al : nullptr));
+        if (!epi) sd_chol_solve(PQ, RZ, al, k, k, tol, S.ds, S.st);
+        S.rep->n_update += 2;
+        S.rep->n_gram++;
+        double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
+        S.tb();
+        if (!launch_cg_tail_stream(S.n, k, X, R, P, Q, al, RZn, &S.ds->halt, spart, S.ctx->d_tickets,
+                                   S.ctx->num_sms, S.st, epi ? &e_be : nullptr))
+            return set_error(S.ctx, BK_ERR_UNSUPPORTED, "fused CG tail not applicable");
+        S.te(BK_K_FUSED_TAIL);
+        TRY(S.launched("cg_tail"));
+        if (!epi) {
+            if (S.allred) {
+                S.rep->n_allreduce++;
+                TRY(allreduce_sum(S.ctx, RZn, (int64_t)k * k));
+            }
+            sd_conv_check(RZn, k + 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
+            sd_chol_solve(RZ, RZn, be, k, k, tol, S.ds, S.st);
+            std::swap(RZ, RZn);
+        }
+        S.rep->n_small += 2;
+        TRY(S.upd(P, k, 1.0, R, k, 1.0, P, k, k, be));
+        if ((it + 1) % S.o->check_every == 0 || it + 1 == S.o->max_iters) {
+            TRY(S.poll());
+            if (S.hs->halt) break;
+        }
+    }
+    for (int it = 0; !fused && it < S.o->max_iters; ++it) {
         TRY(S.spmm(P, k, Q, k));
         TRY(S.gram(P, k, k, Q, k, PQ));
         sd_chol_solve(PQ, RZ, al, k, k, tol, S.ds, S.st);
@@ -295,14 +347,6 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
 //   X += P al + w S ; R = S - w T ; P = R + (P - w V) be ; rr = ||R_c||^2   (one pass)
 //   convergence test on rr
 // 21 N x k passes per iteration instead of 28 for the unfused sequence.
-static bool fused_bicgstab_enabled() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("BK_FUSED");
-        v = e ? atoi(e) : 1;
-    }
-    return v != 0;
-}
 
 int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
     const int k = S.k;
@@ -328,7 +372,7 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     const double tol = S.o->breakdown_tol;
     const double* om = &S.ds->omega;
     const double* nom = &S.ds->neg_omega;
-    const bool fused = fused_bicgstab_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
+    const bool fused = fused_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
                        ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
     // one rank: the k x k steps run in the epilogue of the pass that produces their
     // input (no separate small-kernel launches); p > 1: after the allreduce

@@ -963,6 +963,126 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
     if (finish_reduce<64>(U.red, s_red, k, k, 32, true)) small_epilogue(U.red.epi, smem);
 }
 
+// ------------------------------------------------------------------ fused block-CG tail
+// X <- X + P al ; R <- R - Q al ; G = R^T R (new R) -- one pass (O4 steps in order).
+// Streams: 0 X, 1 P, 2 R, 3 Q.  al: k x k (B fragments in shared memory).  The new R rows
+// are written back into the consumed stage tile, and each warp accumulates the Gram of its
+// 8-row blocks on the tensor cores; CTA partials + the common fixed-order reduction.
+struct CgTail {
+    Streams S;
+    int k;
+    const double* al;
+    double* X;
+    double* R;
+    const int* halt;
+    GramStream red;     // gram-mode reduction of G (part, ticket, G, ka = kb = k)
+};
+
+template <int NQ, int NK>
+__global__ void __launch_bounds__(NC + 32, 2) cg_tail_stream_kernel(const CgTail U) {
+    constexpr int KBP = 8 * NK, NOUT = KBP * KBP;
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    if (U.halt && *U.halt) return;
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(U.S, smem, full, empty, s_direct);
+        return;
+    }
+    const int k = U.k, kq = lane & 3, mg = lane >> 2;
+    double* s_ba = reinterpret_cast<double*>(smem + NSTAGE * STAGE_BYTES + 128);
+#pragma unroll
+    for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+        for (int nb = 0; nb < NK; ++nb) s_ba[(ks * NK + nb) * 32 + lane] = U.al[(4 * ks + kq) * k + 8 * nb + mg];
+    __syncwarp();
+    double g[NK][NK][2];
+#pragma unroll
+    for (int i = 0; i < NK; ++i)
+#pragma unroll
+        for (int j = 0; j < NK; ++j) g[i][j][0] = g[i][j][1] = 0.0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < U.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * U.S.T;
+        const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
+        unsigned char* st = smem + s * STAGE_BYTES;
+        const bool dir = s_direct[s] != 0;
+        const double* Xt = dir ? U.S.p[0] + r0 * k : reinterpret_cast<const double*>(st + U.S.off[0]);
+        const double* Pt = dir ? U.S.p[1] + r0 * k : reinterpret_cast<const double*>(st + U.S.off[1]);
+        double* Rt = dir ? nullptr : reinterpret_cast<double*>(st + U.S.off[2]);
+        const double* Rg = U.S.p[2] + r0 * k;
+        const double* Qt = dir ? U.S.p[3] + r0 * k : reinterpret_cast<const double*>(st + U.S.off[3]);
+        for (int rb = 8 * warp; rb < nr; rb += 8 * (NC / 32)) {
+            const int r = rb + mg;
+            const bool rin = r < nr;
+            double ap[NQ], aq[NQ];   // A fragments: P and -Q (row mg, col 4 ks + kq)
+#pragma unroll
+            for (int ks = 0; ks < NQ; ++ks) {
+                ap[ks] = rin ? Pt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+                aq[ks] = rin ? -Qt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+            }
+#pragma unroll
+            for (int nb = 0; nb < NK; ++nb) {
+                const int c = 8 * nb + 2 * kq;
+                double x0 = 0.0, x1 = 0.0, q0 = 0.0, q1 = 0.0;
+                if (rin) {
+                    const double2 xv = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
+                    const double2 rv = dir ? *reinterpret_cast<const double2*>(Rg + (int64_t)r * k + c)
+                                           : *reinterpret_cast<const double2*>(Rt + (int64_t)r * k + c);
+                    x0 = xv.x; x1 = xv.y; q0 = rv.x; q1 = rv.y;
+                }
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) {
+                    const double b = s_ba[(ks * NK + nb) * 32 + lane];
+                    dmma(x0, x1, ap[ks], b);
+                    dmma(q0, q1, aq[ks], b);
+                }
+                if (rin) {
+                    const int64_t o = (r0 + r) * k + c;
+                    *reinterpret_cast<double2*>(U.X + o) = make_double2(x0, x1);
+                    *reinterpret_cast<double2*>(U.R + o) = make_double2(q0, q1);
+                }
+                if (!dir) *reinterpret_cast<double2*>(Rt + (int64_t)(rb + mg) * k + c) =
+                    rin ? make_double2(q0, q1) : make_double2(0.0, 0.0);
+            }
+            // Gram of the block's new rows (this warp wrote them): two k-steps of 4 rows
+            __syncwarp();
+            const double* Rn = dir ? U.R + r0 * k : Rt;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int rr = rb + 4 * h + kq;
+                double a[NK];
+#pragma unroll
+                for (int i = 0; i < NK; ++i) a[i] = rr < nr ? Rn[(int64_t)rr * k + 8 * i + mg] : 0.0;
+#pragma unroll
+                for (int i = 0; i < NK; ++i)
+#pragma unroll
+                    for (int j = 0; j < NK; ++j) dmma(g[i][j][0], g[i][j][1], a[i], a[j]);
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NC));
+    double* s_red = reinterpret_cast<double*>(smem);
+#pragma unroll
+    for (int i = 0; i < NK; ++i)
+#pragma unroll
+        for (int j = 0; j < NK; ++j) {
+            double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + 8 * j + 2 * kq;
+            d[0] = g[i][j][0];
+            d[1] = g[i][j][1];
+        }
+    if (finish_reduce<NOUT>(U.red, s_red, k * k, k, KBP, false)) small_epilogue(U.red.epi, smem);
+}
+
 int panel_mode() {
     static int v = -1;
     if (v < 0) {
@@ -1228,6 +1348,35 @@ bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, c
     }
     BK_BT(2, 1) BK_BT(4, 2) BK_BT(6, 3) BK_BT(8, 4)
 #undef BK_BT
+    return false;
+}
+
+bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double* P, const double* Q,
+                           const double* al, double* G, const int* halt, double* part, int* ticket, int num_sms,
+                           cudaStream_t st, const SmallEpi* epi) {
+    if (n <= 0 || k % 8 != 0 || k > 32) return false;
+    const double* arr[4] = {X, P, R, Q};
+    CgTail U{};
+    for (int q = 0; q < 4; ++q) {
+        if ((uintptr_t)arr[q] & 15) return false;
+        U.S.p[q] = arr[q];
+        U.S.w[q] = k;
+    }
+    stream_geom(U.S, 4, n);
+    U.k = k; U.al = al; U.X = X; U.R = R; U.halt = halt;
+    U.red.part = part; U.red.ticket = ticket; U.red.G = G; U.red.G2 = nullptr; U.red.ka = k; U.red.kb = k;
+    if (epi) U.red.epi = *epi;
+    const int grid = grid_for(U.S.ntiles, num_sms);
+    const int smem = NSTAGE * STAGE_BYTES + 128 + (k / 4) * (k / 8) * 32 * 8;
+#define BK_CT(Q, K)                                                                              \
+    if (k == 8 * K) {                                                                            \
+        static bool at = false;                                                                  \
+        if (!at) { set_smem((const void*)cg_tail_stream_kernel<Q, K>, smem); at = true; }        \
+        BK_KERNEL(cg_tail_stream_kernel<Q, K><<<grid, NC + 32, smem, st>>>(U));                   \
+        return true;                                                                             \
+    }
+    BK_CT(2, 1) BK_CT(4, 2) BK_CT(6, 3) BK_CT(8, 4)
+#undef BK_CT
     return false;
 }
 
