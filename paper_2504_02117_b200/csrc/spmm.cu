@@ -239,6 +239,8 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs& a, const int* col, con
 
 // ------------------------------------------------------------------ persistent TMA pipeline
 // NC consumer threads, NS ring stages, MINB CTAs per SM (variants: DESIGN.md §4.1)
+int env_int(const char* name, int dflt);
+
 template <int NC, int NS, int MINB, int TR_, int CAP_>
 struct PipeCfg {
     static constexpr int TR = TR_, CAP = CAP_;
@@ -257,8 +259,14 @@ struct PipeCfg {
 
 template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP, bool PAIR>
 __global__ void __launch_bounds__(NC + 32, MINB)
-bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
+bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int chunked) {
     using L = PipeCfg<NC, NS, MINB, TR, CAP>;
+    // tile order: interleaved over the CTAs (default), or one contiguous chunk per CTA
+    // (BK_PIPE_CHUNK=1; tried for L1 reuse of the y-1 / centre bands on 3-D lattices:
+    // 10-35 % slower -- the CTAs' z-neighbour rows are no longer L2-resident)
+    const int tb = chunked ? (int)((int64_t)blockIdx.x * ntiles / gridDim.x) : (int)blockIdx.x;
+    const int te = chunked ? (int)((int64_t)(blockIdx.x + 1) * ntiles / gridDim.x) : ntiles;
+    const int tstep = chunked ? 1 : (int)gridDim.x;
     constexpr int LANES = KP / VEC;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * L::STAGE_BYTES);
@@ -285,7 +293,7 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
         if ((tid & 31) == 0) {
             const uint64_t pol = evict_first_policy();
             int i = 0;
-            for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+            for (int tile = tb; tile < te; tile += tstep, ++i) {
                 const int s = i % NS;
                 if (i >= NS) mbar_wait(&empty[s], ((i / NS) - 1) & 1);
                 unsigned char* st = smem + s * L::STAGE_BYTES;
@@ -314,7 +322,7 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
     const bool lane_in = c0 < a.k;
     double* t_row = s_t + grp * (KP + 1);
     int i = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+    for (int tile = tb; tile < te; tile += tstep, ++i) {
         const int s = i % NS;
         mbar_wait(&full[s], (i / NS) & 1);
         const unsigned char* st = smem + s * L::STAGE_BYTES;
@@ -350,7 +358,9 @@ void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
     }
     const int64_t cap = (int64_t)MINB * num_sms;
     const int64_t grid = ntiles < cap ? ntiles : cap;
-    BK_KERNEL(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR><<<(unsigned)grid, NC + 32, smem, st>>>(a, (int)ntiles));
+    static const int chunked = env_int("BK_PIPE_CHUNK", 0) > 0;
+    BK_KERNEL(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR><<<(unsigned)grid, NC + 32, smem, st>>>(
+        a, (int)ntiles, chunked));
 }
 
 // ------------------------------------------------------------------ simple tile kernel (A/B variant)
@@ -1339,6 +1349,11 @@ void launch_bspmm(const SpmmArgs& a, cudaStream_t st) {
 
 bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     if (!win_enabled() || p.nbands <= 0 || a.rows || a.Xg) return false;
+    // 3-D lattices (5 bands): the plain apply is faster with L1 gathers (pipe kernel,
+    // c4 k = 16: 0.66 vs 0.57 of HBM) -- staging 5 band segments fills shared memory
+    // with L2-hit bytes; the coupled apply keeps the DMMA tile epilogue
+    static const int w3 = env_int("BK_WIN_3D", -1);
+    if (w3 < 0 && p.nbands >= 5 && a.C == nullptr) return false;
     if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
     // the window copies contiguous X rows: packed X (ldx == k), 16-byte aligned
     if (a.ldx != a.k || ((uintptr_t)a.X % 16) != 0) return false;
