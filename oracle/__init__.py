@@ -12,7 +12,8 @@ module both sides use is ``synth`` (seeded inputs, no method arithmetic).
   step by step in float64 numpy with numpy/LAPACK for the k x k steps, plus
   O7 (dense reference solve) and O8 (the DIRK window of SURVEY.md §8(f) NEXT-1:
   sequential SDIRK stepping, the all-at-once Kronecker solve, the splitting
-  fixed point).  SURVEY.md §8(c) and DESIGN.md §3 give the
+  fixed point), O9 (the Chebyshev polynomial preconditioner and
+  its Gershgorin interval).  SURVEY.md §8(c) and DESIGN.md §3 give the
   readings.  Pins live in tests/test_oracle_*.py.
 
 Parity status: every function here is pinned (see DESIGN.md §3 table).
@@ -213,11 +214,63 @@ def _colnorms(R):
 
 
 def _apply_prec(minv, R):
-    return R if minv is None else R * minv[:, None]
+    if minv is None:
+        return R
+    if callable(minv):
+        return minv(R)
+    return R * minv[:, None]
+
+
+# --------------------------------------------------------------------------- O9 (NEXT-4)
+def jacobi_gershgorin(A):
+    """O9a: Gershgorin upper bound of the spectrum of D^{-1} A (D = diag A):
+    every eigenvalue lies in a disc centred at 1 with radius sum_{j != i} |a_ij| / |a_ii|,
+    so lambda_max <= max_i sum_j |a_ij| / |a_ii| (R28)."""
+    A = CsrNp.of(A)
+    rows = np.repeat(np.arange(A.n_rows), np.diff(A.row_ptr))
+    absum = np.bincount(rows, weights=np.abs(A.val), minlength=A.n_rows)
+    return float(np.max(absum / np.abs(A.diag())))
+
+
+def chebyshev_bounds(A, lmin=None, lmax=None, ratio=30.0):
+    """Interval [lmin, lmax] of the Chebyshev preconditioner (R28): lmax defaults to
+    the Gershgorin bound O9a, lmin to lmax / ratio."""
+    lmax = jacobi_gershgorin(A) if lmax is None or lmax <= 0 else float(lmax)
+    lmin = lmax / ratio if lmin is None or lmin <= 0 else float(lmin)
+    return lmin, lmax
+
+
+def chebyshev_prec(A, R, steps, lmin, lmax):
+    """O9: Z = p(D^{-1}A) D^{-1} R -- `steps` steps of Chebyshev acceleration for A Z = R from
+    Z = 0 with the Jacobi splitting on the interval [lmin, lmax] (Saad, Iterative Methods for
+    Sparse Linear Systems, Alg. 12.1, in its order and notation, the
+    polynomial stand-in for the paper's AMG preconditioner of Block-CG / Block-BiCGStab,
+    PAPER.md P:774):
+        theta = (lmax + lmin)/2, delta = (lmax - lmin)/2, sigma = theta/delta, rho_0 = 1/sigma,
+        d_0 = D^{-1} R / theta, Z_1 = d_0;
+        for j = 1 .. steps-1:  rho_j = 1/(2 sigma - rho_{j-1});
+            d_j = rho_j rho_{j-1} d_{j-1} + (2 rho_j / delta) D^{-1} (R - A Z_j);  Z_{j+1} = Z_j + d_j.
+    p has degree steps - 1; p(lam) = (1 - T_s((theta - lam)/delta) / T_s(sigma)) / lam."""
+    A = CsrNp.of(A)
+    R = _np(R, np.float64)
+    dinv = 1.0 / A.diag()
+    theta = (lmax + lmin) / 2.0
+    delta = (lmax - lmin) / 2.0
+    sigma = theta / delta
+    rho = 1.0 / sigma
+    d = dinv[:, None] * R / theta
+    Z = d.copy()
+    for _ in range(steps - 1):
+        rho_n = 1.0 / (2.0 * sigma - rho)
+        res = R - spmm(A, Z)
+        d = rho_n * rho * d + (2.0 * rho_n / delta) * (dinv[:, None] * res)
+        Z = Z + d
+        rho = rho_n
+    return Z
 
 
 def block_cg(A, B, X0=None, *, rtol=1e-10, max_iters=1000, precond="none",
-             breakdown_tol=1e-13, conv_mode="all"):
+             breakdown_tol=1e-13, conv_mode="all", cheb_steps=4, cheb_lmin=None, cheb_lmax=None):
     """O4: block CG (O'Leary 1980, cited PAPER.md P:43; DUNE Block-CG P:1054-1056).
 
     R = B - A X; Z = M^{-1} R; P = Z; RZ = R^T Z.  Loop: Q = A P;
@@ -225,12 +278,18 @@ def block_cg(A, B, X0=None, *, rtol=1e-10, max_iters=1000, precond="none",
     column ||R_c|| <= rtol ||R0_c|| ("defect reduction ... for all
     right-hand-sides"; DESIGN.md R5); Z = M^{-1} R; RZn = R^T Z;
     RZ beta = RZn (Cholesky); P = Z + P beta; RZ = RZn.
+    M^{-1}: none, Jacobi (D^{-1}) or the Chebyshev polynomial O9 (symmetric positive definite
+    for SPD A when lmax bounds the spectrum of D^{-1}A, R28).
     """
     A = CsrNp.of(A)
     B = _np(B, np.float64)
     n, k = B.shape
     X = np.zeros_like(B) if X0 is None else _np(X0, np.float64).copy()
-    minv = None if precond == "none" else 1.0 / A.diag()
+    if precond == "chebyshev":
+        lmin, lmax = chebyshev_bounds(A, cheb_lmin, cheb_lmax)
+        minv = lambda R: chebyshev_prec(A, R, cheb_steps, lmin, lmax)  # noqa: E731
+    else:
+        minv = None if precond == "none" else 1.0 / A.diag()
     rep = Report()
     R = B - spmm(A, X)
     r0 = _colnorms(R)
