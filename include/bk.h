@@ -107,6 +107,8 @@ typedef struct bk_csr_info {
     int     n_bands;          /* diagonal bands of the windowed apply
                                  (bk_plan_bands; 0: unstaged gathers)        */
     int     band_extra_rows;  /* window rows per tile beyond n_bands * T      */
+    double  jacobi_gershgorin; /* max_i sum_j |a_ij| / |a_ii| (all ranks): an upper
+                                  bound of the spectrum of D^-1 A (Chebyshev lmax) */
 } bk_csr_info;
 int bk_csr_get_info(const bk_csr *A, bk_csr_info *info);
 
@@ -157,14 +159,22 @@ int block_update(bk_ctx *ctx, int64_t n, int kp, int k, double a, double *X, int
  * rep->true_relres is recomputed from scratch at the end.
  * Returns BK_OK, BK_NOT_CONVERGED or BK_BREAKDOWN (also in rep->status).   */
 enum bk_method  { BK_CG = 0, BK_GMRES = 1, BK_BICGSTAB = 2 };
-enum bk_precond { BK_PRECOND_NONE = 0, BK_PRECOND_JACOBI = 1 };
+/* Preconditioners (CG only: M^-1 must be SPD).  CHEBYSHEV (SURVEY.md §8(f) NEXT-4,
+ * the polynomial stand-in for the paper's AMG preconditioner):
+ * M^-1 R = cheb_steps steps of Chebyshev acceleration (Saad Alg. 12.1) for A Z = R
+ * from Z = 0 with the Jacobi splitting on [cheb_lmin, cheb_lmax]:
+ * Z = p(D^-1 A) D^-1 R, deg p = cheb_steps - 1 (cheb_steps - 1 applies per use).
+ * cheb_lmax <= 0: the Gershgorin bound (bk_csr_info.jacobi_gershgorin);
+ * cheb_lmin <= 0: cheb_lmax / 30 (R28).  SPD for SPD A whenever
+ * cheb_lmax bounds the spectrum of D^-1 A.                                       */
+enum bk_precond { BK_PRECOND_NONE = 0, BK_PRECOND_JACOBI = 1, BK_PRECOND_CHEBYSHEV = 2 };
 enum bk_conv    { BK_CONV_ALL = 0, BK_CONV_FIRST = 1 };
 
 typedef struct bk_solve_opts {
     int    method;          /* enum bk_method                                 */
     int    max_iters;       /* block iterations (GMRES: inner steps, total)   */
     int    restart;         /* GMRES(m): m >= 1                               */
-    int    precond;         /* enum bk_precond (JACOBI: CG only)              */
+    int    precond;         /* enum bk_precond (JACOBI, CHEBYSHEV: CG only)   */
     int    conv_mode;       /* enum bk_conv                                   */
     int    x0_is_zero;      /* 1: ignore X on entry                           */
     int    check_every;     /* host-side convergence poll period (>= 1)       */
@@ -173,7 +183,17 @@ typedef struct bk_solve_opts {
     double breakdown_tol;   /* relative pivot threshold (default 1e-13)       */
     int    timing;          /* 1: CUDA events around every N x k kernel on the
                                ctx stream -> rep->t_class_ms / n_class       */
+    int    cheb_steps;      /* CHEBYSHEV: steps (>= 1; default 4)             */
+    double cheb_lmin;       /* CHEBYSHEV interval (<= 0: defaults, above)     */
+    double cheb_lmax;
 } bk_solve_opts;
+
+/* NEXT-4: Z = M^-1 R for the preconditioner opts->precond of A (NONE: copy;
+ * JACOBI: D^-1 R; CHEBYSHEV: as above).  R, Z: n_local x k row-major, host or
+ * device, Z must not alias R.  Collective for nranks > 1 (the Chebyshev applies
+ * exchange halos).  Returns BK_OK or an error code.                               */
+int bk_precond_apply(bk_ctx *ctx, const bk_csr *A, int k, const bk_solve_opts *opts, const double *R,
+                     int64_t ldr, double *Z, int64_t ldz);
 
 /* kernel classes of bk_solve_report.t_class_ms / n_class */
 enum bk_kclass { BK_K_SPMM = 0, BK_K_GRAM = 1, BK_K_UPDATE = 2, BK_K_FUSED_TAIL = 3,

@@ -31,21 +31,22 @@ BK_ERR_CUDA, BK_ERR_NCCL, BK_ERR_OOM, BK_ERR_UNSUPPORTED = 4, 5, 6, 7
 BK_MAX_K, BK_MAX_KA = 32, 4096
 BK_GRAM_ALLREDUCE = 1
 METHODS = {"cg": 0, "gmres": 1, "bicgstab": 2}
-PRECONDS = {"none": 0, "jacobi": 1}
+PRECONDS = {"none": 0, "jacobi": 1, "chebyshev": 2}
 CONV = {"all": 0, "first": 1}
 
 EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last_error", "bk_ctx_create", "bk_ctx_set_stream",
             "bk_ctx_synchronize", "bk_ctx_destroy", "bk_get_nccl_unique_id", "bk_ctx_set_comm",
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
             "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo",
-            "bk_plan_bands", "bk_dirk_solve"]
+            "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply"]
 
 
 class SolveOpts(ctypes.Structure):
     _fields_ = [("method", ctypes.c_int), ("max_iters", ctypes.c_int), ("restart", ctypes.c_int),
                 ("precond", ctypes.c_int), ("conv_mode", ctypes.c_int), ("x0_is_zero", ctypes.c_int),
                 ("check_every", ctypes.c_int), ("use_graphs", ctypes.c_int), ("rtol", ctypes.c_double),
-                ("breakdown_tol", ctypes.c_double), ("timing", ctypes.c_int)]
+                ("breakdown_tol", ctypes.c_double), ("timing", ctypes.c_int), ("cheb_steps", ctypes.c_int),
+                ("cheb_lmin", ctypes.c_double), ("cheb_lmax", ctypes.c_double)]
 
 
 KCLASSES = ["spmm", "gram", "update", "fused_tail", "fused_gram", "copy", "fused_dots"]
@@ -65,7 +66,7 @@ class CsrInfo(ctypes.Structure):
                 ("nnz", ctypes.c_int64), ("n_ghost", ctypes.c_int64), ("n_boundary_rows", ctypes.c_int64),
                 ("n_send_rows", ctypes.c_int64), ("n_neighbors", ctypes.c_int),
                 ("interior_contiguous", ctypes.c_int), ("n_bands", ctypes.c_int),
-                ("band_extra_rows", ctypes.c_int)]
+                ("band_extra_rows", ctypes.c_int), ("jacobi_gershgorin", ctypes.c_double)]
 
 
 _P, _I, _I64, _D = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64, ctypes.c_double
@@ -93,6 +94,7 @@ _sig = {
     "bk_plan_halo": ([_I, _I, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P], _I),
     "bk_plan_bands": ([_I64, _P, _P, _I, _P], _I),
     "bk_dirk_solve": ([_P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _I64, _P, _I64, _I, _D, _P, _P], _I),
+    "bk_precond_apply": ([_P, _P, _I, _P, _P, _I64, _P, _I64], _I),
 }
 for _n, (_a, _r) in _sig.items():
     _f = getattr(_lib, _n)
@@ -303,7 +305,8 @@ def block_update(ctx: Context, X, P, C, a: float = 1.0, s: float = 1.0, n=None, 
 
 
 def solve_opts(method="cg", rtol=1e-10, max_iters=1000, restart=30, precond="none", conv_mode="all",
-               x0_is_zero=False, check_every=1, breakdown_tol=1e-13, use_graphs=False, timing=False) -> SolveOpts:
+               x0_is_zero=False, check_every=1, breakdown_tol=1e-13, use_graphs=False, timing=False,
+               cheb_steps=4, cheb_lmin=0.0, cheb_lmax=0.0) -> SolveOpts:
     o = SolveOpts()
     _lib.bk_solve_opts_default(ctypes.byref(o))
     o.method = METHODS[method]
@@ -317,6 +320,9 @@ def solve_opts(method="cg", rtol=1e-10, max_iters=1000, restart=30, precond="non
     o.breakdown_tol = breakdown_tol
     o.use_graphs = int(bool(use_graphs))
     o.timing = int(bool(timing))
+    o.cheb_steps = int(cheb_steps)
+    o.cheb_lmin = float(cheb_lmin or 0.0)
+    o.cheb_lmax = float(cheb_lmax or 0.0)
     return o
 
 
@@ -342,6 +348,18 @@ def block_krylov_solve(ctx: Context, A: Matrix, B, X, **opts):
            "t_class_ms": {c: rep.t_class_ms[i] for i, c in enumerate(KCLASSES)},
            "n_class": {c: rep.n_class[i] for i, c in enumerate(KCLASSES)}}
     return st, out
+
+
+def precond_apply(ctx: Context, A: Matrix, R, Z, precond="chebyshev", cheb_steps=4, cheb_lmin=0.0, cheb_lmax=0.0):
+    """Z = M^-1 R (bk_precond_apply, NEXT-4): none / jacobi / chebyshev."""
+    pr, nr, kr, ldr = _mv(R, "R")
+    pz, nz, kz, ldz = _mv(Z, "Z")
+    if kr != kz or nr != nz:
+        raise ValueError("R and Z must have the same shape")
+    o = solve_opts(precond=precond, cheb_steps=cheb_steps, cheb_lmin=cheb_lmin, cheb_lmax=cheb_lmax)
+    ctx.check(_lib.bk_precond_apply(ctx.handle, A.handle, kr, ctypes.byref(o), _P(pr), ldr, _P(pz), ldz),
+              "bk_precond_apply")
+    return Z
 
 
 def plan_halo(nranks: int, rank: int, rank_begin, row_ptr, col_global):

@@ -376,8 +376,17 @@ extern "C" int bk_csr_create(bk_ctx* ctx, bk_csr** out, int64_t n_global, int64_
     }
     // Jacobi diagonal (local numbering: diagonal column of row i is i)
     launch_extract_diag_inv(n_local, 0, A->d_rp, A->d_col, A->d_val, A->d_dinv, st);
-    int rr = post_launch(ctx, "bk_csr_create");
+    // Gershgorin bound of D^-1 A for the Chebyshev preconditioner (max over ranks)
+    unsigned long long* d_g = nullptr;
+    int rr = cuda_check(ctx, cudaMalloc(&d_g, sizeof *d_g), "bk_csr_create gershgorin");
+    if (!rr) rr = cuda_check(ctx, cudaMemsetAsync(d_g, 0, sizeof *d_g, st), "bk_csr_create gershgorin");
+    if (!rr) launch_gershgorin(n_local, A->d_rp, A->d_val, A->d_dinv, d_g, st);
+    if (!rr) rr = post_launch(ctx, "bk_csr_create");
+    if (!rr) rr = allreduce_max(ctx, reinterpret_cast<double*>(d_g), 1);
+    if (!rr) rr = cuda_check(ctx, cudaMemcpyAsync(&A->gersh, d_g, sizeof(double), cudaMemcpyDeviceToHost, st),
+                             "bk_csr_create gershgorin");
     if (!rr) rr = cuda_check(ctx, cudaStreamSynchronize(st), "bk_csr_create sync");
+    if (d_g) cudaFree(d_g);
     if (rr) { bk_csr_destroy(A); return rr; }
     ctx->mats.push_back(A);
     *out = A;
@@ -420,6 +429,7 @@ extern "C" int bk_csr_get_info(const bk_csr* A, bk_csr_info* info) {
     info->interior_contiguous = A->interior_contig;
     info->n_bands = A->band.nbands;
     info->band_extra_rows = A->band.extra;
+    info->jacobi_gershgorin = A->gersh;
     return BK_OK;
 }
 
@@ -618,6 +628,7 @@ extern "C" void bk_solve_opts_default(bk_solve_opts* o) {
     o->use_graphs = 0;
     o->rtol = 1e-10;
     o->breakdown_tol = 1e-13;
+    o->cheb_steps = 4;
 }
 
 extern "C" int block_krylov_solve(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb, double* X,
@@ -635,8 +646,11 @@ extern "C" int block_krylov_solve(bk_ctx* ctx, const bk_csr* A, int k, const dou
     ARG_CHECK(ctx, o->method != BK_GMRES || (o->restart >= 1 && (int64_t)(o->restart + 1) * k <= BK_MAX_KA),
               "block_krylov_solve: GMRES needs restart >= 1 and (restart+1)*k <= 4096");
     ARG_CHECK(ctx, o->rtol >= 0.0 && o->breakdown_tol >= 0.0, "block_krylov_solve: negative tolerance");
-    ARG_CHECK(ctx, o->precond == BK_PRECOND_NONE || (o->precond == BK_PRECOND_JACOBI && o->method == BK_CG),
-              "block_krylov_solve: JACOBI preconditioning is implemented for CG only");
+    ARG_CHECK(ctx, o->precond == BK_PRECOND_NONE ||
+                       ((o->precond == BK_PRECOND_JACOBI || o->precond == BK_PRECOND_CHEBYSHEV) && o->method == BK_CG),
+              "block_krylov_solve: JACOBI / CHEBYSHEV preconditioning is implemented for CG only");
+    ARG_CHECK(ctx, o->precond != BK_PRECOND_CHEBYSHEV || cheb_opts_ok(A, o),
+              "block_krylov_solve: CHEBYSHEV needs cheb_steps >= 1 and 0 < lmin < lmax (after defaults)");
     BK_TRY
     bool bh;
     const double* dB = stage_in(ctx, WS_STAGE_X, B, A->n_local, ldb, &bh);
@@ -656,6 +670,34 @@ extern "C" int block_krylov_solve(bk_ctx* ctx, const bk_csr* A, int k, const dou
     }
     CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
     return r;
+    BK_CATCH(ctx)
+}
+
+// ------------------------------------------------------------------ NEXT-4 preconditioner apply
+extern "C" int bk_precond_apply(bk_ctx* ctx, const bk_csr* A, int k, const bk_solve_opts* o, const double* R,
+                                int64_t ldr, double* Z, int64_t ldz) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, A && A->ctx == ctx && o, "bk_precond_apply: NULL matrix/opts or matrix from another ctx");
+    ARG_CHECK(ctx, k >= 1 && k <= BK_MAX_K && ldr >= k && ldz >= k, "bk_precond_apply: bad k / leading dims");
+    ARG_CHECK(ctx, A->n_local == 0 || (R && Z), "bk_precond_apply: NULL pointer");
+    ARG_CHECK(ctx, (const void*)R != (const void*)Z, "bk_precond_apply: Z must not alias R");
+    ARG_CHECK(ctx, o->precond >= BK_PRECOND_NONE && o->precond <= BK_PRECOND_CHEBYSHEV,
+              "bk_precond_apply: unknown preconditioner");
+    ARG_CHECK(ctx, o->precond != BK_PRECOND_CHEBYSHEV || cheb_opts_ok(A, o),
+              "bk_precond_apply: CHEBYSHEV needs cheb_steps >= 1 and 0 < lmin < lmax (after defaults)");
+    BK_TRY
+    bool rh;
+    const double* dR = stage_in(ctx, WS_STAGE_X, R, A->n_local, ldr, &rh);
+    const bool zh = !is_device_ptr(Z);
+    double* dZ = zh ? (double*)ws_get(ctx, WS_STAGE_Y, (size_t)A->n_local * ldz * sizeof(double)) : Z;
+    r = precond_apply_impl(ctx, A, k, o, dR, ldr, dZ, ldz);
+    if (r) return r;
+    if (zh)
+        CUDA_OK(ctx, cudaMemcpyAsync(Z, dZ, (size_t)A->n_local * ldz * sizeof(double), cudaMemcpyDeviceToHost,
+                                     ctx->stream));
+    CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
     BK_CATCH(ctx)
 }
 

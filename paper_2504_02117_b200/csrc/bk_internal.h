@@ -161,6 +161,18 @@ void launch_coldot(int64_t n, int k, const double* X, int64_t ldx, const double*
                    int num_sms, cudaStream_t st);
 void launch_row_scale(int64_t n, int k, const double* dinv, const double* X, int64_t ldx,
                       double* out, int64_t ldo, cudaStream_t st);
+// NEXT-4 Chebyshev preconditioner (solve.cpp cheb_apply; oracle O9)
+void launch_cheb_step(int64_t n, int k, const double* R, int64_t ldr, const double* AZ, const double* dinv,
+                      double* W, double* Z, int64_t ldz, double cw, double cr, cudaStream_t st);
+void launch_gershgorin(int64_t n, const int32_t* rp, const double* val, const double* dinv, unsigned long long* out,
+                       cudaStream_t st);
+int allreduce_max(bk_ctx* ctx, double* d, int64_t n);
+// Chebyshev interval after defaults (lmax <= 0: Gershgorin, lmin <= 0: lmax / 30)
+void cheb_bounds(const bk_csr* A, const bk_solve_opts* o, double* lmin, double* lmax);
+bool cheb_opts_ok(const bk_csr* A, const bk_solve_opts* o);
+// Z = M^-1 R (solve.cpp); collective for nranks > 1
+int precond_apply_impl(bk_ctx* ctx, const bk_csr* A, int k, const bk_solve_opts* o, const double* R, int64_t ldr,
+                       double* Z, int64_t ldz);
 void launch_extract_diag_inv(int64_t n, int64_t row_offset, const int32_t* rp, const int32_t* col,
                              const double* val, double* dinv, cudaStream_t st);
 void launch_fill(double* p, int64_t n, double v, cudaStream_t st);
@@ -249,6 +261,7 @@ struct bk_csr {
     int32_t* d_col = nullptr;             // local numbering
     double* d_val = nullptr;
     double* d_dinv = nullptr;             // Jacobi
+    double gersh = 0.0;                   // Gershgorin bound of D^-1 A (all ranks)
     int64_t n_ghost = 0;
     int32_t* d_boundary_rows = nullptr;
     int64_t n_boundary = 0;

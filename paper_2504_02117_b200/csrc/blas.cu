@@ -310,6 +310,45 @@ __global__ void diag_inv_kernel(int64_t n, int64_t row_offset, const int32_t* __
     dinv[i] = d != 0.0 ? 1.0 / d : 1.0;
 }
 
+// NEXT-4 Chebyshev step (oracle O9): first step (AZ == null): W = cr D^-1 R, Z = W;
+// else W = cw W + cr D^-1 (R - AZ), Z += W.  Rows in groups of k threads (coalesced
+// row-major), grid-stride over row blocks.  W, AZ: ld = k.
+__global__ void cheb_step_kernel(int64_t n, int k, const double* __restrict__ R, int64_t ldr,
+                                 const double* __restrict__ AZ, const double* __restrict__ dinv,
+                                 double* __restrict__ W, double* __restrict__ Z, int64_t ldz, double cw, double cr) {
+    const int rpb = blockDim.x / k;
+    const int lr = threadIdx.x / k, c = threadIdx.x % k;
+    if (lr >= rpb) return;
+    for (int64_t i = (int64_t)blockIdx.x * rpb + lr; i < n; i += (int64_t)gridDim.x * rpb) {
+        const double di = dinv[i];
+        const double r = R[i * ldr + c];
+        if (AZ == nullptr) {
+            const double w = cr * (di * r);
+            W[i * k + c] = w;
+            Z[i * ldz + c] = w;
+        } else {
+            const double w = fma(cw, W[i * k + c], cr * (di * (r - AZ[i * k + c])));
+            W[i * k + c] = w;
+            Z[i * ldz + c] += w;
+        }
+    }
+}
+
+// Gershgorin bound of D^-1 A: max_i |dinv_i| sum_j |a_ij| (non-negative doubles order as
+// their bit patterns: atomicMax on the bits is exact and order independent)
+__global__ void gershgorin_kernel(int64_t n, const int32_t* __restrict__ rp, const double* __restrict__ val,
+                                  const double* __restrict__ dinv, unsigned long long* out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double g = 0.0;
+    if (i < n) {
+        double s = 0.0;
+        for (int p = rp[i]; p < rp[i + 1]; ++p) s += fabs(val[p]);
+        g = s * fabs(dinv[i]);
+    }
+    for (int o = 16; o > 0; o >>= 1) g = fmax(g, __shfl_xor_sync(0xffffffffu, g, o));
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)__double_as_longlong(g));
+}
+
 __global__ void fill_kernel(double* p, int64_t n, double v) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) p[i] = v;
@@ -405,6 +444,20 @@ void launch_row_scale(int64_t n, int k, const double* dinv, const double* X, int
 void launch_extract_diag_inv(int64_t n, int64_t row_offset, const int32_t* rp, const int32_t* col,
                              const double* val, double* dinv, cudaStream_t st) {
     if (n > 0) BK_KERNEL(diag_inv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, row_offset, rp, col, val, dinv));
+}
+
+void launch_cheb_step(int64_t n, int k, const double* R, int64_t ldr, const double* AZ, const double* dinv,
+                      double* W, double* Z, int64_t ldz, double cw, double cr, cudaStream_t st) {
+    if (n <= 0) return;
+    const int rpb = 256 / k;
+    int64_t grid = (n + rpb - 1) / rpb;
+    if (grid > 148 * 16) grid = 148 * 16;
+    BK_KERNEL(cheb_step_kernel<<<(unsigned)grid, 256, 0, st>>>(n, k, R, ldr, AZ, dinv, W, Z, ldz, cw, cr));
+}
+
+void launch_gershgorin(int64_t n, const int32_t* rp, const double* val, const double* dinv, unsigned long long* out,
+                       cudaStream_t st) {
+    if (n > 0) BK_KERNEL(gershgorin_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, rp, val, dinv, out));
 }
 
 void launch_fill(double* p, int64_t n, double v, cudaStream_t st) {

@@ -97,6 +97,17 @@ int allreduce_sum(bk_ctx* ctx, double* d, int64_t n) {
 #endif
 }
 
+int allreduce_max(bk_ctx* ctx, double* d, int64_t n) {
+#ifdef BK_NO_NCCL
+    (void)d; (void)n;
+    return ctx->nranks <= 1 ? BK_OK : set_error(ctx, BK_ERR_UNSUPPORTED, "built without NCCL");
+#else
+    if (ctx->nranks <= 1 || n == 0) return BK_OK;
+    NCCL_OK(ctx, ncclAllReduce(d, d, (size_t)n, ncclDouble, ncclMax, ctx->comm, ctx->stream));
+    return BK_OK;
+#endif
+}
+
 int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::vector<int32_t>& col_local,
                    const std::vector<int32_t>& colg) {
 #ifdef BK_NO_NCCL

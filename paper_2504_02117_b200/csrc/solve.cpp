@@ -18,6 +18,67 @@
 #include "bk_internal.h"
 
 namespace bk {
+
+// ---------------------------------------------------------------- NEXT-4 preconditioners (oracle O9)
+void cheb_bounds(const bk_csr* A, const bk_solve_opts* o, double* lmin, double* lmax) {
+    *lmax = o->cheb_lmax > 0.0 ? o->cheb_lmax : A->gersh;
+    *lmin = o->cheb_lmin > 0.0 ? o->cheb_lmin : *lmax / 30.0;
+}
+
+bool cheb_opts_ok(const bk_csr* A, const bk_solve_opts* o) {
+    double lo, hi;
+    cheb_bounds(A, o, &lo, &hi);
+    return o->cheb_steps >= 1 && lo > 0.0 && hi > lo && std::isfinite(hi);
+}
+
+namespace {
+// Z = M^-1 R.  CHEBYSHEV (Saad Alg. 12.1 with the Jacobi splitting, the steps of O9):
+//   d_0 = D^-1 R / theta, Z = d_0;  j = 1 .. steps-1: rho_j = 1/(2 sigma - rho_{j-1}),
+//   d_j = rho_j rho_{j-1} d_{j-1} + (2 rho_j/delta) D^-1 (R - A Z), Z += d_j
+// one apply + one fused elementwise pass (cheb_step_kernel) per step.  W, AZ: n x k scratch.
+int prec_core(bk_ctx* ctx, const bk_csr* A, int k, const bk_solve_opts* o, const double* R, int64_t ldr,
+              double* Z, int64_t ldz, double* W, double* AZ, int64_t* n_spmm) {
+    const int64_t n = A->n_local;
+    cudaStream_t st = ctx->stream;
+    if (o->precond == BK_PRECOND_NONE) {
+        if (n == 0) return BK_OK;
+        return cuda_check(ctx,
+                          cudaMemcpy2DAsync(Z, ldz * sizeof(double), R, ldr * sizeof(double), k * sizeof(double), n,
+                                            cudaMemcpyDeviceToDevice, st),
+                          "precond copy");
+    }
+    if (o->precond == BK_PRECOND_JACOBI) {
+        launch_row_scale(n, k, A->d_dinv, R, ldr, Z, ldz, st);
+        return cuda_check(ctx, cudaGetLastError(), "jacobi");
+    }
+    double lmin, lmax;
+    cheb_bounds(A, o, &lmin, &lmax);
+    const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma = theta / delta;
+    double rho = 1.0 / sigma;
+    launch_cheb_step(n, k, R, ldr, nullptr, A->d_dinv, W, Z, ldz, 0.0, 1.0 / theta, st);
+    int r = cuda_check(ctx, cudaGetLastError(), "cheb_step");
+    for (int j = 1; j < o->cheb_steps && !r; ++j) {
+        const double rho_n = 1.0 / (2.0 * sigma - rho);
+        r = spmm_dev(ctx, A, k, Z, ldz, nullptr, k, 1.0, 0.0, AZ, k);
+        if (r) break;
+        if (n_spmm) ++*n_spmm;
+        launch_cheb_step(n, k, R, ldr, AZ, A->d_dinv, W, Z, ldz, rho_n * rho, 2.0 * rho_n / delta, st);
+        r = cuda_check(ctx, cudaGetLastError(), "cheb_step");
+        rho = rho_n;
+    }
+    return r;
+}
+}  // namespace
+
+int precond_apply_impl(bk_ctx* ctx, const bk_csr* A, int k, const bk_solve_opts* o, const double* R, int64_t ldr,
+                       double* Z, int64_t ldz) {
+    enum { WS_PREC = 104 };
+    const size_t vb = (size_t)std::max<int64_t>(A->n_local, 1) * k * sizeof(double);
+    double* W = o->precond == BK_PRECOND_CHEBYSHEV ? (double*)ws_get(ctx, WS_PREC, vb) : nullptr;
+    double* AZ = o->precond == BK_PRECOND_CHEBYSHEV ? (double*)ws_get(ctx, WS_PREC + 1, vb) : nullptr;
+    return prec_core(ctx, A, k, o, R, ldr, Z, ldz, W, AZ, nullptr);
+}
+
 namespace {
 
 struct Solver {
@@ -84,6 +145,18 @@ struct Solver {
         return cuda_check(ctx, cudaStreamSynchronize(st), "status sync");
     }
     int launched(const char* w) { return cuda_check(ctx, cudaGetLastError(), w); }
+    // Z = M^-1 R (JACOBI / CHEBYSHEV; W, AZ scratch for CHEBYSHEV)
+    double *pw = nullptr, *paz = nullptr;
+    int prec(const double* R, double* Z) {
+        if (o->precond == BK_PRECOND_CHEBYSHEV && !pw) {
+            pw = vec();
+            paz = vec();
+        }
+        tb();
+        const int r = prec_core(ctx, A, k, o, R, k, Z, k, pw, paz, &rep->n_spmm);
+        te(BK_K_UPDATE);
+        return r;
+    }
 
     int spmm(const double* X, int64_t ldx, double* Y, int64_t ldy, double alpha = 1.0, double beta = 0.0) {
         rep->n_spmm++;
@@ -248,7 +321,7 @@ static bool fused_enabled() {
 
 int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
     const int k = S.k;
-    const bool jac = S.o->precond == BK_PRECOND_JACOBI;
+    const bool jac = S.o->precond != BK_PRECOND_NONE;   // Jacobi or Chebyshev: Z = M^-1 R
     double* R = S.vec();
     double* P = S.vec();
     double* Q = S.vec();
@@ -256,7 +329,7 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     double* sm = S.small(8 * 32 * 32);
     double *PQ = sm, *RZ = sm + 1024, *RZn = sm + 2048, *al = sm + 3072, *be = sm + 4096, *nr = sm + 5120;
     TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
-    if (jac) launch_row_scale(S.n, k, S.A->d_dinv, R, k, Z, k, S.st);
+    if (jac) TRY(S.prec(R, Z));
     TRY(S.copy(P, k, Z, k));
     TRY(S.gram(R, k, k, Z, k, RZ));
     if (jac) {
@@ -318,7 +391,7 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
         if (jac) {
             TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
             sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
-            launch_row_scale(S.n, k, S.A->d_dinv, R, k, Z, k, S.st);
+            TRY(S.prec(R, Z));
             TRY(S.gram(R, k, k, Z, k, RZn));
         } else {
             TRY(S.gram(R, k, k, R, k, RZn));

@@ -303,7 +303,8 @@ def test_update_integer_bitwise_and_inplace(ctx, bk):
 
 # ----------------------------------------------------------------------------- a6 solve
 SOLVES = [("cg", "c1s", {}), ("gmres", "c1", {"restart": 100}), ("gmres", "c1", {"restart": 20}),
-          ("bicgstab", "c1", {}), ("cg", "c1s", {"precond": "jacobi"})]
+          ("bicgstab", "c1", {}), ("cg", "c1s", {"precond": "jacobi"}),
+          ("cg", "c1s", {"precond": "chebyshev", "cheb_steps": 4})]
 # k = 8, 16 take the fused BiCGStab passes; k = 1, 4 the unfused ones.
 # (GMRES(20) at k = 16 stagnates on c1 in the oracle as well: not a parity case.)
 SOLVE_CASES = [(m, c, kw, k) for (m, c, kw) in SOLVES for k in (1, 4, 8, 16)
@@ -465,3 +466,66 @@ def test_dirk_outer_tolerance_and_arguments(ctx, bk):
     K2 = bk.Matrix.from_csr(ctx, synth.convdiff2d(8, tau=float("inf"), gamma=1.0))
     with pytest.raises(bk.BkError):
         bk.dirk_solve(ctx, Ms, K2, mass, tau, A1, A2, B, B0, Y)           # different partition
+
+
+# ----------------------------------------------------------------------------- NEXT-4 Chebyshev
+def _spd_cases():
+    return {"poisson": synth.laplace_mms2d(40), "richards": synth.richards3d(12, 10, 9)}
+
+
+@pytest.mark.parametrize("name", ["poisson", "richards"])
+def test_gershgorin_bound_matches_oracle(ctx, bk, name):
+    A = _spd_cases()[name]
+    M = bk.Matrix.from_csr(ctx, A)
+    g = M.info()["jacobi_gershgorin"]
+    assert abs(g - oracle.jacobi_gershgorin(A)) <= 4e-16 * g
+
+
+@pytest.mark.parametrize("name", ["poisson", "richards"])
+@pytest.mark.parametrize("k", [1, 4, 16, 12])
+@pytest.mark.parametrize("steps", [1, 3, 6])
+def test_chebyshev_apply_matches_oracle(ctx, bk, name, k, steps):
+    A = _spd_cases()[name]
+    R = synth.multivector(A.n_rows, k, 2)
+    M = bk.Matrix.from_csr(ctx, A)
+    lmin, lmax = oracle.chebyshev_bounds(A)
+    Zr = oracle.chebyshev_prec(A, R.numpy(), steps, lmin, lmax)
+    Z = torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
+    bk.precond_apply(ctx, M, cu(R), Z, "chebyshev", cheb_steps=steps, cheb_lmin=lmin, cheb_lmax=lmax)
+    # composite of `steps` applies: error budget 1e-12 relative to max |Z| per step
+    check_close(Z.cpu().numpy(), Zr, steps * np.abs(Zr).max(), what=f"cheb {name} k{k} s{steps}")
+    Zd = torch.full_like(Z, float("nan"))                       # default interval (Gershgorin, / 30)
+    bk.precond_apply(ctx, M, cu(R), Zd, "chebyshev", cheb_steps=steps)
+    check_close(Zd.cpu().numpy(), Zr, 10 * steps * np.abs(Zr).max(), what="default bounds")
+
+
+def test_jacobi_apply_bitwise_and_host_buffers(ctx, bk):
+    A = _spd_cases()["richards"]
+    R = synth.multivector(A.n_rows, 8, 4)
+    M = bk.Matrix.from_csr(ctx, A)
+    Z = torch.empty(A.n_rows, 8, dtype=torch.float64, device="cuda")
+    bk.precond_apply(ctx, M, cu(R), Z, "jacobi")
+    assert np.array_equal(Z.cpu().numpy(), R.numpy() * (1.0 / np.diag(oracle._dense(A)))[:, None])
+    Zh = torch.empty(A.n_rows, 8, dtype=torch.float64)             # host R / Z staging
+    bk.precond_apply(ctx, M, R, Zh, "chebyshev", cheb_steps=3)
+    Zg = torch.empty_like(Z)
+    bk.precond_apply(ctx, M, cu(R), Zg, "chebyshev", cheb_steps=3)
+    assert torch.equal(Zh, Zg.cpu())
+
+
+@pytest.mark.parametrize("k", [1, 8, 16])
+def test_chebyshev_pcg_matches_oracle_and_cuts_iterations(ctx, bk, k):
+    A = synth.laplace_mms2d(40)
+    B = synth.multivector(A.n_rows, k, 2)
+    M = bk.Matrix.from_csr(ctx, A)
+    X = torch.zeros(A.n_rows, k, dtype=torch.float64, device="cuda")
+    st, rep = bk.block_krylov_solve(ctx, M, cu(B), X, method="cg", rtol=1e-10, max_iters=2000, x0_is_zero=True,
+                                    precond="chebyshev", cheb_steps=5)
+    Xr, rr = oracle.block_cg(A, B, rtol=1e-10, max_iters=2000, precond="chebyshev", cheb_steps=5)
+    assert st == 0 and rep["converged"] and rr.converged
+    assert abs(rep["iterations"] - rr.iterations) <= 1
+    assert np.linalg.norm(X.cpu().numpy() - Xr) / np.linalg.norm(Xr) <= 1e-8
+    X0 = torch.zeros_like(X)
+    _, rep0 = bk.block_krylov_solve(ctx, M, cu(B), X0, method="cg", rtol=1e-10, max_iters=2000, x0_is_zero=True)
+    assert 2 * rep["iterations"] < rep0["iterations"]
+    assert rep["n_spmm"] >= rep["iterations"] * 5       # 1 + (steps - 1) applies per iteration
