@@ -45,6 +45,11 @@ bool is_device_ptr(const void* p) {
     return attr.type == cudaMemoryTypeDevice || attr.type == cudaMemoryTypeManaged;
 }
 
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return e ? atoi(e) : dflt;
+}
+
 void* ws_get(bk_ctx* ctx, int slot, size_t bytes) {
     if ((int)ctx->ws.size() <= slot) ctx->ws.resize(slot + 1);
     bk_buf& b = ctx->ws[slot];
@@ -454,6 +459,8 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
     if (ctx->nranks == 1 || A->n_ghost == 0) {
         a.row0 = 0;
         a.nrows = A->n_local;
+        static const int walk = env_int("BK_PIPE_WALK", 0);
+        if (walk && A->band.nbands >= 3) a.walk_line = -(int64_t)A->band.dmin[A->band.nbands / 2 - 1];
         if (!launch_bspmm_win(a, A->band, ctx->stream)) launch_bspmm(a, ctx->stream);
         return post_launch(ctx, "bspmm_apply");
     }

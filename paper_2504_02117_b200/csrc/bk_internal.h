@@ -60,6 +60,7 @@ struct SpmmArgs {
     double alpha, beta;
     double* Y;
     int64_t ldy;
+    int64_t walk_line;      // pipe kernel: grid line length for the y-walk tile order (0: interleaved)
 };
 
 // out = a*Xin + s*(P C) + (w_host * (*w_dev)) * W     (any term may be absent)
@@ -167,6 +168,7 @@ void launch_cheb_step(int64_t n, int k, const double* R, int64_t ldr, const doub
 void launch_gershgorin(int64_t n, const int32_t* rp, const double* val, const double* dinv, unsigned long long* out,
                        cudaStream_t st);
 int allreduce_max(bk_ctx* ctx, double* d, int64_t n);
+int env_int(const char* name, int dflt);   // integer environment knob (A/B experiments)
 // Chebyshev interval after defaults (lmax <= 0: Gershgorin, lmin <= 0: lmax / 30)
 void cheb_bounds(const bk_csr* A, const bk_solve_opts* o, double* lmin, double* lmax);
 bool cheb_opts_ok(const bk_csr* A, const bk_solve_opts* o);

@@ -239,8 +239,6 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs& a, const int* col, con
 
 // ------------------------------------------------------------------ persistent TMA pipeline
 // NC consumer threads, NS ring stages, MINB CTAs per SM (variants: DESIGN.md §4.1)
-int env_int(const char* name, int dflt);
-
 template <int NC, int NS, int MINB, int TR_, int CAP_>
 struct PipeCfg {
     static constexpr int TR = TR_, CAP = CAP_;
@@ -259,14 +257,21 @@ struct PipeCfg {
 
 template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP, bool PAIR>
 __global__ void __launch_bounds__(NC + 32, MINB)
-bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int chunked) {
+bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
     using L = PipeCfg<NC, NS, MINB, TR, CAP>;
-    // tile order: interleaved over the CTAs (default), or one contiguous chunk per CTA
-    // (BK_PIPE_CHUNK=1; tried for L1 reuse of the y-1 / centre bands on 3-D lattices:
-    // 10-35 % slower -- the CTAs' z-neighbour rows are no longer L2-resident)
-    const int tb = chunked ? (int)((int64_t)blockIdx.x * ntiles / gridDim.x) : (int)blockIdx.x;
-    const int te = chunked ? (int)((int64_t)(blockIdx.x + 1) * ntiles / gridDim.x) : ntiles;
-    const int tstep = chunked ? 1 : (int)gridDim.x;
+    // tile order: interleaved over the CTAs (walk = 0, default), or a walk along y
+    // (walk = tiles per grid line w): CTA b takes x block b % w and walks a contiguous
+    // range of lines, so the X rows of the centre / y-1 bands were gathered by its own
+    // previous tiles (L1).  w = 1 is one contiguous chunk per CTA.  (BK_PIPE_WALK /
+    // BK_PIPE_CHUNK)
+    int tb = (int)blockIdx.x, te = ntiles, tstep = (int)gridDim.x;
+    if (walk > 0) {
+        const int nl = ntiles / walk, nch = (int)gridDim.x / walk, xb = (int)blockIdx.x % walk,
+                  ch = (int)blockIdx.x / walk;
+        tb = (int)((int64_t)ch * nl / nch) * walk + xb;
+        te = (int)((int64_t)(ch + 1) * nl / nch) * walk + xb;
+        tstep = walk;
+    }
     constexpr int LANES = KP / VEC;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * L::STAGE_BYTES);
@@ -357,10 +362,19 @@ void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
         attr = true;
     }
     const int64_t cap = (int64_t)MINB * num_sms;
-    const int64_t grid = ntiles < cap ? ntiles : cap;
+    int64_t grid = ntiles < cap ? ntiles : cap;
     static const int chunked = env_int("BK_PIPE_CHUNK", 0) > 0;
+    int walk = chunked ? 1 : 0;
+    if (a.walk_line > 0 && a.walk_line % TR == 0) {   // y walk: tiles per line, whole lines only
+        const int w = (int)(a.walk_line / TR);
+        if (ntiles % w == 0 && cap >= w) {
+            walk = w;
+            grid = (cap / w) * w;
+            if (grid > ntiles) grid = ntiles;
+        }
+    }
     BK_KERNEL(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR><<<(unsigned)grid, NC + 32, smem, st>>>(
-        a, (int)ntiles, chunked));
+        a, (int)ntiles, walk));
 }
 
 // ------------------------------------------------------------------ simple tile kernel (A/B variant)
@@ -800,10 +814,6 @@ bspmm_win_kernel(const BandArgs w) {
     }
 }
 
-int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return e ? atoi(e) : dflt;
-}
 
 // ------------------------------------------------------------------ rolling-window apply (lattice stencils)
 // DESIGN.md §4.1.  For a band plan with lattice structure (2-D: bands -nx, [-1,1], +nx;
