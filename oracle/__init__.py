@@ -561,3 +561,8 @@ def dirk_fixed_point(L, K, mass, tau, A1, A2, B, B0, Y0, iters, inner=None):
         Y = np.linalg.solve(Ld, rhs) if inner is None else inner(L, rhs, Y)
         hist.append(Y.copy())
     return Y, hist
+
+
+# --------------------------------------------------------------------------- O10 (NEXT-3)
+from .alg1 import (DRProblem, algorithm1, dr_f, dr_jacobian, iota, residual as alg1_residual,  # noqa: E402,F401
+                   sequential_dirk, shift as alg1_shift, window_A)

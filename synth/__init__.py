@@ -499,3 +499,14 @@ def expected_nnz(shape3) -> int:
     if nz == 1:
         return 5 * N - 2 * (nx + ny)
     return 7 * N - 2 * (nx * ny + ny * nz + nx * nz)
+
+
+# ---------------------------------------------------------------------------
+# NEXT-3 (Algorithm 1): seeded fields of the nonlinear diffusion-reaction problem
+# (initial state y0 and source field g; the operator itself is method arithmetic and
+# lives in oracle/alg1.py and the CUDA kernels, R29)
+# ---------------------------------------------------------------------------
+def dr_fields(nx: int, ny: int, nz: int, seed: int = 1, device="cpu"):
+    """(y0, g): U(0,1) per cell (streams 11, 12), lexicographic x-fastest numbering."""
+    idx = torch.arange(nx * ny * nz, dtype=torch.int64, device=device)
+    return uniform01(seed, 11, idx), uniform01(seed, 12, idx)
