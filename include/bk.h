@@ -252,6 +252,42 @@ int bk_dirk_solve(bk_ctx *ctx, const bk_csr *L, const bk_csr *K, double mass, do
                   double *Y, int64_t ldy, int max_outer, double outer_tol,
                   const bk_solve_opts *inner, bk_dirk_report *rep);
 
+/* NEXT-3: Algorithm 1 "Block Krylov Time Stepping with Pipelining" (§2.2
+ * P:600-621; eq. matrix-equation-pipelining; shift P:592-594; iota P:574-580)
+ * on the nonlinear diffusion-reaction problem M y' + f(t, y) = 0 of an nx x ny x nz
+ * cell-centred lattice (x fastest; h = 1/nx; M = h^3 I; Neumann; R29):
+ *   f(t,u)_a = sum_b h D_ab (u_a - u_b) + h^3 (u_a - u_a^2) - h^3 sin(1 + t) g_a,
+ *   D_ab = 1 + (u_a^2 + u_b^2)/2,
+ * stepped with the stiffly accurate DIRK tableau A (m x m row-major, host; c = A 1),
+ * t^n = n tau, a pipelined window of `window` consecutive stages.  Per stage: shift;
+ * Newton loop: R = M Y A1^T + F(T,Y) A2^T - B0 (sign reading R30); stop when
+ * ||R_0||_2 < eps; J = M/tau + a_kk Df(t, Y_0) assembled on the device; solve J V = R
+ * with block_krylov_solve(inner, x0 = 0, k = window); Y -= V.
+ * y0, g: N = nx ny nz doubles (host or device).  traj: N x n_steps row-major with
+ * leading dimension ldt >= n_steps (host or device; column n = y^{n+1}), may be NULL.
+ * newton_its: host int[n_steps * m] (Newton iterations per accepted stage) or NULL.
+ * Single rank only (nranks == 1).  Returns BK_OK, BK_NOT_CONVERGED (a stage needed
+ * more than max_newton iterations; rep->failed_stage) or an error status.           */
+typedef struct bk_dr_problem {
+    int64_t nx, ny, nz;
+    double  tau;
+    const double *y0;
+    const double *g;
+} bk_dr_problem;
+typedef struct bk_alg1_report {
+    int    status;
+    int    stages_accepted;
+    int    newton_iterations_total;
+    int    inner_iterations_total;
+    int    inner_breakdowns;
+    int    failed_stage;
+    double last_norm;
+    double t_total_ms;
+} bk_alg1_report;
+int bk_alg1_run(bk_ctx *ctx, const bk_dr_problem *prob, int m, const double *A, int n_steps, int window,
+                double eps, int max_newton, const bk_solve_opts *inner, double *traj, int64_t ldt,
+                int *newton_its, bk_alg1_report *rep);
+
 /* ---------------------------------------------------------------- host-only
  * Halo plan of a contiguous row partition (pure host code, no CUDA; exported
  * for CPU tests of the multi-GPU path).  Given this rank's local CSR columns

@@ -38,7 +38,7 @@ EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last
             "bk_ctx_synchronize", "bk_ctx_destroy", "bk_get_nccl_unique_id", "bk_ctx_set_comm",
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
             "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo",
-            "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply"]
+            "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply", "bk_alg1_run"]
 
 
 class SolveOpts(ctypes.Structure):
@@ -95,6 +95,7 @@ _sig = {
     "bk_plan_bands": ([_I64, _P, _P, _I, _P], _I),
     "bk_dirk_solve": ([_P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _I64, _P, _I64, _I, _D, _P, _P], _I),
     "bk_precond_apply": ([_P, _P, _I, _P, _P, _I64, _P, _I64], _I),
+    "bk_alg1_run": ([_P, _P, _I, _P, _I, _I, _D, _I, _P, _P, _I64, _P, _P], _I),
 }
 for _n, (_a, _r) in _sig.items():
     _f = getattr(_lib, _n)
@@ -360,6 +361,46 @@ def precond_apply(ctx: Context, A: Matrix, R, Z, precond="chebyshev", cheb_steps
     ctx.check(_lib.bk_precond_apply(ctx.handle, A.handle, kr, ctypes.byref(o), _P(pr), ldr, _P(pz), ldz),
               "bk_precond_apply")
     return Z
+
+
+class DrProblem(ctypes.Structure):
+    _fields_ = [("nx", ctypes.c_int64), ("ny", ctypes.c_int64), ("nz", ctypes.c_int64), ("tau", ctypes.c_double),
+                ("y0", ctypes.c_void_p), ("g", ctypes.c_void_p)]
+
+
+class Alg1Report(ctypes.Structure):
+    _fields_ = [("status", ctypes.c_int), ("stages_accepted", ctypes.c_int),
+                ("newton_iterations_total", ctypes.c_int), ("inner_iterations_total", ctypes.c_int),
+                ("inner_breakdowns", ctypes.c_int), ("failed_stage", ctypes.c_int), ("last_norm", ctypes.c_double),
+                ("t_total_ms", ctypes.c_double)]
+
+
+def alg1_run(ctx: Context, nx, ny, nz, tau, y0, g, A_tab, n_steps, window, eps, *, max_newton=50, traj=None,
+             **inner):
+    """Algorithm 1 (bk_alg1_run, NEXT-3).  y0, g: N-vectors (torch, host or device).  traj:
+    optional N x n_steps output (torch, host or device).  Returns (status, newton its per stage,
+    report dict)."""
+    import torch
+    y0 = y0.contiguous()
+    g = g.contiguous()
+    for t, nm in ((y0, "y0"), (g, "g")):
+        if t.dtype != torch.float64 or t.numel() != nx * ny * nz:
+            raise ValueError(f"{nm} must be float64 with nx*ny*nz entries")
+    A = np.ascontiguousarray(np.asarray(A_tab, dtype=np.float64))
+    m = A.shape[0]
+    pb = DrProblem(nx, ny, nz, float(tau), y0.data_ptr(), g.data_ptr())
+    pt, ldt = (None, 0)
+    if traj is not None:
+        pt, nt, kt, ldt = _mv(traj, "traj")
+    its = (ctypes.c_int * max(1, n_steps * m))()
+    o = solve_opts(**inner)
+    rep = Alg1Report()
+    st = _lib.bk_alg1_run(ctx.handle, ctypes.byref(pb), m, A.ctypes.data, n_steps, window, float(eps), max_newton,
+                          ctypes.byref(o), _P(pt), ldt, its, ctypes.byref(rep))
+    if st not in (BK_OK, BK_NOT_CONVERGED):
+        ctx.check(st, "bk_alg1_run")
+    out = {f: getattr(rep, f) for f, _ in Alg1Report._fields_}
+    return st, list(its[:n_steps * m]), out
 
 
 def plan_halo(nranks: int, rank: int, rank_begin, row_ptr, col_global):

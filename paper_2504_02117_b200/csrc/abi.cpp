@@ -708,6 +708,34 @@ extern "C" int bk_precond_apply(bk_ctx* ctx, const bk_csr* A, int k, const bk_so
     BK_CATCH(ctx)
 }
 
+// ------------------------------------------------------------------ NEXT-3 Algorithm 1 (alg1.cpp)
+extern "C" int bk_alg1_run(bk_ctx* ctx, const bk_dr_problem* pb, int m, const double* A, int n_steps, int window,
+                           double eps, int max_newton, const bk_solve_opts* inner, double* traj, int64_t ldt,
+                           int* newton_its, bk_alg1_report* rep) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, pb && A && inner && rep, "bk_alg1_run: NULL problem/tableau/opts/report");
+    ARG_CHECK(ctx, ctx->nranks <= 1, "bk_alg1_run: single rank only");
+    ARG_CHECK(ctx, pb->nx >= 1 && pb->ny >= 1 && pb->nz >= 1 && pb->nx * pb->ny * pb->nz < (1ll << 31) &&
+                       pb->tau > 0.0 && pb->y0 && pb->g,
+              "bk_alg1_run: bad lattice / tau / NULL y0, g");
+    ARG_CHECK(ctx, m >= 1 && m <= 8 && n_steps >= 0 && window >= 1 && window <= BK_MAX_K && eps > 0.0 &&
+                       max_newton >= 0,
+              "bk_alg1_run: need 1 <= m <= 8, n_steps >= 0, 1 <= window <= 32, eps > 0, max_newton >= 0");
+    ARG_CHECK(ctx, !is_device_ptr(A), "bk_alg1_run: A must be a host array");
+    ARG_CHECK(ctx, !traj || ldt >= n_steps, "bk_alg1_run: ldt < n_steps");
+    ARG_CHECK(ctx, inner->method >= BK_CG && inner->method <= BK_BICGSTAB && inner->check_every >= 1 &&
+                       inner->max_iters >= 0 && inner->rtol >= 0.0 &&
+                       (inner->method != BK_GMRES || (int64_t)(inner->restart + 1) * window <= BK_MAX_KA),
+              "bk_alg1_run: bad inner solver options");
+    for (int i = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j)
+            ARG_CHECK(ctx, A[i * m + j] == 0.0, "bk_alg1_run: A must be lower triangular (DIRK)");
+    BK_TRY
+    return alg1_impl(ctx, pb, m, A, n_steps, window, eps, max_newton, inner, traj, ldt, newton_its, rep);
+    BK_CATCH(ctx)
+}
+
 // ------------------------------------------------------------------ NEXT-1 DIRK window (dirk.cpp)
 extern "C" int bk_dirk_solve(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k,
                              const double* A1, const double* A2, const double* B, const double* B0, int64_t ldb,

@@ -168,6 +168,14 @@ void launch_cheb_step(int64_t n, int k, const double* R, int64_t ldr, const doub
 void launch_gershgorin(int64_t n, const int32_t* rp, const double* val, const double* dinv, unsigned long long* out,
                        cudaStream_t st);
 int allreduce_max(bk_ctx* ctx, double* d, int64_t n);
+int alg1_impl(bk_ctx* ctx, const bk_dr_problem* pb, int m, const double* A, int n_steps, int w, double eps,
+              int max_newton, const bk_solve_opts* inner, double* traj, int64_t ldt, int* newton_its,
+              bk_alg1_report* rep);
+// NEXT-3 nonlinear diffusion-reaction operator (nonlin.cu; oracle O10)
+void launch_dr_f(int64_t nx, int64_t ny, int64_t nz, double h, const double* Y, int64_t ldy, int w,
+                 const double* sinT, const double* g, double* F, int64_t ldf, cudaStream_t st);
+void launch_dr_jac(int64_t nx, int64_t ny, int64_t nz, double h, const double* u, int64_t ldu, double shift,
+                   double scale, const int32_t* rp, const int32_t* col, double* val, int* bad, cudaStream_t st);
 int env_int(const char* name, int dflt);   // integer environment knob (A/B experiments)
 // Chebyshev interval after defaults (lmax <= 0: Gershgorin, lmin <= 0: lmax / 30)
 void cheb_bounds(const bk_csr* A, const bk_solve_opts* o, double* lmin, double* lmax);

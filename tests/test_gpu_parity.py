@@ -529,3 +529,57 @@ def test_chebyshev_pcg_matches_oracle_and_cuts_iterations(ctx, bk, k):
     _, rep0 = bk.block_krylov_solve(ctx, M, cu(B), X0, method="cg", rtol=1e-10, max_iters=2000, x0_is_zero=True)
     assert 2 * rep["iterations"] < rep0["iterations"]
     assert rep["n_spmm"] >= rep["iterations"] * 5       # 1 + (steps - 1) applies per iteration
+
+
+# ----------------------------------------------------------------------------- NEXT-3 Algorithm 1
+ALG1_CASES = [("sdirk2", 1, (6, 5, 4)), ("sdirk2", 2, (6, 5, 4)), ("sdirk3", 3, (6, 5, 4)),
+              ("sdirk3", 1, (12, 10, 9)), ("sdirk3", 4, (12, 10, 9))]
+
+
+@pytest.mark.parametrize("tab,window,shape", ALG1_CASES)
+def test_alg1_matches_oracle(ctx, bk, tab, window, shape):
+    nx, ny, nz = shape
+    tau, nst = 0.05, 3
+    A = synth.SDIRK2 if tab == "sdirk2" else synth.SDIRK3
+    y0, g = synth.dr_fields(nx, ny, nz, 1)
+    P = oracle.DRProblem(nx, ny, nz, y0.numpy(), g.numpy(), tau)
+    eps = 1e-12 * np.sqrt(P.N) * P.mass / P.tau
+    ref, its_ref = oracle.algorithm1(P, A, nst, window, eps=eps)
+    traj = torch.full((P.N, nst), float("nan"), dtype=torch.float64, device="cuda")
+    st, its, rep = bk.alg1_run(ctx, nx, ny, nz, tau, cu(y0), cu(g), A, nst, window, eps, traj=traj,
+                               method="gmres", restart=60, rtol=1e-14, max_iters=600)
+    assert st == 0 and rep["stages_accepted"] == nst * len(A)
+    assert np.abs(traj.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
+    # Newton counts: the accept test sits at eps; inexact (1e-14) inner solves may move a
+    # borderline stage by one iteration
+    assert sum(abs(a - b) for a, b in zip(its, its_ref)) <= 2, (its, its_ref)
+    trh = torch.zeros(P.N, nst, dtype=torch.float64)               # host trajectory + host y0 / g
+    st2, its2, _ = bk.alg1_run(ctx, nx, ny, nz, tau, y0, g, A, nst, window, eps, traj=trh,
+                               method="gmres", restart=60, rtol=1e-14, max_iters=600)
+    assert st2 == 0 and torch.equal(trh, traj.cpu()) and its2 == its
+
+
+def test_alg1_pipelining_single_newton_after_warmup(ctx, bk):
+    """PAPER.md remark (non-linear convergence): with a full window every stage converges after
+    one Newton iteration once the pipeline is warm (the oracle shows the same, O10)."""
+    nx, ny, nz, tau, nst = 12, 10, 9, 0.05, 4
+    A = synth.SDIRK3
+    y0, g = synth.dr_fields(nx, ny, nz, 1)
+    P = oracle.DRProblem(nx, ny, nz, y0.numpy(), g.numpy(), tau)
+    eps = 1e-10 * np.sqrt(P.N) * P.mass / P.tau
+    st, its, rep = bk.alg1_run(ctx, nx, ny, nz, tau, cu(y0), cu(g), A, nst, 3, eps, method="bicgstab",
+                               rtol=1e-12, max_iters=500)
+    assert st == 0
+    assert all(i == 1 for i in its[-3:]), its
+    st1, its1, _ = bk.alg1_run(ctx, nx, ny, nz, tau, cu(y0), cu(g), A, nst, 1, eps, method="bicgstab",
+                               rtol=1e-12, max_iters=500)
+    assert sum(its) < sum(its1)
+
+
+def test_alg1_not_converged_and_bad_args(ctx, bk):
+    y0, g = synth.dr_fields(4, 4, 4, 1)
+    st, its, rep = bk.alg1_run(ctx, 4, 4, 4, 0.05, cu(y0), cu(g), synth.SDIRK2, 2, 2, 1e-300, max_newton=2,
+                               method="gmres", rtol=1e-12)
+    assert st == 2 and rep["failed_stage"] == 0
+    with pytest.raises(Exception):
+        bk.alg1_run(ctx, 4, 4, 4, 0.05, cu(y0), cu(g), [[0.5, 0.1], [0.5, 0.5]], 1, 1, 1e-8)   # not DIRK
