@@ -356,6 +356,23 @@ def run_ours(args):
             ts.append(a.elapsed_time(b))
         solve_report = {"c1_gmres_k4_ms": statistics.median(ts), "iterations": rep["iterations"],
                         "converged": rep["converged"], "max_true_relres": float(max(rep["true_relres"]))}
+        # block CG (symmetric c1 variant) and block BiCGStab to 1e-10, iterations replayed from a
+        # CUDA graph (bk_solve_opts.use_graphs), convergence polled every 8 iterations
+        for name, cfg1, meth in (("c1s_cg_k4", "c1s", "cg"), ("c1_bicgstab_k4", "c1", "bicgstab")):
+            A1 = synth.make_matrix(cfg1)
+            M1 = bk.Matrix.from_csr(ctx, A1)
+            ts = []
+            for _ in range(5):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(stream)
+                st, rep = bk.block_krylov_solve(ctx, M1, B1, X1, method=meth, rtol=1e-10, x0_is_zero=True,
+                                                use_graphs=True, check_every=8)
+                b.record(stream)
+                torch.cuda.synchronize()
+                ts.append(a.elapsed_time(b))
+            solve_report[name + "_graphs_ms"] = statistics.median(ts)
+            solve_report[name + "_iterations"] = rep["iterations"]
+            solve_report[name + "_max_true_relres"] = float(max(rep["true_relres"]))
 
     # ---- e2e: same step through the C ABI with pinned HOST buffers (H2D/D2H inside the timed region)
     e2e = None

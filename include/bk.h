@@ -178,7 +178,10 @@ typedef struct bk_solve_opts {
     int    conv_mode;       /* enum bk_conv                                   */
     int    x0_is_zero;      /* 1: ignore X on entry                           */
     int    check_every;     /* host-side convergence poll period (>= 1)       */
-    int    use_graphs;      /* reserved (ignored): iterations are enqueued    */
+    int    use_graphs;      /* 1: CG / BiCGStab iterations replayed from a CUDA
+                               graph captured once per solve (one rank, timing
+                               off; GMRES ignores it) -- for small, launch-bound
+                               systems                                        */
     double rtol;
     double breakdown_tol;   /* relative pivot threshold (default 1e-13)       */
     int    timing;          /* 1: CUDA events around every N x k kernel on the

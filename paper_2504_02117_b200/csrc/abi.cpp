@@ -212,6 +212,7 @@ extern "C" int bk_ctx_destroy(bk_ctx* ctx) {
     for (cudaEvent_t e : ctx->tev) cudaEventDestroy(e);
     for (auto& b : ctx->ws)
         if (b.p) cudaFree(b.p);
+    if (ctx->cap_stream) cudaStreamDestroy(ctx->cap_stream);
     if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
     if (ctx->d_tickets) cudaFree(ctx->d_tickets);
 #ifndef BK_NO_NCCL

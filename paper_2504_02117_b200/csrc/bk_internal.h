@@ -242,6 +242,7 @@ struct bk_ctx {
     int num_sms = 148;
     int sticky = 0;
     std::string last_error;
+    cudaStream_t cap_stream = nullptr;   // CUDA graph capture (bk_solve_opts.use_graphs)
     std::vector<bk_buf> ws;       // slot-indexed grow-only device workspaces
     double* h_pinned = nullptr;   // pinned host staging for small results
     int* d_tickets = nullptr;     // zeroed device counters for last-CTA reductions

@@ -158,6 +158,73 @@ struct Solver {
         return r;
     }
 
+    // Runs body() (one iteration) until max_iters or a halt, polling every check_every
+    // iterations.  opts.use_graphs (one rank, no timing): after `period` eager iterations
+    // (buffers allocated, kernel attributes set), `period` iterations are captured once into
+    // a CUDA graph and replayed -- their kernel arguments are fixed (period 2 where the body
+    // swaps two k x k buffers) and every update after a halt is a no-op, so replays past
+    // convergence leave X unchanged.
+    template <class F>
+    int iterate(int period, F&& body) {
+        const int maxit = o->max_iters, ce = o->check_every;
+        bool graphs = o->use_graphs && !allred && !o->timing && n > 0;
+        cudaGraphExec_t exec = nullptr;
+        int64_t dl = 0, dsp = 0, dgr = 0, dup = 0, dsm = 0;   // per replay: launches, counters
+        auto due = [&](int done) { return done % ce == 0 || done == maxit; };
+        int it = 0, r = 0;
+        while (it < maxit) {
+            if (graphs && !exec && it >= period && maxit - it >= period) {
+                const int64_t l0 = g_launches.load(), s0 = rep->n_spmm, g0 = rep->n_gram, u0 = rep->n_update,
+                              m0 = rep->n_small;
+                cudaGraph_t gph = nullptr;
+                // capture on a private non-blocking stream (the ctx stream may be the legacy
+                // default stream, which cannot be captured); replays go to the ctx stream
+                if (!ctx->cap_stream) cudaStreamCreateWithFlags(&ctx->cap_stream, cudaStreamNonBlocking);
+                cudaStream_t keep = st;
+                st = ctx->stream = ctx->cap_stream;
+                bool ok = st && cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed) == cudaSuccess;
+                for (int q = 0; ok && q < period; ++q) ok = body() == 0;
+                ok = (cudaStreamEndCapture(st, &gph) == cudaSuccess) && ok && gph;
+                st = ctx->stream = keep;
+                ok = ok && cudaGraphInstantiate(&exec, gph, 0) == cudaSuccess;
+                if (gph) cudaGraphDestroy(gph);
+                cudaGetLastError();
+                dl = g_launches.load() - l0;   // captured, not launched yet
+                g_launches -= dl;
+                dsp = rep->n_spmm - s0; dgr = rep->n_gram - g0; dup = rep->n_update - u0; dsm = rep->n_small - m0;
+                rep->n_spmm = s0; rep->n_gram = g0; rep->n_update = u0; rep->n_small = m0;
+                if (!ok) {   // fall back to eager launches
+                    if (exec) cudaGraphExecDestroy(exec);
+                    exec = nullptr;
+                    graphs = false;
+                    ctx->last_error.clear();
+                    continue;
+                }
+            }
+            if (exec && maxit - it >= period) {
+                if ((r = cuda_check(ctx, cudaGraphLaunch(exec, st), "graph launch"))) break;
+                rep->n_spmm += dsp; rep->n_gram += dgr; rep->n_update += dup; rep->n_small += dsm;
+                g_launches += dl;
+                bool p = false;
+                for (int q = 1; q <= period; ++q) p = p || due(it + q);
+                it += period;
+                if (p) {
+                    if ((r = poll())) break;
+                    if (hs->halt) break;
+                }
+                continue;
+            }
+            if ((r = body())) break;
+            ++it;
+            if (due(it)) {
+                if ((r = poll())) break;
+                if (hs->halt) break;
+            }
+        }
+        if (exec) cudaGraphExecDestroy(exec);
+        return r;
+    }
+
     int spmm(const double* X, int64_t ldx, double* Y, int64_t ldy, double alpha = 1.0, double beta = 0.0) {
         rep->n_spmm++;
         tb();
@@ -349,7 +416,7 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     e_al.kind = 4; e_al.k = k; e_al.st = S.ds; e_al.G = PQ; e_al.Rhs = RZ; e_al.Out = al; e_al.tol = tol;
     e_be.kind = 5; e_be.k = k; e_be.st = S.ds; e_be.g = RZn; e_be.Rhs = RZ; e_be.Out = be; e_be.tol = tol;
     e_be.rtol = S.o->rtol; e_be.conv_mode = S.o->conv_mode;
-    for (int it = 0; fused && it < S.o->max_iters; ++it) {
+    auto cg_fused = [&]() -> int {
         TRY(S.spmm(P, k, Q, k));
         const double* arr[2] = {P, Q};
         const int xs[1] = {0}, ys[1] = {1};
@@ -376,12 +443,9 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
         }
         S.rep->n_small += 2;
         TRY(S.upd(P, k, 1.0, R, k, 1.0, P, k, k, be));
-        if ((it + 1) % S.o->check_every == 0 || it + 1 == S.o->max_iters) {
-            TRY(S.poll());
-            if (S.hs->halt) break;
-        }
-    }
-    for (int it = 0; !fused && it < S.o->max_iters; ++it) {
+        return 0;
+    };
+    auto cg_plain = [&]() -> int {
         TRY(S.spmm(P, k, Q, k));
         TRY(S.gram(P, k, k, Q, k, PQ));
         sd_chol_solve(PQ, RZ, al, k, k, tol, S.ds, S.st);
@@ -401,11 +465,11 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
         S.rep->n_small += 2;
         TRY(S.upd(P, k, 1.0, Z, k, 1.0, P, k, k, be));
         std::swap(RZ, RZn);
-        if ((it + 1) % S.o->check_every == 0 || it + 1 == S.o->max_iters) {
-            TRY(S.poll());
-            if (S.hs->halt) break;
-        }
-    }
+        return 0;
+    };
+    // (the RZ / RZn swap makes two iterations the period of the launch sequence)
+    if (fused) TRY(S.iterate(epi ? 1 : 2, cg_fused));
+    else TRY(S.iterate(2, cg_plain));
     return finish(S, B, ldb, X, ldx, e0);
 }
 
@@ -456,7 +520,7 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     e_be.kind = 2; e_be.k = k; e_be.st = S.ds; e_be.ts = ts; e_be.tt = tt; e_be.Rhs = RtT; e_be.Out = be;
     e_be.sign = -1.0; e_be.LU = LUf; e_be.piv = piv;
     e_cv.kind = 3; e_cv.k = k; e_cv.st = S.ds; e_cv.g = nr; e_cv.rtol = S.o->rtol; e_cv.conv_mode = S.o->conv_mode;
-    for (int it = 0; it < S.o->max_iters; ++it) {
+    auto iteration = [&]() -> int {
         TRY(S.spmm(P, k, V, k));
         if (fused) {
             const double* arr[3] = {Rt, V, R};
@@ -510,11 +574,9 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
             TRY(S.upd(Tmp, k, 1.0, P, k, 0.0, nullptr, k, 0, nullptr, V, k, 1.0, nom));
             TRY(S.upd(P, k, 1.0, R, k, 1.0, Tmp, k, k, be));
         }
-        if ((it + 1) % S.o->check_every == 0 || it + 1 == S.o->max_iters) {
-            TRY(S.poll());
-            if (S.hs->halt) break;
-        }
-    }
+        return 0;
+    };
+    TRY(S.iterate(1, iteration));
     return finish(S, B, ldb, X, ldx, e0);
 }
 

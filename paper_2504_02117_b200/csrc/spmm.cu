@@ -41,13 +41,24 @@ struct Batch { static constexpr int B = VEC >= 8 ? 2 : (VEC >= 4 ? 4 : 8); };
 // ------------------------------------------------------------------ PTX helpers
 
 __device__ __forceinline__ void ld_x(const double* p, double (&x)[1]) { x[0] = __ldg(p); }
+// VEC % 4 == 0: 256-bit loads (sm_100 LDG.E.ENL2.256; rows 32-byte aligned, launch_k checks):
+// the k/4 lanes of a row cover a whole 128-byte X line per instruction -- half the L1
+// wavefronts of 128-bit loads (the gather-bound pipe kernel runs L1TEX at 98 %)
 template <int VEC>
-__device__ __forceinline__ void ld_x(const double* p, double (&x)[VEC]) {
+__device__ __forceinline__ void ld_x(const double* __restrict__ p, double (&x)[VEC]) {
+    if constexpr (VEC % 4 == 0) {
 #pragma unroll
-    for (int t = 0; t < VEC; t += 2) {
-        double2 v = __ldg(reinterpret_cast<const double2*>(p) + t / 2);
-        x[t] = v.x;
-        x[t + 1] = v.y;
+        for (int t = 0; t < VEC; t += 4)
+            asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+                         : "=d"(x[t]), "=d"(x[t + 1]), "=d"(x[t + 2]), "=d"(x[t + 3])
+                         : "l"(p + t));
+    } else {
+#pragma unroll
+        for (int t = 0; t < VEC; t += 2) {
+            double2 v = __ldg(reinterpret_cast<const double2*>(p) + t / 2);
+            x[t] = v.x;
+            x[t + 1] = v.y;
+        }
     }
 }
 
@@ -512,7 +523,11 @@ int max_vec() {
 template <int KP>
 void launch_k(const SpmmArgs& a, cudaStream_t st, bool vec2) {
     // a lane's VEC columns must lie inside the row: k, k_out multiples of VEC
-    const int mv = max_vec();
+    const int mv0 = max_vec();
+    // 4- and 8-column lanes gather with 256-bit loads: 32-byte aligned X (and ghost) rows
+    const bool al32 = ((uintptr_t)a.X % 32 == 0) && (a.ldx % 4 == 0) &&
+                      (a.Xg == nullptr || (((uintptr_t)a.Xg % 32 == 0) && a.ldg % 4 == 0));
+    const int mv = al32 ? mv0 : 2;
     if constexpr (KP >= 8) {
         if (vec2 && mv >= 8 && a.k % 8 == 0 && a.kout % 8 == 0) return launch_kv<KP, 8>(a, st);
     }
@@ -1362,8 +1377,11 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     // 3-D lattices (5 bands): the plain apply is faster with L1 gathers (pipe kernel,
     // c4 k = 16: 0.66 vs 0.57 of HBM) -- staging 5 band segments fills shared memory
     // with L2-hit bytes; the coupled apply keeps the DMMA tile epilogue
+    // The same holds for k > 16 on 2-D lattices once the gathers are 256-bit loads (c2 k = 32:
+    // 0.65 vs 0.63, k = 24: 0.54 vs 0.49; the band kernel is shared-memory bound there,
+    // L1TEX 83 %).
     static const int w3 = env_int("BK_WIN_3D", -1);
-    if (w3 < 0 && p.nbands >= 5 && a.C == nullptr) return false;
+    if (w3 < 0 && a.C == nullptr && (p.nbands >= 5 || a.k > 16)) return false;
     if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
     // the window copies contiguous X rows: packed X (ldx == k), 16-byte aligned
     if (a.ldx != a.k || ((uintptr_t)a.X % 16) != 0) return false;

@@ -583,3 +583,25 @@ def test_alg1_not_converged_and_bad_args(ctx, bk):
     assert st == 2 and rep["failed_stage"] == 0
     with pytest.raises(Exception):
         bk.alg1_run(ctx, 4, 4, 4, 0.05, cu(y0), cu(g), [[0.5, 0.1], [0.5, 0.5]], 1, 1, 1e-8)   # not DIRK
+
+
+# ----------------------------------------------------------------------------- CUDA graph replay
+@pytest.mark.parametrize("method,cfg,k", [("cg", "c1s", 4), ("cg", "c1s", 8), ("cg", "c1s", 16),
+                                          ("bicgstab", "c1", 4), ("bicgstab", "c1", 16)])
+def test_graph_replay_is_bitwise_identical(ctx, bk, method, cfg, k):
+    """bk_solve_opts.use_graphs replays the captured iteration: same kernels, same order, so the
+    iterate is bitwise identical; polling every 8 iterations adds only halted (no-op) iterations."""
+    A = synth.make_matrix(cfg)
+    B = cu(synth.multivector(A.n_rows, k, 2))
+    M = bk.Matrix.from_csr(ctx, A)
+    X0 = torch.zeros(A.n_rows, k, dtype=torch.float64, device="cuda")
+    st0, r0 = bk.block_krylov_solve(ctx, M, B, X0, method=method, rtol=1e-10, x0_is_zero=True)
+    for ce in (1, 8):
+        X1 = torch.zeros_like(X0)
+        n0 = bk.kernel_launch_count()
+        st1, r1 = bk.block_krylov_solve(ctx, M, B, X1, method=method, rtol=1e-10, x0_is_zero=True,
+                                        use_graphs=True, check_every=ce)
+        assert bk.kernel_launch_count() > n0
+        assert st1 == st0 == 0 and r1["iterations"] == r0["iterations"]
+        assert torch.equal(X1, X0)
+        assert np.array_equal(r1["true_relres"], r0["true_relres"])

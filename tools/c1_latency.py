@@ -21,7 +21,9 @@ for cfg, meth, kw in (("c1", "gmres", {"restart": 100}), ("c1s", "cg", {}), ("c1
     M = bk.Matrix.from_csr(ctx, A)
     B = synth.multivector(A.n_rows, 4, 2, device="cuda")
     X = torch.zeros_like(B)
-    for ce in (1, 4, 16):
+    for ce, gr in ((1, False), (4, False), (16, False), (1, True), (16, True)):
+        if gr and meth == "gmres":
+            continue
         ts = []
         for r in range(6):
             torch.cuda.synchronize()
@@ -29,7 +31,7 @@ for cfg, meth, kw in (("c1", "gmres", {"restart": 100}), ("c1s", "cg", {}), ("c1
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             st, rep = bk.block_krylov_solve(ctx, M, B, X, method=meth, rtol=1e-10, x0_is_zero=True, check_every=ce,
-                                            **kw)
+                                            use_graphs=gr, **kw)
             e1.record()
             torch.cuda.synchronize()
             nl = bk.kernel_launch_count() - n0
@@ -37,7 +39,7 @@ for cfg, meth, kw in (("c1", "gmres", {"restart": 100}), ("c1s", "cg", {}), ("c1
                 ts.append(e0.elapsed_time(e1))
         st, rt = bk.block_krylov_solve(ctx, M, B, X, method=meth, rtol=1e-10, x0_is_zero=True, check_every=ce,
                                        timing=True, **kw)
-        print(json.dumps({"cfg": cfg, "method": meth, "check_every": ce, "ms": round(statistics.median(ts), 3),
+        print(json.dumps({"cfg": cfg, "method": meth, "check_every": ce, "graphs": gr, "ms": round(statistics.median(ts), 3),
                           "iterations": rep["iterations"], "launches": nl,
                           "us_per_iter": round(1e3 * statistics.median(ts) / max(rep["iterations"], 1), 1),
                           "t_class_ms": {c: round(v, 3) for c, v in rt["t_class_ms"].items() if v},

@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-timeout 600 python tools/alg1_timing.py > gpurun_out/alg1_c3.jsonl 2>&1
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_step.csv python bench.py --profile-step --steps 1 --warmup 1 --no-sweep --no-e2e --no-configs > gpurun_out/ncu_step.log 2>&1
-KEEP= bash tools/ncu_cap.sh spmm_k32 "bspmm_win_kernel" python tools/one_apply.py --cfg c2 --k 32 > /dev/null 2>&1
-bash tools/ncu_cap.sh pipe_c4_k16 "bspmm_pipe_kernel" python tools/one_apply.py --cfg c4 --k 16 > /dev/null 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/t_all.log 2>&1
+timeout 300 python tools/sweep.py --cfg c2 --ks 16,24,32 --ops spmm > gpurun_out/v4_c2b.jsonl 2>&1
