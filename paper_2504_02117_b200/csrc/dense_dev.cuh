@@ -36,6 +36,9 @@ __device__ __forceinline__ void load_rows_w(const double* __restrict__ src, doub
 // LU with partial pivoting (explicit row swaps), Out = G^{-1} (sign Rhs).
 // LUo / pivo (optional): the factors (P G = L U, unit L below the diagonal,
 // getrf layout) and the pivot row of each step, for lu_resolve_w.
+// Column-parallel elimination: lane c owns column c of [A | B] (k + nrhs <= 64: two
+// columns per lane), so step j costs k - j - 1 fused updates per lane; pivots and
+// 1/U_jj are broadcast.
 __device__ __forceinline__ void lu_solve_warp(int defer, const double* __restrict__ G, const double* __restrict__ Rhs,
                                               double* __restrict__ Out, int k, int nrhs, double sign, double tol,
                                               DevStatus* st, double* __restrict__ LUo, int* __restrict__ pivo,
@@ -50,6 +53,8 @@ __device__ __forceinline__ void lu_solve_warp(int defer, const double* __restric
         if (l < k) mx = fmax(mx, fabs(A[r * LD + l]));
     mx = wmax(mx);
     if (!(mx > 0.0)) mx = 2.2250738585072014e-308;
+    // the two columns of lane l: A column l (if l < k) and B column l (if l < nrhs)
+    const bool ha = l < k, hb = l < nrhs;
 #pragma unroll 1
     for (int j = 0; j < k; ++j) {
         double v = (l >= j && l < k) ? fabs(A[l * LD + j]) : -1.0;
@@ -68,19 +73,21 @@ __device__ __forceinline__ void lu_solve_warp(int defer, const double* __restric
             return;
         }
         if (l == 0) s_piv[j] = p;
-        if (p != j) {   // lane l swaps column l of rows j and p
-            if (l < k) { const double t = A[j * LD + l]; A[j * LD + l] = A[p * LD + l]; A[p * LD + l] = t; }
-            if (l < nrhs) { const double t = B[j * LD + l]; B[j * LD + l] = B[p * LD + l]; B[p * LD + l] = t; }
+        if (p != j) {   // lane l swaps its columns' entries of rows j and p
+            if (ha) { const double t = A[j * LD + l]; A[j * LD + l] = A[p * LD + l]; A[p * LD + l] = t; }
+            if (hb) { const double t = B[j * LD + l]; B[j * LD + l] = B[p * LD + l]; B[p * LD + l] = t; }
         }
         __syncwarp();
-        if (l > j && l < k) {
-            const double f = A[l * LD + j] / A[j * LD + j];
+        const double inv = 1.0 / A[j * LD + j];
+        const double aj = (ha && l > j) ? A[j * LD + l] : 0.0, bj = hb ? B[j * LD + l] : 0.0;
 #pragma unroll 4
-            for (int c = j + 1; c < k; ++c) A[l * LD + c] = fma(-f, A[j * LD + c], A[l * LD + c]);
-#pragma unroll 4
-            for (int c = 0; c < nrhs; ++c) B[l * LD + c] = fma(-f, B[j * LD + c], B[l * LD + c]);
-            A[l * LD + j] = f;   // L multiplier (getrf layout)
+        for (int r = j + 1; r < k; ++r) {
+            const double f = A[r * LD + j] * inv;   // multiplier of row r (broadcast)
+            if (ha && l > j) A[r * LD + l] = fma(-f, aj, A[r * LD + l]);
+            if (hb) B[r * LD + l] = fma(-f, bj, B[r * LD + l]);
         }
+        __syncwarp();
+        if (l > j && l < k) A[l * LD + j] *= inv;   // L multiplier (getrf layout), lane = row
         __syncwarp();
     }
     // back substitution, lane = right-hand-side column (solution overwrites B)

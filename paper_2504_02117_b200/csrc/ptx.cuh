@@ -93,4 +93,19 @@ __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b)
                  : "d"(a), "d"(b));
 }
 
+
+// shared-memory loads by 32-bit shared address ("memory": not moved across the mbarrier waits)
+__device__ __forceinline__ double2 lds_d2(uint32_t a) {
+    double2 v;
+    asm("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(a) : "memory");
+    return v;
+}
+__device__ __forceinline__ double lds_d(uint32_t a) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+
+
+
 }  // namespace bk

@@ -411,7 +411,9 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     // epilogue) ; P = R + P be.  13 N x k passes per iteration instead of 14, 4 launches instead of 9.
     const bool fused = !jac && fused_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
                        ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
-    const bool epi = fused && !S.allred;
+    // (BK_EPI=0: separate one-warp kernels instead of the epilogues -- A/B timing)
+    static const int epi_env = env_int("BK_EPI", 1);
+    const bool epi = fused && !S.allred && epi_env != 0;
     SmallEpi e_al, e_be;
     e_al.kind = 4; e_al.k = k; e_al.st = S.ds; e_al.G = PQ; e_al.Rhs = RZ; e_al.Out = al; e_al.tol = tol;
     e_be.kind = 5; e_be.k = k; e_be.st = S.ds; e_be.g = RZn; e_be.Rhs = RZ; e_be.Out = be; e_be.tol = tol;
@@ -513,7 +515,9 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
                        ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
     // one rank: the k x k steps run in the epilogue of the pass that produces their
     // input (no separate small-kernel launches); p > 1: after the allreduce
-    const bool epi = fused && !S.allred;
+    // (BK_EPI=0: separate one-warp kernels instead of the epilogues -- A/B timing)
+    static const int epi_env = env_int("BK_EPI", 1);
+    const bool epi = fused && !S.allred && epi_env != 0;
     SmallEpi e_al, e_be, e_cv;
     e_al.kind = 1; e_al.k = k; e_al.st = S.ds; e_al.G = M1; e_al.Rhs = RR; e_al.Out = al; e_al.sign = 1.0;
     e_al.tol = tol; e_al.LU = LUf; e_al.piv = piv;

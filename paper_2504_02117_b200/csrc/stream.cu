@@ -778,38 +778,64 @@ __global__ void __launch_bounds__(NC + 32, 2) gram_panel_stream_kernel(const Gra
         for (int p = 0; p < NXP; ++p) { xb[p] = base[Gs.xps[p]] + Gs.xpo[p] + 2 * mg; xw[p] = Gs.S.w[Gs.xps[p]]; }
 #pragma unroll
         for (int p = 0; p < NYP; ++p) { yb[p] = base[Gs.yps[p]] + Gs.ypo[p] + 2 * mg; yw[p] = Gs.S.w[Gs.yps[p]]; }
-        for (int q0 = 4 * warp; q0 < nr; q0 += 4 * (NC / 32) * NSET) {
-            double2 a[NSET][NXP], b[NSET][NYP];
+        // the row loop with the operand loads as a parameter: shared-memory loads (LDS.128)
+        // for staged tiles, global loads for the ragged / unaligned ones (generic loads of
+        // staged data went through the long-scoreboard path)
+        auto rows = [&](auto lda, auto ldb) {
+            for (int q0 = 4 * warp; q0 < nr; q0 += 4 * (NC / 32) * NSET) {
+                double2 a[NSET][NXP], b[NSET][NYP];
 #pragma unroll
-            for (int t = 0; t < NSET; ++t) {
-                const int r = q0 + 4 * (NC / 32) * t + kq;
-                const bool rin = r < nr;
+                for (int t = 0; t < NSET; ++t) {
+                    const int r = q0 + 4 * (NC / 32) * t + kq;
+                    const bool rin = r < nr;
 #pragma unroll
-                for (int p = 0; p < NXP; ++p)
-                    a[t][p] = rin ? *reinterpret_cast<const double2*>(xb[p] + (int64_t)r * xw[p]) : make_double2(0.0, 0.0);
+                    for (int p = 0; p < NXP; ++p) a[t][p] = rin ? lda(p, r) : make_double2(0.0, 0.0);
 #pragma unroll
-                for (int p = 0; p < NYP; ++p)
-                    b[t][p] = rin ? *reinterpret_cast<const double2*>(yb[p] + (int64_t)r * yw[p]) : make_double2(0.0, 0.0);
+                    for (int p = 0; p < NYP; ++p) b[t][p] = rin ? ldb(p, r) : make_double2(0.0, 0.0);
+                }
+#pragma unroll
+                for (int t = 0; t < NSET; ++t)
+#pragma unroll
+                    for (int p = 0; p < NXP; ++p)
+#pragma unroll
+                        for (int q = 0; q < NYP; ++q) {
+                            dmma(acc[t][2 * p][2 * q][0], acc[t][2 * p][2 * q][1], a[t][p].x, b[t][q].x);
+                            dmma(acc[t][2 * p][2 * q + 1][0], acc[t][2 * p][2 * q + 1][1], a[t][p].x, b[t][q].y);
+                            dmma(acc[t][2 * p + 1][2 * q][0], acc[t][2 * p + 1][2 * q][1], a[t][p].y, b[t][q].x);
+                            dmma(acc[t][2 * p + 1][2 * q + 1][0], acc[t][2 * p + 1][2 * q + 1][1], a[t][p].y,
+                                 b[t][q].y);
+                        }
             }
+        };
+        const bool dir = s_direct[s] != 0;
+        if (!dir) {
+            uint32_t xa[NXP], ya[NYP];
 #pragma unroll
-            for (int t = 0; t < NSET; ++t)
+            for (int p = 0; p < NXP; ++p) xa[p] = smem_u32(xb[p]);
 #pragma unroll
-                for (int p = 0; p < NXP; ++p)
-#pragma unroll
-                    for (int q = 0; q < NYP; ++q) {
-                        dmma(acc[t][2 * p][2 * q][0], acc[t][2 * p][2 * q][1], a[t][p].x, b[t][q].x);
-                        dmma(acc[t][2 * p][2 * q + 1][0], acc[t][2 * p][2 * q + 1][1], a[t][p].x, b[t][q].y);
-                        dmma(acc[t][2 * p + 1][2 * q][0], acc[t][2 * p + 1][2 * q][1], a[t][p].y, b[t][q].x);
-                        dmma(acc[t][2 * p + 1][2 * q + 1][0], acc[t][2 * p + 1][2 * q + 1][1], a[t][p].y, b[t][q].y);
-                    }
+            for (int p = 0; p < NYP; ++p) ya[p] = smem_u32(yb[p]);
+            rows([&](int p, int r) { return lds_d2(xa[p] + (uint32_t)(r * xw[p]) * 8u); },
+                 [&](int p, int r) { return lds_d2(ya[p] + (uint32_t)(r * yw[p]) * 8u); });
+        } else {
+            rows([&](int p, int r) { return __ldg(reinterpret_cast<const double2*>(xb[p] + (int64_t)r * xw[p])); },
+                 [&](int p, int r) { return __ldg(reinterpret_cast<const double2*>(yb[p] + (int64_t)r * yw[p])); });
         }
         if (Gs.ndot > 0) {
             const int ne = nr * kw;
             const double *a0 = base[Gs.da[0]], *b0 = base[Gs.db[0]];
             const double *a1 = Gs.ndot > 1 ? base[Gs.da[1]] : a0, *b1 = Gs.ndot > 1 ? base[Gs.db[1]] : b0;
-            for (int e = threadIdx.x; e < ne; e += NC) {
-                dd[0] = fma(a0[e], b0[e], dd[0]);
-                dd[1] = fma(a1[e], b1[e], dd[1]);
+            if (!dir) {
+                const uint32_t sa0 = smem_u32(a0), sb0 = smem_u32(b0), sa1 = smem_u32(a1), sb1 = smem_u32(b1);
+                for (int e = threadIdx.x; e < ne; e += NC) {
+                    const uint32_t o = (uint32_t)e * 8u;
+                    dd[0] = fma(lds_d(sa0 + o), lds_d(sb0 + o), dd[0]);
+                    dd[1] = fma(lds_d(sa1 + o), lds_d(sb1 + o), dd[1]);
+                }
+            } else {
+                for (int e = threadIdx.x; e < ne; e += NC) {
+                    dd[0] = fma(a0[e], b0[e], dd[0]);
+                    dd[1] = fma(a1[e], b1[e], dd[1]);
+                }
             }
         }
         __syncwarp();

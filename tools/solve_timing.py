@@ -23,7 +23,10 @@ ap.add_argument("--iters", default="5,10,20")
 ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--check-every", type=int, default=0, help="0: = iteration count (one poll)")
 ap.add_argument("--restart", type=int, default=30)
+ap.add_argument("--side-stream", action="store_true", help="run on a non-default torch stream")
 a = ap.parse_args()
+if a.side_stream:
+    torch.cuda.set_stream(torch.cuda.Stream())
 ctx = bk.Context(0)
 A = synth.make_matrix(a.cfg, device="cuda")
 M = bk.Matrix.from_csr(ctx, A)
