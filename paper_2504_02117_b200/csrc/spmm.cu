@@ -250,6 +250,66 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs& a, const int* col, con
 
 // ------------------------------------------------------------------ persistent TMA pipeline
 // NC consumer threads, NS ring stages, MINB CTAs per SM (variants: DESIGN.md §4.1)
+// Coupled apply on the FP64 tensor cores for the gather (pipe) kernel: each warp's rows of a
+// pass (32 / LANES of them) go to a per-warp scratch (TS doubles per row), then
+// Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA with C as B fragments
+// ([ks][nb][lane] in shared memory); blocks of 8 rows, rows beyond the warp's share are zero.
+template <int KP, int VEC, int NC, int TR>
+__device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col, const double* val, const int* s_rp,
+                                              int nr, int64_t r0, int grp, int c0, bool lane_in,
+                                              const double* s_Cf, double* w_scr) {
+    constexpr int LANES = KP / VEC;
+    constexpr int RPP = NC / LANES;
+    constexpr int PASSES = (TR + RPP - 1) / RPP;
+    constexpr int WR = 32 / LANES;                  // rows per warp per pass
+    constexpr int NB8 = (WR + 7) / 8;               // 8-row DMMA blocks per pass
+    constexpr int NQ = KP / 4, NKO = KP / 8, TS = KP + 2;
+    const int lane32 = threadIdx.x & 31, mg = lane32 >> 2, kq = lane32 & 3;
+    const int lrow = lane32 / LANES;                // row of this lane inside the warp's share
+    const int wrow0 = grp - lrow;                   // first group index of the warp
+#pragma unroll 1
+    for (int pass = 0; pass < PASSES; ++pass) {
+        const int r = pass * RPP + grp;
+        const bool active = r < nr;
+        double acc[VEC];
+#pragma unroll
+        for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
+        if (active) row_accumulate<VEC, false>(a, col, val, s_rp[r], s_rp[r + 1], c0, lane_in, acc);
+        double* tp = w_scr + lrow * TS + c0;
+        const bool keep = active && lane_in;
+        reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
+        reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+        __syncwarp();
+#pragma unroll
+        for (int b = 0; b < NB8; ++b) {
+            const int lr = 8 * b + mg;                  // scratch row of the fragment
+            const bool rv = lr < WR;
+            double af[NQ];
+#pragma unroll
+            for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
+            const int row = pass * RPP + wrow0 + lr;
+#pragma unroll
+            for (int nb = 0; nb < NKO; ++nb) {
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                const int c = 8 * nb + 2 * kq;
+                if (rv && row < nr && c < a.kout) {
+                    double* yp = a.Y + (r0 + row) * a.ldy + c;
+                    double v0 = a.alpha * d0, v1 = a.alpha * d1;
+                    if (a.beta != 0.0) {
+                        v0 = fma(a.beta, yp[0], v0);
+                        if (c + 1 < a.kout) v1 = fma(a.beta, yp[1], v1);
+                    }
+                    if (c + 1 < a.kout) __stcs(reinterpret_cast<double2*>(yp), make_double2(v0, v1));
+                    else __stcs(yp, v0);
+                }
+            }
+        }
+        __syncwarp();                                   // scratch reused by the next pass
+    }
+}
+
 template <int NC, int NS, int MINB, int TR_, int CAP_>
 struct PipeCfg {
     static constexpr int TR = TR_, CAP = CAP_;
@@ -262,7 +322,8 @@ struct PipeCfg {
     static constexpr int STAGE_BYTES = RP_BYTES + COL_BYTES + VAL_BYTES;
     // ring + barriers/meta + (C and one scratch line per row group when coupled)
     static constexpr int bytes(int kp, int rpp, bool has_c) {
-        return NS * STAGE_BYTES + 64 * 8 + (has_c ? (kp * kp + rpp * (kp + 1)) * 8 : 0);
+        // (TCE: C fragments = kp*kp doubles, per-warp scratch (32/lanes rows of kp+2) <= rpp*(kp+2))
+        return NS * STAGE_BYTES + 64 * 8 + (has_c ? (kp * kp + rpp * (kp + 2)) * 8 : 0);
     }
 };
 
@@ -301,7 +362,17 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
-    if (tid < NC) load_C<KP, HAS_C>(a, s_C, tid, NC);
+    constexpr bool TCE = HAS_C && KP >= 8 && VEC == 4;
+    if constexpr (TCE) {   // C as m8n8k4 B fragments [ks][nb][lane]
+        constexpr int NQ = KP / 4, NKO = KP / 8;
+        for (int i = tid; i < NQ * NKO * 32; i += NC + 32) {
+            const int l = i & 31, ks = (i >> 5) / NKO, nb = (i >> 5) % NKO;
+            const int r = 4 * ks + (l & 3), c = 8 * nb + (l >> 2);
+            s_C[i] = (r < a.k && c < a.kout) ? a.C[r * a.kout + c] : 0.0;
+        }
+    } else {
+        if (tid < NC) load_C<KP, HAS_C>(a, s_C, tid, NC);
+    }
     __syncthreads();
 
     if (warp == NC / 32) {
@@ -349,7 +420,16 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
         const int p0 = s_rp[0];
         const int off = p0 & 3;
         const bool staged = s_staged[s] != 0;
-        if (staged) {
+        if constexpr (TCE) {
+            double* w_scr = s_t + warp * (32 / LANES) * (KP + 2);
+            if (staged) {
+                const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
+                const double* sval = reinterpret_cast<const double*>(st + L::RP_BYTES + L::COL_BYTES) + off - p0;
+                tile_rows_tce<KP, VEC, NC, TR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, w_scr);
+            } else {
+                tile_rows_tce<KP, VEC, NC, TR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, w_scr);
+            }
+        } else if (staged) {
             const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
             const double* sval = reinterpret_cast<const double*>(st + L::RP_BYTES + L::COL_BYTES) + off - p0;
             tile_rows<KP, VEC, HAS_C, NC, TR, PAIR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, t_row);
@@ -1380,8 +1460,12 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     // The same holds for k > 16 on 2-D lattices once the gathers are 256-bit loads (c2 k = 32:
     // 0.65 vs 0.63, k = 24: 0.54 vs 0.49; the band kernel is shared-memory bound there,
     // L1TEX 83 %).
+    static const int wc = env_int("BK_WIN_COUPLED", 1);
+    if (a.C != nullptr && !wc) return false;
     static const int w3 = env_int("BK_WIN_3D", -1);
-    if (w3 < 0 && a.C == nullptr && (p.nbands >= 5 || a.k > 16)) return false;
+    // Coupled applies (DMMA epilogue in both kernels): the band kernel for k <= 16 (c2 k = 16:
+    // 0.56 vs 0.52), the gather kernel above (k = 32: 0.38 vs 0.35).
+    if (w3 < 0 && (a.C == nullptr ? (p.nbands >= 5 || a.k > 16) : a.k > 16)) return false;
     if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
     // the window copies contiguous X rows: packed X (ldx == k), 16-byte aligned
     if (a.ldx != a.k || ((uintptr_t)a.X % 16) != 0) return false;
