@@ -605,3 +605,47 @@ def test_graph_replay_is_bitwise_identical(ctx, bk, method, cfg, k):
         assert st1 == st0 == 0 and r1["iterations"] == r0["iterations"]
         assert torch.equal(X1, X0)
         assert np.array_equal(r1["true_relres"], r0["true_relres"])
+
+
+def test_chebyshev_pcg_graph_replay_bitwise(ctx, bk):
+    A = synth.laplace_mms2d(40)
+    B = cu(synth.multivector(A.n_rows, 8, 2))
+    M = bk.Matrix.from_csr(ctx, A)
+    X0 = torch.zeros(A.n_rows, 8, dtype=torch.float64, device="cuda")
+    st0, r0 = bk.block_krylov_solve(ctx, M, B, X0, method="cg", rtol=1e-10, x0_is_zero=True,
+                                    precond="chebyshev", cheb_steps=4)
+    X1 = torch.zeros_like(X0)
+    st1, r1 = bk.block_krylov_solve(ctx, M, B, X1, method="cg", rtol=1e-10, x0_is_zero=True,
+                                    precond="chebyshev", cheb_steps=4, use_graphs=True, check_every=4)
+    assert st0 == st1 == 0 and r0["iterations"] == r1["iterations"] and torch.equal(X0, X1)
+
+
+def test_precond_apply_strided_and_jacobi_none(ctx, bk):
+    A = synth.richards3d(10, 9, 8)
+    k = 4
+    R = synth.multivector(A.n_rows, k, 3)
+    M = bk.Matrix.from_csr(ctx, A)
+    Rw = torch.zeros(A.n_rows, 6, dtype=torch.float64, device="cuda")
+    Rw[:, :k] = cu(R)
+    Zw = torch.full((A.n_rows, 7), float("nan"), dtype=torch.float64, device="cuda")
+    lmin, lmax = oracle.chebyshev_bounds(A)
+    bk.precond_apply(ctx, M, Rw[:, :k], Zw[:, :k], "chebyshev", cheb_steps=3, cheb_lmin=lmin, cheb_lmax=lmax)
+    Zr = oracle.chebyshev_prec(A, R.numpy(), 3, lmin, lmax)
+    check_close(Zw[:, :k].cpu().numpy(), Zr, 3 * np.abs(Zr).max(), what="strided cheb")
+    assert torch.isnan(Zw[:, k:]).all()                              # columns beyond k untouched
+    Zn = torch.empty(A.n_rows, k, dtype=torch.float64, device="cuda")
+    bk.precond_apply(ctx, M, cu(R), Zn, "none")
+    assert torch.equal(Zn.cpu(), R)
+
+
+@pytest.mark.parametrize("k", [8, 16])
+def test_fused_cg_matches_unfused_iterates(ctx, bk, k):
+    """The fused CG passes run the O4 steps in a different summation order:
+    iterates agree with the oracle to 1e-10 after 10 fixed iterations, like the unfused path."""
+    A = synth.make_matrix("c1s")
+    B = synth.multivector(A.n_rows, k, 2)
+    M = bk.Matrix.from_csr(ctx, A)
+    Xs, _ = oracle.block_cg(A, B, rtol=1e-30, max_iters=10)
+    X = torch.zeros(A.n_rows, k, dtype=torch.float64, device="cuda")
+    bk.block_krylov_solve(ctx, M, cu(B), X, method="cg", rtol=1e-30, max_iters=10, x0_is_zero=True)
+    assert np.linalg.norm(X.cpu().numpy() - Xs) / np.linalg.norm(Xs) <= 1e-10
