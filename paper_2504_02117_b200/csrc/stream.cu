@@ -94,6 +94,7 @@ struct UpdStream {
     const double* w_dev;
     const double* C;    // kp x k
     double* out;
+    int64_t ldo;        // output leading dimension (>= k; inputs are contiguous)
     const int* halt;
 };
 
@@ -121,7 +122,7 @@ __device__ __forceinline__ void upd_tile(const UpdStream& U, const double* Pt, c
             if (Wt) v = fma(wv, Wt[(int64_t)r * k + cb + j], v);
             o[j] = v;
         }
-        double* op = U.out + (r0 + r) * k + cb;
+        double* op = U.out + (r0 + r) * U.ldo + cb;
         if (CW == 4) {
             reinterpret_cast<double2*>(op)[0] = make_double2(o[0], o[1]);
             reinterpret_cast<double2*>(op)[1] = make_double2(o[2], o[3]);
@@ -165,7 +166,7 @@ __device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* P
             // D(row = mg, cols 2kq, 2kq+1): the accumulator layout of m8n8k4
 #pragma unroll
             for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], bf[ks][nb]);
-            if (rin) *reinterpret_cast<double2*>(U.out + (r0 + r) * k + c) = make_double2(d0, d1);
+            if (rin) *reinterpret_cast<double2*>(U.out + (r0 + r) * U.ldo + c) = make_double2(d0, d1);
         }
     }
 }
@@ -1140,7 +1141,9 @@ size_t stream_part_doubles(int num_sms) { return (size_t)(2 * num_sms + 40) * 20
 
 bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
     // contiguous operands only, kp and k <= 32, out not aliasing P/Xin/W rows in other tiles is fine
-    if (u.kp < 0 || u.kp > 32 || u.k > 32 || (u.kp > 0 && u.ldp != u.kp) || u.ldo != u.k) return false;
+    // (a strided output -- e.g. a GMRES basis block -- is written row by row from registers)
+    if (u.kp < 0 || u.kp > 32 || u.k > 32 || (u.kp > 0 && u.ldp != u.kp) || u.ldo < u.k) return false;
+    if (u.ldo != u.k && ((u.ldo & 1) || u.k % 2)) return false;
     if (u.kp > 0 && (const double*)u.out == u.P) return false;   // in-place X <- X C: blas.cu reads rows first
     if (u.a != 0.0 && (u.ldxin != u.k || !u.Xin)) return false;
     if (u.W && u.ldw != u.k) return false;
@@ -1166,7 +1169,7 @@ bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
     U.S.ntiles = (int)((u.n + U.S.T - 1) / U.S.T);
     U.kp = u.kp; U.k = u.k; U.cw = cw;
     U.a = u.a; U.s = u.s; U.w_host = u.w_host; U.w_dev = u.w_dev;
-    U.C = u.C; U.out = u.out; U.halt = u.halt;
+    U.C = u.C; U.out = u.out; U.ldo = u.ldo; U.halt = u.halt;
     const int smem = NSTAGE * STAGE_BYTES + 128 + 32 * 32 * 8;
     const int grid = grid_for(U.S.ntiles, num_sms);
     if (grid <= 0) return true;

@@ -45,7 +45,8 @@ struct WideArgs {
     int ka, kb;
     bool hasW;
     // gram
-    double* part;    // [gridDim.x][ka * kb]
+    double* part;    // [gridDim.x * rs][ka * kb]
+    int rs;          // row slices: with fewer column blocks than warps, warp = (block, slice)
     // update
     double a, s;
     const double* H; // ka x k row-major
@@ -127,6 +128,10 @@ gram_wide_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant_
     }
     const int kq = lane & 3, mg = lane >> 2;
     const int NA = (w.ka + 7) / 8;
+    // rs > 1 (NAW == 1, NA * rs <= 16): warp owns block warp % NA and rows slice warp / NA
+    const int RS = w.rs;
+    const int wb = RS > 1 ? warp % NA : warp, sl = RS > 1 ? warp / NA : 0;
+    const bool wact = sl < RS;
     double acc[NAW][NBK][2];
 #pragma unroll
     for (int t = 0; t < NAW; ++t)
@@ -137,7 +142,7 @@ gram_wide_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant_
     int voff[NAW];
 #pragma unroll
     for (int t = 0; t < NAW; ++t) {
-        const int c = 8 * (warp + WNW * t) + mg;
+        const int c = 8 * (wb + WNW * t) + mg;
         voff[t] = c < w.ka ? (c / bw) * w.V.ps + (c % bw) : -1;
     }
     int woff[NBK];
@@ -150,14 +155,14 @@ gram_wide_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant_
         const unsigned char* st = smem + s * w.stage_bytes;
         const double* Vs = reinterpret_cast<const double*>(st + w.V.off);
         const double* Ws = reinterpret_cast<const double*>(st + w.W.off);
-        for (int q0 = 0; q0 < w.T; q0 += 4) {
+        for (int q0 = 4 * sl; wact && q0 < w.T; q0 += 4 * RS) {
             const int r = q0 + kq;
             double b[NBK];
 #pragma unroll
             for (int j = 0; j < NBK; ++j) b[j] = woff[j] >= 0 ? Ws[r * wpW + woff[j]] : 0.0;
 #pragma unroll
             for (int t = 0; t < NAW; ++t) {
-                if (warp + WNW * t < NA) {   // warp-uniform
+                if (wb + WNW * t < NA) {   // warp-uniform
                     const double av = voff[t] >= 0 ? Vs[voff[t] + r * bw] : 0.0;
 #pragma unroll
                     for (int j = 0; j < NBK; ++j) dmma(acc[t][j][0], acc[t][j][1], av, b[j]);
@@ -167,11 +172,12 @@ gram_wide_kernel(const __grid_constant__ CUtensorMap tmV, const __grid_constant_
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
-    // this CTA's partial: block (blk, j): rows 8 blk + mg, cols 8 j + 2 kq (+1)
-    double* P = w.part + (int64_t)blockIdx.x * w.ka * w.kb;
+    // this CTA's (row slice's) partial: block (blk, j): rows 8 blk + mg, cols 8 j + 2 kq (+1)
+    if (!wact) return;
+    double* P = w.part + ((int64_t)blockIdx.x * RS + sl) * w.ka * w.kb;
 #pragma unroll
     for (int t = 0; t < NAW; ++t) {
-        const int blk = warp + WNW * t;
+        const int blk = wb + WNW * t;
         if (blk >= NA) continue;
         const int a = 8 * blk + mg;
 #pragma unroll
@@ -201,7 +207,7 @@ __global__ void wide_reduce_kernel(const double* __restrict__ part, int nblk, in
 }
 
 // ------------------------------------------------------------------ wide update: out = a W + s V H
-// T = 8 rb rows per tile (rb = 4, 2, 1 row blocks); warp = (row block warp % rb, K slice warp / rb of 16 / rb);
+// T = 8 rb rows per tile (rb = 16, 8, 4 row blocks); warp = (row block warp % rb, K slice warp / rb of 16 / rb);
 // NK = ceil(k / 8) output column blocks.  H (ka x k) B fragments read through L1 (__ldg).
 template <int NK>
 __global__ void __launch_bounds__(WNC + 32, 1)
@@ -358,7 +364,13 @@ bool wide_enabled() {
     return v != 0;
 }
 
-size_t gram_wide_ws_doubles(int ka, int kb, int num_sms) { return (size_t)num_sms * ka * kb + 64; }
+static int wide_row_slices(int ka) {
+    const int NA = (ka + 7) / 8;
+    return NA < WNW ? WNW / NA : 1;
+}
+size_t gram_wide_ws_doubles(int ka, int kb, int num_sms) {
+    return (size_t)num_sms * wide_row_slices(ka) * ka * kb + 64;
+}
 
 // G (ka x kb) = V^T W, V: n x ka (ldv), W: n x kb (ldw); false = not applicable
 bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, const double* W, int64_t ldw,
@@ -384,6 +396,7 @@ bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, c
     const int NA = (ka + 7) / 8, NBK = (kb + 7) / 8;
     const int naw = (NA + WNW - 1) / WNW;
     const int grid = w.ntiles < num_sms ? w.ntiles : num_sms;
+    w.rs = wide_row_slices(ka);   // idle warps take row slices of the tile
     bool ok = false;
 #define BK_GW(A, B)                                                                           \
     if (!ok && naw <= A && NBK == B) {                                                        \
@@ -398,7 +411,7 @@ bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, c
     if (!ok) return false;
     const int nout = ka * kb;
     BK_KERNEL(wide_reduce_kernel<<<(nout + 255) / 256 < 2 * num_sms ? (nout + 255) / 256 : 2 * num_sms, 256, 0, st>>>(
-        part, grid, nout, G));
+        part, grid * w.rs, nout, G));
     return true;
 }
 
@@ -424,11 +437,13 @@ bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
     const int NK = (u.k + 7) / 8;
     const int red_bytes = 128 * 8 * NK * 8;
     const int64_t hf_bytes = (int64_t)((u.kp + 3) / 4) * NK * 32 * 8;
-    // 32-row tiles with >= 2 stages (measured: 16 / 8-row tiles lose to the generic kernel,
-    // the per-tile barriers dominate); H fragments in shared memory if they fit
+    // the largest tile (128, 64 or 32 rows) with >= 2 stages: a tile costs two CTA barriers and
+    // a single producer thread ~1 us per tile, so small tiles are latency-bound (c3 k = 12:
+    // 32-row tiles 1.7 TB/s; measured: 16 / 8-row tiles lose to the generic kernel); H
+    // fragments in shared memory if they fit
     int smem = 0;
     bool ok = false;
-    for (int rb = 4; rb >= 4 && !ok; rb /= 2) {
+    for (int rb = 16; rb >= 4 && !ok; rb /= 2) {
         if (!geometry(w, u.n, 8 * rb, &tmV, &tmW)) return false;
         w.rb = rb;
         for (int hf = 1; hf >= 0 && !ok; --hf) {
