@@ -601,7 +601,27 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
     double* y = S.small((size_t)m * k * k);
     double* sm = S.small(8 * 32 * 32);
     double *G1 = sm, *R1 = sm + 1024, *R1i = sm + 2048, *R2i = sm + 3072, *Sr = sm + 4096, *nr = sm + 5120;
+    // CholQR2 (O5): Q1 = W R1^-1 with R1^T R1 = W^T W; R2^T R2 = Q1^T Q1; V = Q1 R2^-1, R = R2 R1.
+    // Q1 goes to a contiguous scratch (streaming Gram, no strided read-back) and the basis
+    // block is written once from W with the product R1^-1 R2^-1 (no in-place strided pass).
+    double* Q1 = S.vec();
+    double* R12i = S.small(32 * 32);
     const double tol = S.o->breakdown_tol;
+    auto cholqr2 = [&](const double* Wm, double* Vout, double* Rprod) -> int {
+        TRY(S.gram(Wm, k, k, Wm, k, G1));
+        sd_chol_qr(G1, R1, R1i, nullptr, nullptr, k, tol, S.ds, S.st);
+        TRY(S.upd(Q1, k, 0.0, nullptr, 0, 1.0, Wm, k, k, R1i));
+        TRY(S.gram(Q1, k, k, Q1, k, G1));
+        sd_chol_qr(G1, nullptr, R2i, R1, Rprod, k, tol, S.ds, S.st);
+        {   // R12i = R1^-1 R2^-1 (k x k, an update over k rows)
+            UpdArgs u{};
+            u.n = k; u.kp = k; u.k = k; u.a = 0.0; u.s = 1.0; u.P = R1i; u.ldp = k; u.C = R2i;
+            u.out = R12i; u.ldo = k; u.halt = &S.ds->halt;
+            launch_update(u, S.st);
+            TRY(S.launched("cholqr2 R12i"));
+        }
+        return S.upd(Vout, ldv, 0.0, nullptr, 0, 1.0, Wm, k, k, R12i);
+    };
     TRY(S.residual(B, ldb, X, ldx, W, S.o->x0_is_zero));
     TRY(S.coldot(W, k, W, k, nullptr, 0, nr, nullptr));
     sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
@@ -612,12 +632,7 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
         cudaMemsetAsync(g, 0, hk * sizeof(double), S.st);
         cudaMemsetAsync(Rtri, 0, (size_t)ldr * ldr * sizeof(double), S.st);
         // [V_0, S] = CholQR2(R)
-        TRY(S.gram(W, k, k, W, k, G1));
-        sd_chol_qr(G1, R1, R1i, nullptr, nullptr, k, tol, S.ds, S.st);
-        TRY(S.upd(Vb, ldv, 0.0, nullptr, 0, 1.0, W, k, k, R1i));
-        TRY(S.gram(Vb, ldv, k, Vb, ldv, G1));
-        sd_chol_qr(G1, nullptr, R2i, R1, Sr, k, tol, S.ds, S.st);
-        TRY(S.upd(Vb, ldv, 0.0, nullptr, 0, 1.0, Vb, ldv, k, R2i));
+        TRY(cholqr2(W, Vb, Sr));
         sd_copy(Sr, g, k * k, S.st);
         int j = 0;
         for (; j < m; ++j) {
@@ -632,12 +647,7 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
             TRY(S.upd(W, k, 1.0, W, k, -1.0, Vb, ldv, ka, H2));
             sd_add(H1, H2, Hcol, ka * k, S.st);
             // [V_{j+1}, H_{j+1,j}] = CholQR2(W)
-            TRY(S.gram(W, k, k, W, k, G1));
-            sd_chol_qr(G1, R1, R1i, nullptr, nullptr, k, tol, S.ds, S.st);
-            TRY(S.upd(Vn, ldv, 0.0, nullptr, 0, 1.0, W, k, k, R1i));
-            TRY(S.gram(Vn, ldv, k, Vn, ldv, G1));
-            sd_chol_qr(G1, nullptr, R2i, R1, Hcol + (int64_t)ka * k, k, tol, S.ds, S.st);
-            TRY(S.upd(Vn, ldv, 0.0, nullptr, 0, 1.0, Vn, ldv, k, R2i));
+            TRY(cholqr2(W, Vn, Hcol + (int64_t)ka * k));
             sd_gmres_step(Hcol, j, k, Qs, Rtri, ldr, g, S.o->rtol, S.o->conv_mode, S.ds, S.st);
             S.rep->n_small += 5;
             ++it;

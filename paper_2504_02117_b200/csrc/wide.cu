@@ -417,7 +417,7 @@ bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, c
 
 // out = a Xin + s V H (Xin, out: n x k, ld k; V: n x ka, ldv; H: ka x k device); false = not applicable
 bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
-    if (!wide_enabled() || u.n <= 0 || u.kp < 16 || u.kp > 2048 || u.k < 1 || u.k > 32 || u.W) return false;
+    if (!wide_enabled() || u.n <= 0 || u.kp < 4 || u.kp > 2048 || u.k < 1 || u.k > 32 || u.W) return false;
     if (!u.P || !u.C || u.ldo < u.k) return false;
     if ((const double*)u.out == u.P) return false;
     if (u.a != 0.0 && !u.Xin) return false;
