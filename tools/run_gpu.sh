@@ -1,4 +1,6 @@
 mkdir -p gpurun_out
-timeout 900 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-timeout 600 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_step.csv python bench.py --profile-step --steps 1 --warmup 3 --no-sweep --no-e2e --no-configs > gpurun_out/ncu_step.log 2>&1
-timeout 300 python tools/alg1_timing.py > gpurun_out/alg1_c3.jsonl 2>&1
+timeout 900 python -m pytest tests -m gpu -x -q -k "gmres or update or solve or dirk or alg1 or wide" > gpurun_out/t_sub.log 2>&1
+timeout 300 python tools/solve_timing.py --cfg c3 --k 12 --method gmres --iters 6,12 --restart 6 > gpurun_out/gm_t.log 2>&1
+timeout 300 python tools/solve_timing.py --cfg c2 --k 16 --method gmres --iters 6,12 --restart 6 > gpurun_out/gm_t2.log 2>&1
+timeout 300 python tools/solve_timing.py --cfg c2 --k 16 --method gmres --iters 20,30 --restart 30 > gpurun_out/gm_t3.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/l_gmres.csv python tools/solve_timing.py --cfg c3 --k 12 --method gmres --iters 3,6 --reps 1 --restart 6 > gpurun_out/gm.log 2>&1
