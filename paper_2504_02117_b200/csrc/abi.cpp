@@ -462,6 +462,26 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
         a.nrows = A->n_local;
         static const int walk = env_int("BK_PIPE_WALK", 0);
         if (walk && A->band.nbands >= 3) a.walk_line = -(int64_t)A->band.dmin[A->band.nbands / 2 - 1];
+        // 3-D lattice whose z-neighbour planes do not stay in L2 across two planes of streaming
+        // (c5: 512 x 512 planes): y-slab tile order, opt-in (BK_SLAB=1; measured c5 k = 16
+        // 0.68 -> 0.70, but k = 32 0.57 -> 0.57 and c4 k = 32 0.64 -> 0.61)
+        static const int slab = env_int("BK_SLAB", 0);
+        const BandPlan& bp = A->band;
+        if (slab && bp.nbands == 5 && bp.dmin[0] == bp.dmax[0] && bp.dmin[1] == bp.dmax[1] && bp.dmin[1] < 0 &&
+            bp.dmin[0] < bp.dmin[1] && a.row0 == bp.row0 && a.nrows == bp.nrows) {
+            const int64_t nx = -(int64_t)bp.dmin[1], plane = -(int64_t)bp.dmin[0];
+            if (plane % nx == 0 && a.nrows % plane == 0) {
+                const int64_t ny = plane / nx, nz = a.nrows / plane;
+                const double row_bytes = 16.0 * k + 88.0;
+                const double budget = 56.0 * 1024 * 1024;   // of the 126 MB L2
+                int S = 1;
+                while (2.0 * (double)(ny / S) * nx * row_bytes > budget && ny % (2 * S) == 0 && ny / (2 * S) >= 8)
+                    S *= 2;
+                if (S > 1 && ny < (1 << 30) && nz < (1 << 30) && nx < (1 << 30)) {
+                    a.sl_S = S; a.sl_tpl = (int)nx; a.sl_ny = (int)ny; a.sl_nz = (int)nz;
+                }
+            }
+        }
         if (!launch_bspmm_win(a, A->band, ctx->stream)) launch_bspmm(a, ctx->stream);
         return post_launch(ctx, "bspmm_apply");
     }

@@ -61,6 +61,10 @@ struct SpmmArgs {
     double* Y;
     int64_t ldy;
     int64_t walk_line;      // pipe kernel: grid line length for the y-walk tile order (0: interleaved)
+    // pipe kernel, 3-D lattices: y-slab tile order (sl_S > 0): slab s of sl_L lines, then z,
+    // then the line, then the x block (sl_tpl tiles per line) -- keeps the z-neighbour planes
+    // of the rows in flight L2-resident when whole planes do not fit
+    int sl_S, sl_L, sl_tpl, sl_ny, sl_nz;
 };
 
 // out = a*Xin + s*(P C) + (w_host * (*w_dev)) * W     (any term may be absent)

@@ -327,6 +327,16 @@ struct PipeCfg {
     }
 };
 
+// processing-order tile t -> tile index (y-slab order, SpmmArgs::sl_*); identity if sl_S == 0
+__device__ __forceinline__ int slab_tile(const SpmmArgs& a, int t) {
+    if (a.sl_S <= 0) return t;
+    const int per_plane = a.sl_L * a.sl_tpl, per_slab = a.sl_nz * per_plane;
+    const int s = t / per_slab, rem = t - s * per_slab;
+    const int z = rem / per_plane, rem2 = rem - z * per_plane;
+    const int yl = rem2 / a.sl_tpl, xb = rem2 - yl * a.sl_tpl;
+    return ((z * a.sl_ny + s * a.sl_L + yl) * a.sl_tpl) + xb;
+}
+
 template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP, bool PAIR>
 __global__ void __launch_bounds__(NC + 32, MINB)
 bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
@@ -384,7 +394,7 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
                 const int s = i % NS;
                 if (i >= NS) mbar_wait(&empty[s], ((i / NS) - 1) & 1);
                 unsigned char* st = smem + s * L::STAGE_BYTES;
-                const int64_t r0 = a.row0 + (int64_t)tile * TR;
+                const int64_t r0 = a.row0 + (int64_t)slab_tile(a, tile) * TR;
                 const int nr = (int)((a.row0 + a.nrows - r0) < TR ? (a.row0 + a.nrows - r0) : TR);
                 const int p0 = a.rp[r0], p1 = a.rp[r0 + nr];
                 const int64_t ra = r0 & ~(int64_t)3;
@@ -413,7 +423,7 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
         const int s = i % NS;
         mbar_wait(&full[s], (i / NS) & 1);
         const unsigned char* st = smem + s * L::STAGE_BYTES;
-        const int64_t r0 = a.row0 + (int64_t)tile * TR;
+        const int64_t r0 = a.row0 + (int64_t)slab_tile(a, tile) * TR;
         const int nr = (int)((a.row0 + a.nrows - r0) < TR ? (a.row0 + a.nrows - r0) : TR);
         const int roff = (int)(r0 & 3);
         const int* s_rp = reinterpret_cast<const int*>(st) + roff;
@@ -456,6 +466,16 @@ void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
     int64_t grid = ntiles < cap ? ntiles : cap;
     static const int chunked = env_int("BK_PIPE_CHUNK", 0) > 0;
     int walk = chunked ? 1 : 0;
+    SpmmArgs b = a;
+    if (b.sl_S > 0) {   // slab order needs whole tiles per line and a permutation of all tiles
+        const int64_t line = (int64_t)b.sl_tpl;   // (host passed the line length here)
+        if (line % TR != 0 || (int64_t)b.sl_ny * b.sl_nz * line != b.nrows || b.sl_ny % b.sl_S != 0) {
+            b.sl_S = 0;
+        } else {
+            b.sl_tpl = (int)(line / TR);
+            b.sl_L = b.sl_ny / b.sl_S;
+        }
+    }
     if (a.walk_line > 0 && a.walk_line % TR == 0) {   // y walk: tiles per line, whole lines only
         const int w = (int)(a.walk_line / TR);
         if (ntiles % w == 0 && cap >= w) {
@@ -465,7 +485,7 @@ void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
         }
     }
     BK_KERNEL(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR><<<(unsigned)grid, NC + 32, smem, st>>>(
-        a, (int)ntiles, walk));
+        b, (int)ntiles, walk));
 }
 
 // ------------------------------------------------------------------ simple tile kernel (A/B variant)

@@ -649,3 +649,29 @@ def test_fused_cg_matches_unfused_iterates(ctx, bk, k):
     X = torch.zeros(A.n_rows, k, dtype=torch.float64, device="cuda")
     bk.block_krylov_solve(ctx, M, cu(B), X, method="cg", rtol=1e-30, max_iters=10, x0_is_zero=True)
     assert np.linalg.norm(X.cpu().numpy() - Xs) / np.linalg.norm(Xs) <= 1e-10
+
+
+def _slab_case(k):
+    import paper_2504_02117_b200 as m
+    ctx = m.Context(0)
+    A = synth.richards3d(256, 256, 3, integer=True)                  # 2 x 256 x 256 x (16k + 88) B > 56 MB at k = 32
+    X = synth.multivector(A.n_rows, k, 3, integer=True)
+    M = m.Matrix.from_csr(ctx, A)
+    Y = torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
+    m.bspmm_apply(ctx, M, cu(X), Y)
+    assert np.array_equal(Y.cpu().numpy(), oracle.spmm(A, X))
+
+
+@pytest.mark.parametrize("k", [16, 32])
+def test_spmm_slab_order_bitwise(k):
+    """Large 3-D planes with the opt-in y-slab tile order of the gather kernel (BK_SLAB=1,
+    DESIGN.md §4.1): a permutation of the tiles, so the apply stays bitwise equal to the oracle
+    on integer data (run in a subprocess: the knob is read once per process)."""
+    import subprocess
+    import sys
+    code = f"import sys; sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.join(ROOT, 'tests')!r}); " \
+           f"import test_gpu_parity as t; t._slab_case({k})"
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BK_SLAB="1"), capture_output=True,
+                       text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    _slab_case(k)                                                      # and the default order
