@@ -607,9 +607,17 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
     double* Q1 = S.vec();
     double* R12i = S.small(32 * 32);
     const double tol = S.o->breakdown_tol;
+    // (small systems are launch-bound: there the two-pass in-place form with one launch fewer)
+    const bool small_n = S.n < 65536;
     auto cholqr2 = [&](const double* Wm, double* Vout, double* Rprod) -> int {
         TRY(S.gram(Wm, k, k, Wm, k, G1));
         sd_chol_qr(G1, R1, R1i, nullptr, nullptr, k, tol, S.ds, S.st);
+        if (small_n) {
+            TRY(S.upd(Vout, ldv, 0.0, nullptr, 0, 1.0, Wm, k, k, R1i));
+            TRY(S.gram(Vout, ldv, k, Vout, ldv, G1));
+            sd_chol_qr(G1, nullptr, R2i, R1, Rprod, k, tol, S.ds, S.st);
+            return S.upd(Vout, ldv, 0.0, nullptr, 0, 1.0, Vout, ldv, k, R2i);
+        }
         TRY(S.upd(Q1, k, 0.0, nullptr, 0, 1.0, Wm, k, k, R1i));
         TRY(S.gram(Q1, k, k, Q1, k, G1));
         sd_chol_qr(G1, nullptr, R2i, R1, Rprod, k, tol, S.ds, S.st);

@@ -417,7 +417,10 @@ bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, c
 
 // out = a Xin + s V H (Xin, out: n x k, ld k; V: n x ka, ldv; H: ka x k device); false = not applicable
 bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
-    if (!wide_enabled() || u.n <= 0 || u.kp < 4 || u.kp > 2048 || u.k < 1 || u.k > 32 || u.W) return false;
+    // (small systems: launch-bound, the generic kernel has less fixed cost for narrow V)
+    const bool small_n = u.n < 65536;
+    if (!wide_enabled() || u.n <= 0 || u.kp < (small_n ? 16 : 4) || u.kp > 2048 || u.k < 1 || u.k > 32 || u.W)
+        return false;
     if (!u.P || !u.C || u.ldo < u.k) return false;
     if ((const double*)u.out == u.P) return false;
     if (u.a != 0.0 && !u.Xin) return false;
@@ -443,7 +446,7 @@ bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
     // fragments in shared memory if they fit
     int smem = 0;
     bool ok = false;
-    for (int rb = 16; rb >= 4 && !ok; rb /= 2) {
+    for (int rb = small_n ? 4 : 16; rb >= 4 && !ok; rb /= 2) {
         if (!geometry(w, u.n, 8 * rb, &tmV, &tmW)) return false;
         w.rb = rb;
         for (int hf = 1; hf >= 0 && !ok; --hf) {
