@@ -881,47 +881,53 @@ bspmm_win_kernel(const BandArgs w) {
                     band_accumulate<VEC, NB, MR>(s_win, scol, sval, rs, re, thr, fo, kk, c0, sw, acc);
                 }
             }
-            if constexpr (TCE) {   // (A X) row to the tile buffer; padded columns zero
-                double* tp = s_tT + r * TS + c0;
+            if constexpr (TCE) {
+                // this warp's rows of the pass -> its scratch (padded columns zero), then
+                // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA by the warp itself: no
+                // CTA barrier, so other warps keep gathering
+                constexpr int WR = 32 / (KP / VEC), NB8 = (WR + 7) / 8;
+                double* w_scr = s_tT + warp * WR * TS;
+                const int lrow = lane32 / (KP / VEC);
+                double* tp = w_scr + lrow * TS + c0;
                 const bool keep = active && c0 < a.k;
                 reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
                 reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+                __syncwarp();
+                const int mg = lane32 >> 2, kq = lane32 & 3;
+#pragma unroll
+                for (int b = 0; b < NB8; ++b) {
+                    const int lr = 8 * b + mg;
+                    const bool rv = lr < WR;
+                    double af[NQ];
+#pragma unroll
+                    for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
+                    const int row = pass * RPP + warp * WR + lr;
+#pragma unroll
+                    for (int nb = 0; nb < NKO; ++nb) {
+                        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                        for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                        const int c = 8 * nb + 2 * kq;
+                        if (rv && row < nr && c < a.kout) {
+                            double* yp = a.Y + (r0 + row) * a.ldy + c;
+                            double v0 = a.alpha * d0, v1 = a.alpha * d1;
+                            if (a.beta != 0.0) {
+                                v0 = fma(a.beta, yp[0], v0);
+                                if (c + 1 < a.kout) v1 = fma(a.beta, yp[1], v1);
+                            }
+                            if (c + 1 < a.kout) __stcs(reinterpret_cast<double2*>(yp), make_double2(v0, v1));
+                            else __stcs(yp, v0);
+                        }
+                    }
+                }
+                __syncwarp();
             } else {
                 row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
             }
         }
         __syncwarp();
         if (lane32 == 0) mbar_arrive(&empty[s]);   // the stage is no longer read
-        if constexpr (TCE) {
-            // Y(8-row block) = alpha (A X)(block) C + beta Y: DMMA m8n8k4, A = the tile rows,
-            // B = C fragments; fragment D[g][2q..2q+1] -> row rb + g, columns 8 nb + 2q
-            asm volatile("bar.sync 1, %0;" ::"r"(NC));
-            const int mg = lane32 >> 2, kq = lane32 & 3;
-            for (int rb = 8 * warp; rb < nr; rb += 8 * (NC / 32)) {
-                double af[NQ];
-#pragma unroll
-                for (int ks = 0; ks < NQ; ++ks) af[ks] = s_tT[(rb + mg) * TS + 4 * ks + kq];
-                const int row = rb + mg;
-#pragma unroll
-                for (int nb = 0; nb < NKO; ++nb) {
-                    double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-                    for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
-                    const int c = 8 * nb + 2 * kq;
-                    if (row < nr && c < a.kout) {
-                        double* yp = a.Y + (r0 + row) * a.ldy + c;
-                        double v0 = a.alpha * d0, v1 = a.alpha * d1;
-                        if (a.beta != 0.0) {
-                            v0 = fma(a.beta, yp[0], v0);
-                            if (c + 1 < a.kout) v1 = fma(a.beta, yp[1], v1);
-                        }
-                        if (c + 1 < a.kout) __stcs(reinterpret_cast<double2*>(yp), make_double2(v0, v1));
-                        else __stcs(yp, v0);
-                    }
-                }
-            }
-            asm volatile("bar.sync 1, %0;" ::"r"(NC));   // tile buffer reused by the next tile
-        }
+
         if (++s == w.ns) {
             s = 0;
             ph ^= 1u;
@@ -1483,9 +1489,9 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     static const int wc = env_int("BK_WIN_COUPLED", 1);
     if (a.C != nullptr && !wc) return false;
     static const int w3 = env_int("BK_WIN_3D", -1);
-    // Coupled applies (DMMA epilogue in both kernels): the band kernel for k <= 16 (c2 k = 16:
-    // 0.56 vs 0.52), the gather kernel above (k = 32: 0.38 vs 0.35).
-    if (w3 < 0 && (a.C == nullptr ? (p.nbands >= 5 || a.k > 16) : a.k > 16)) return false;
+    // Coupled applies (per-warp DMMA epilogue in both kernels) follow the same rule: c2 k = 16
+    // 0.64 band vs 0.52 gather, c4 k = 8 / 16 0.71 / 0.53 gather vs 0.63 / 0.49 band.
+    if (w3 < 0 && (p.nbands >= 5 || a.k > 16)) return false;
     if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
     // the window copies contiguous X rows: packed X (ldx == k), 16-byte aligned
     if (a.ldx != a.k || ((uintptr_t)a.X % 16) != 0) return false;
