@@ -664,14 +664,14 @@ def _slab_case(k):
 
 @pytest.mark.parametrize("k", [16, 32])
 def test_spmm_slab_order_bitwise(k):
-    """Large 3-D planes with the opt-in y-slab tile order of the gather kernel (BK_SLAB=1,
-    DESIGN.md §4.1): a permutation of the tiles, so the apply stays bitwise equal to the oracle
-    on integer data (run in a subprocess: the knob is read once per process)."""
+    """Large 3-D planes with the y-slab tile order of the gather kernel (default for k <= 16,
+    BK_SLAB=2 forces it for every k): a permutation of the tiles, so the apply
+    stays bitwise equal to the oracle on integer data (subprocess: the knob is read once)."""
     import subprocess
     import sys
     code = f"import sys; sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.join(ROOT, 'tests')!r}); " \
            f"import test_gpu_parity as t; t._slab_case({k})"
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BK_SLAB="1"), capture_output=True,
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BK_SLAB="2"), capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
-    _slab_case(k)                                                      # and the default order
+    _slab_case(k)                                                      # and the default choice
