@@ -90,17 +90,25 @@ __device__ __forceinline__ void lu_solve_warp(int defer, const double* __restric
         if (l > j && l < k) A[l * LD + j] *= inv;   // L multiplier (getrf layout), lane = row
         __syncwarp();
     }
-    // back substitution, lane = right-hand-side column (solution overwrites B)
-    if (l < nrhs) {
+    // back substitution, lane = right-hand-side column (solution overwrites B); the 1/U_ii are
+    // formed in parallel (lane i) and broadcast, two partial sums halve the dependent chain
+    const double dinv = l < k ? 1.0 / A[l * LD + l] : 0.0;
 #pragma unroll 1
-        for (int i = k - 1; i >= 0; --i) {
-            double v = B[i * LD + l];
-#pragma unroll 4
-            for (int q = i + 1; q < k; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
-            B[i * LD + l] = v / A[i * LD + i];
+    for (int i = k - 1; i >= 0; --i) {
+        const double di = __shfl_sync(0xffffffffu, dinv, i);
+        if (l < nrhs) {
+            double v0 = B[i * LD + l], v1 = 0.0;
+            int q = i + 1;
+            for (; q + 1 < k; q += 2) {
+                v0 = fma(-A[i * LD + q], B[q * LD + l], v0);
+                v1 = fma(-A[i * LD + q + 1], B[(q + 1) * LD + l], v1);
+            }
+            if (q < k) v0 = fma(-A[i * LD + q], B[q * LD + l], v0);
+            B[i * LD + l] = (v0 + v1) * di;
         }
-        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
     }
+    if (l < nrhs)
+        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
     if (LUo && l < k)
         for (int r = 0; r < k; ++r) LUo[r * k + l] = A[r * LD + l];
     if (pivo && l < k) pivo[l] = s_piv[l];
@@ -126,15 +134,24 @@ __device__ __forceinline__ void lu_resolve_warp(const double* __restrict__ LU, c
             const double bj = B[j * LD + l];
             for (int i = j + 1; i < k; ++i) B[i * LD + l] = fma(-A[i * LD + j], bj, B[i * LD + l]);
         }
-#pragma unroll 1
-        for (int i = k - 1; i >= 0; --i) {
-            double v = B[i * LD + l];
-#pragma unroll 4
-            for (int q = i + 1; q < k; ++q) v = fma(-A[i * LD + q], B[q * LD + l], v);
-            B[i * LD + l] = v / A[i * LD + i];
-        }
-        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
     }
+    const double dinv = l < k ? 1.0 / A[l * LD + l] : 0.0;   // 1/U_ii, broadcast below
+#pragma unroll 1
+    for (int i = k - 1; i >= 0; --i) {
+        const double di = __shfl_sync(0xffffffffu, dinv, i);
+        if (l < nrhs) {
+            double v0 = B[i * LD + l], v1 = 0.0;
+            int q = i + 1;
+            for (; q + 1 < k; q += 2) {
+                v0 = fma(-A[i * LD + q], B[q * LD + l], v0);
+                v1 = fma(-A[i * LD + q + 1], B[(q + 1) * LD + l], v1);
+            }
+            if (q < k) v0 = fma(-A[i * LD + q], B[q * LD + l], v0);
+            B[i * LD + l] = (v0 + v1) * di;
+        }
+    }
+    if (l < nrhs)
+        for (int i = 0; i < k; ++i) Out[i * nrhs + l] = B[i * LD + l];
 }
 
 // Cholesky of A (lower part, lane = row) in place; returns the breakdown column or -1.
