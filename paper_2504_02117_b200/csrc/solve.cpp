@@ -585,10 +585,29 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
 }
 
 // ---------------------------------------------------------------- O5 block GMRES(m)
+// block-major GMRES basis (V_j contiguous n x k blocks): chunk of basis blocks one
+// multi-operand Gram pass can take (the generic kernel's (row, column) block pairs; kw = 16
+// takes the panel kernel), DESIGN.md §4.2
+static int gram_chunk(int kw) {
+    for (int ch = 3; ch >= 1; --ch) {
+        if (kw == 16) return 3;
+        const int na = (ch * kw + 7) / 8, nb = (kw + 7) / 8;
+        const bool ok = nb == 1 ? (na >= 1 && na <= 3) : (na == 2 || na == 3 || na == 4 || na == 6);
+        if (ok) return ch;
+    }
+    return 1;
+}
+
 int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
     const int k = S.k, m = S.o->restart;
-    const int64_t ldv = (int64_t)(m + 1) * k;
-    double* Vb = S.vec((int)ldv);
+    // block-major basis (opt-in, BK_GMRES_BM=1; contiguous n x k blocks: windowed applies,
+    // multi-operand Gram / update passes in chunks of 3 / 4 blocks) or one row-major
+    // n x (m+1)k array (default: the chunked passes re-read W, c3 GMRES(6) 2.11 vs 1.79 ms)
+    static const int bm_env = env_int("BK_GMRES_BM", 0);
+    const bool bm = bm_env && S.n >= 65536 && use_stream_kernels() && k % 2 == 0 && k <= 16;
+    const int64_t ldv = bm ? k : (int64_t)(m + 1) * k;
+    double* Vb = S.vec((int)((m + 1) * k));
+    auto Vblk = [&](int j) { return bm ? Vb + (int64_t)j * S.n * k : Vb + (int64_t)j * k; };
     double* W = S.vec();
     const size_t hk = (size_t)(m + 1) * k * k;
     double* Hcol = S.small(hk);
@@ -609,6 +628,49 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
     const double tol = S.o->breakdown_tol;
     // (small systems are launch-bound: there the two-pass in-place form with one launch fewer)
     const bool small_n = S.n < 65536;
+    // [V_0 .. V_{nb-1}]^T Wm -> Hout (nb k x k), one pass per chunk of basis blocks
+    const int gch = gram_chunk(k);
+    auto gram_basis = [&](int nb, const double* Wm, double* Hout) -> int {
+        if (!bm) return S.gram(Vb, ldv, nb * k, Wm, k, Hout);
+        for (int a0 = 0; a0 < nb; a0 += gch) {
+            const int nc = std::min(gch, nb - a0);
+            const double* arr[4];
+            int xs[3];
+            double* blk[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+            for (int i = 0; i < nc; ++i) {
+                arr[i] = Vblk(a0 + i);
+                xs[i] = i;
+                blk[i][0] = Hout + (int64_t)(a0 + i) * k * k;
+            }
+            arr[nc] = Wm;
+            const int ys[1] = {nc};
+            TRY(S.gram_multi(nc, xs, 1, ys, nc + 1, arr, blk, 0, nullptr, nullptr, nullptr, BK_K_GRAM));
+        }
+        return 0;
+    };
+    // out = a Xin + s [V_0 .. V_{nb-1}] Hc (nb k x k), in passes of <= 4 blocks
+    auto upd_basis = [&](double* out, int64_t ldo, double a, const double* Xin, double s, int nb, const double* Hc,
+                         bool halted) -> int {
+        if (!bm) return S.upd(out, ldo, a, Xin, ldo, s, Vb, ldv, nb * k, Hc, nullptr, 0, 0.0, nullptr, halted);
+        for (int a0 = 0; a0 < nb; a0 += 4) {
+            const int nc = std::min(4, nb - a0);
+            const double* P[4];
+            for (int i = 0; i < nc; ++i) P[i] = Vblk(a0 + i);
+            const double* xin = a0 == 0 ? Xin : out;
+            const double aa = a0 == 0 ? a : 1.0;
+            S.rep->n_update++;
+            S.tb();
+            const bool ok = ldo == k && launch_update_multi(S.n, k, nc, P, Hc + (int64_t)a0 * k * k, aa, xin, s, out,
+                                                            halted ? &S.ds->halt : nullptr, S.ctx->num_sms, S.st);
+            S.te(BK_K_UPDATE);
+            TRY(S.launched("update_multi"));
+            if (!ok)   // one block at a time
+                for (int i = 0; i < nc; ++i)
+                    TRY(S.upd(out, ldo, (a0 + i == 0) ? a : 1.0, (a0 + i == 0) ? Xin : out, ldo, s, Vblk(a0 + i), k, k,
+                              Hc + (int64_t)(a0 + i) * k * k, nullptr, 0, 0.0, nullptr, halted));
+        }
+        return 0;
+    };
     auto cholqr2 = [&](const double* Wm, double* Vout, double* Rprod) -> int {
         TRY(S.gram(Wm, k, k, Wm, k, G1));
         sd_chol_qr(G1, R1, R1i, nullptr, nullptr, k, tol, S.ds, S.st);
@@ -640,19 +702,19 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
         cudaMemsetAsync(g, 0, hk * sizeof(double), S.st);
         cudaMemsetAsync(Rtri, 0, (size_t)ldr * ldr * sizeof(double), S.st);
         // [V_0, S] = CholQR2(R)
-        TRY(cholqr2(W, Vb, Sr));
+        TRY(cholqr2(W, Vblk(0), Sr));
         sd_copy(Sr, g, k * k, S.st);
         int j = 0;
         for (; j < m; ++j) {
-            double* Vj = Vb + (int64_t)j * k;
-            double* Vn = Vb + (int64_t)(j + 1) * k;
+            double* Vj = Vblk(j);
+            double* Vn = Vblk(j + 1);
             const int ka = (j + 1) * k;
             TRY(S.spmm(Vj, ldv, W, k));
             // BCGS2: two passes of Hp = V^T W; W -= V Hp
-            TRY(S.gram(Vb, ldv, ka, W, k, H1));
-            TRY(S.upd(W, k, 1.0, W, k, -1.0, Vb, ldv, ka, H1));
-            TRY(S.gram(Vb, ldv, ka, W, k, H2));
-            TRY(S.upd(W, k, 1.0, W, k, -1.0, Vb, ldv, ka, H2));
+            TRY(gram_basis(j + 1, W, H1));
+            TRY(upd_basis(W, k, 1.0, W, -1.0, j + 1, H1, true));
+            TRY(gram_basis(j + 1, W, H2));
+            TRY(upd_basis(W, k, 1.0, W, -1.0, j + 1, H2, true));
             sd_add(H1, H2, Hcol, ka * k, S.st);
             // [V_{j+1}, H_{j+1,j}] = CholQR2(W)
             TRY(cholqr2(W, Vn, Hcol + (int64_t)ka * k));
@@ -671,7 +733,7 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
         if (S.hs->halt) done = true;
         if (steps > 0) {
             sd_gmres_backsolve(Rtri, ldr, g, y, steps * k, k, S.st);
-            TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, Vb, ldv, steps * k, y, nullptr, 0, 0.0, nullptr, false));
+            TRY(upd_basis(X, ldx, 1.0, X, 1.0, steps, y, false));
         }
         if (!done && it < S.o->max_iters) TRY(S.residual(B, ldb, X, ldx, W, false));
     }

@@ -675,3 +675,40 @@ def test_spmm_slab_order_bitwise(k):
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     _slab_case(k)                                                      # and the default choice
+
+
+def _gm_run(k, its, restart, out):
+    import paper_2504_02117_b200 as m
+    c = m.Context(0)
+    A = synth.convdiff2d(256)                                          # 65 536 rows
+    B = synth.multivector(A.n_rows, k, 2).cuda()
+    M = m.Matrix.from_csr(c, A)
+    X = torch.zeros_like(B)
+    m.block_krylov_solve(c, M, B, X, method="gmres", rtol=1e-30, max_iters=its, restart=restart, x0_is_zero=True)
+    np.save(out, X.cpu().numpy())
+
+
+@pytest.mark.parametrize("k", [4, 8, 12, 16])
+def test_gmres_block_major_basis_matches_oracle(k):
+    """The opt-in block-major GMRES basis (BK_GMRES_BM=1: multi-operand Gram / update passes,
+    DESIGN.md §4.2) on 65 536 rows: 9 fixed iterations (one restart) match the oracle, and 40
+    (two GMRES(20) cycles) match the default strided basis."""
+    import subprocess
+    import sys
+    import tempfile
+    with tempfile.TemporaryDirectory() as td:
+        outs = {}
+        for bm, its, rs in (("1", 9, 6), ("1", 40, 20), ("0", 40, 20)):
+            f = os.path.join(td, f"x_{bm}_{its}.npy")
+            code = (f"import sys; sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.join(ROOT, 'tests')!r}); "
+                    f"import test_gpu_parity as t; t._gm_run({k}, {its}, {rs}, {f!r})")
+            r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BK_GMRES_BM=bm),
+                               capture_output=True, text=True, timeout=600)
+            assert r.returncode == 0, r.stderr[-2000:]
+            outs[(bm, its)] = np.load(f)
+    A = synth.convdiff2d(256)
+    B = synth.multivector(A.n_rows, k, 2)
+    Xs, _ = oracle.block_gmres(A, B, rtol=1e-30, max_iters=9, restart=6)
+    assert np.linalg.norm(outs[("1", 9)] - Xs) / np.linalg.norm(Xs) <= 1e-10
+    Xa, Xb = outs[("1", 40)], outs[("0", 40)]
+    assert np.linalg.norm(Xa - Xb) / np.linalg.norm(Xb) <= 1e-10
