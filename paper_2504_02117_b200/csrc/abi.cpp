@@ -782,8 +782,12 @@ extern "C" int bk_dirk_solve(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, doub
               "bk_dirk_solve: bad inner solver options");
     ARG_CHECK(ctx, inner->method != BK_GMRES || (inner->restart >= 1 && (int64_t)(inner->restart + 1) * k <= BK_MAX_KA),
               "bk_dirk_solve: GMRES needs restart >= 1 and (restart+1)*k <= 4096");
-    ARG_CHECK(ctx, inner->precond == BK_PRECOND_NONE || (inner->precond == BK_PRECOND_JACOBI && inner->method == BK_CG),
-              "bk_dirk_solve: JACOBI preconditioning is implemented for CG only");
+    ARG_CHECK(ctx, inner->precond == BK_PRECOND_NONE ||
+                       ((inner->precond == BK_PRECOND_JACOBI || inner->precond == BK_PRECOND_CHEBYSHEV) &&
+                        inner->method == BK_CG),
+              "bk_dirk_solve: JACOBI / CHEBYSHEV preconditioning is implemented for CG only");
+    ARG_CHECK(ctx, inner->precond != BK_PRECOND_CHEBYSHEV || cheb_opts_ok(L, inner),
+              "bk_dirk_solve: CHEBYSHEV needs cheb_steps >= 1 and 0 < lmin < lmax (after defaults)");
     BK_TRY
     const int64_t n = L->n_local;
     bool bh, b0h;
