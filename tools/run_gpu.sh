@@ -1,3 +1,3 @@
 mkdir -p gpurun_out
-for rep in 1 2; do for s in 0 1; do BK_SLAB=$s timeout 300 python tools/sweep.py --cfg c5 --ks 16 --ops spmm > gpurun_out/c5ab_${s}_$rep.jsonl 2>&1; done; done
-nvidia-smi --query-gpu=clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > gpurun_out/smi.txt
+timeout 900 python tools/dirk_timing.py --n 1024 --s 2,4,8 --method cg --sym --precond chebyshev --inner-rtol 1e-2 --outer-tol 1e-8 > gpurun_out/dirk_t5.jsonl 2>&1
+timeout 900 python tools/dirk_timing.py --n 1024 --s 2,4,8 --method bicgstab --inner-rtol 1e-2 --outer-tol 1e-8 --tau 0.001 > gpurun_out/dirk_t6.jsonl 2>&1
