@@ -254,6 +254,17 @@ int bk_dirk_solve(bk_ctx *ctx, const bk_csr *L, const bk_csr *K, double mass, do
                   const double *A1, const double *A2, const double *B, const double *B0, int64_t ldb,
                   double *Y, int64_t ldy, int max_outer, double outer_tol,
                   const bk_solve_opts *inner, bk_dirk_report *rep);
+/* Same window equation in defect-correction form (the paper's outer / inner tolerance policy
+ * for s > 1, §4.1: a loose inner tolerance, the outer iterations refresh the
+ * right-hand side): per outer iteration F = B A2^T + B0 - M Y (A1 - I/tau)^T ... - L Y is the
+ * defect of the split system, L D = F is solved from D = 0 to inner->rtol (columns scaled to
+ * unit norm; a block breakdown falls back to column-wise solves), Y += D.  Stops when
+ * ||F||_F / ||F_0||_F <= outer_tol (rep->last_change) or after max_outer iterations.
+ * Y holds the initial guess.  Arguments, ownership and errors as bk_dirk_solve.            */
+int bk_dirk_solve_dc(bk_ctx *ctx, const bk_csr *L, const bk_csr *K, double mass, double tau, int k,
+                     const double *A1, const double *A2, const double *B, const double *B0, int64_t ldb,
+                     double *Y, int64_t ldy, int max_outer, double outer_tol,
+                     const bk_solve_opts *inner, bk_dirk_report *rep);
 
 /* NEXT-3: Algorithm 1 "Block Krylov Time Stepping with Pipelining" (§2.2
  * P:600-621; eq. matrix-equation-pipelining; shift P:592-594; iota P:574-580)

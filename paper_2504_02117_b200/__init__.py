@@ -38,7 +38,7 @@ EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last
             "bk_ctx_synchronize", "bk_ctx_destroy", "bk_get_nccl_unique_id", "bk_ctx_set_comm",
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
             "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo",
-            "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply", "bk_alg1_run"]
+            "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply", "bk_alg1_run", "bk_dirk_solve_dc"]
 
 
 class SolveOpts(ctypes.Structure):
@@ -94,6 +94,7 @@ _sig = {
     "bk_plan_halo": ([_I, _I, _P, _I64, _P, _P, _I64, _P, _P, _P, _P, _P], _I),
     "bk_plan_bands": ([_I64, _P, _P, _I, _P], _I),
     "bk_dirk_solve": ([_P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _I64, _P, _I64, _I, _D, _P, _P], _I),
+    "bk_dirk_solve_dc": ([_P, _P, _P, _D, _D, _I, _P, _P, _P, _P, _I64, _P, _I64, _I, _D, _P, _P], _I),
     "bk_precond_apply": ([_P, _P, _I, _P, _P, _I64, _P, _I64], _I),
     "bk_alg1_run": ([_P, _P, _I, _P, _I, _I, _D, _I, _P, _P, _I64, _P, _P], _I),
 }
@@ -456,7 +457,7 @@ class DirkReport(ctypes.Structure):
 
 
 def dirk_solve(ctx: Context, L: Matrix, K: Matrix, mass: float, tau: float, A1, A2, B, B0, Y, *,
-               max_outer=None, outer_tol=0.0, **inner):
+               max_outer=None, outer_tol=0.0, correction=False, **inner):
     """NEXT-1 DIRK window (bk_dirk_solve): M Y A1^T + K Y A2^T = B A2^T + B0 by the splitting
     fixed point; `inner` = block_krylov_solve options.  Y: initial guess in, solution out.
     Returns (status, report dict)."""
@@ -471,7 +472,8 @@ def dirk_solve(ctx: Context, L: Matrix, K: Matrix, mass: float, tau: float, A1, 
         raise ValueError("A1, A2 must be k x k")
     o = solve_opts(**inner)
     rep = DirkReport()
-    st = _lib.bk_dirk_solve(ctx.handle, L.handle, K.handle, float(mass), float(tau), kb, _P(a1.ctypes.data),
+    fn = _lib.bk_dirk_solve_dc if correction else _lib.bk_dirk_solve
+    st = fn(ctx.handle, L.handle, K.handle, float(mass), float(tau), kb, _P(a1.ctypes.data),
                             _P(a2.ctypes.data), _P(pb), _P(p0), ldb, _P(py), ldy,
                             kb if max_outer is None else int(max_outer), float(outer_tol), ctypes.byref(o),
                             ctypes.byref(rep))

@@ -759,10 +759,10 @@ extern "C" int bk_alg1_run(bk_ctx* ctx, const bk_dr_problem* pb, int m, const do
 }
 
 // ------------------------------------------------------------------ NEXT-1 DIRK window (dirk.cpp)
-extern "C" int bk_dirk_solve(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k,
-                             const double* A1, const double* A2, const double* B, const double* B0, int64_t ldb,
-                             double* Y, int64_t ldy, int max_outer, double outer_tol, const bk_solve_opts* inner,
-                             bk_dirk_report* rep) {
+static int dirk_entry(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k,
+                      const double* A1, const double* A2, const double* B, const double* B0, int64_t ldb,
+                      double* Y, int64_t ldy, int max_outer, double outer_tol, const bk_solve_opts* inner,
+                      bk_dirk_report* rep, bool correction) {
     int r = enter(ctx);
     if (r) return r;
     ARG_CHECK(ctx, L && K && L->ctx == ctx && K->ctx == ctx, "bk_dirk_solve: matrix NULL or from another ctx");
@@ -799,11 +799,26 @@ extern "C" int bk_dirk_solve(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, doub
         dY = (double*)ws_get(ctx, WS_STAGE_Y, (size_t)n * ldy * sizeof(double));
         CUDA_OK(ctx, cudaMemcpyAsync(dY, Y, (size_t)n * ldy * sizeof(double), cudaMemcpyHostToDevice, ctx->stream));
     }
-    r = dirk_impl(ctx, L, K, mass, tau, k, A1, A2, dB, dB0, ldb, dY, ldy, max_outer, outer_tol, inner, rep);
+    r = dirk_impl(ctx, L, K, mass, tau, k, A1, A2, dB, dB0, ldb, dY, ldy, max_outer, outer_tol, inner, rep,
+                  correction);
     if (r == BK_ERR_CUDA || r == BK_ERR_NCCL || r == BK_ERR_OOM || r == BK_ERR_ARG) return r;
     if (yh)
         CUDA_OK(ctx, cudaMemcpyAsync(Y, dY, (size_t)n * ldy * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
     CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
     return r;
     BK_CATCH(ctx)
+}
+
+extern "C" int bk_dirk_solve(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k,
+                             const double* A1, const double* A2, const double* B, const double* B0, int64_t ldb,
+                             double* Y, int64_t ldy, int max_outer, double outer_tol, const bk_solve_opts* inner,
+                             bk_dirk_report* rep) {
+    return dirk_entry(ctx, L, K, mass, tau, k, A1, A2, B, B0, ldb, Y, ldy, max_outer, outer_tol, inner, rep, false);
+}
+
+extern "C" int bk_dirk_solve_dc(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k,
+                                const double* A1, const double* A2, const double* B, const double* B0, int64_t ldb,
+                                double* Y, int64_t ldy, int max_outer, double outer_tol, const bk_solve_opts* inner,
+                                bk_dirk_report* rep) {
+    return dirk_entry(ctx, L, K, mass, tau, k, A1, A2, B, B0, ldb, Y, ldy, max_outer, outer_tol, inner, rep, true);
 }

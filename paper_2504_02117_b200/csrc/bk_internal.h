@@ -313,7 +313,7 @@ int solve_impl(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb
                int64_t ldx, const bk_solve_opts* o, bk_solve_report* rep);
 int dirk_impl(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k, const double* A1h,
               const double* A2h, const double* B, const double* B0, int64_t ldb, double* Y, int64_t ldy,
-              int max_outer, double outer_tol, const bk_solve_opts* inner, bk_dirk_report* rep);
+              int max_outer, double outer_tol, const bk_solve_opts* inner, bk_dirk_report* rep, bool correction = false);
 // device-pointer variants used by the solvers (no host staging, no validation)
 int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, const double* C,
              int kout, double alpha, double beta, double* Y, int64_t ldy);

@@ -38,7 +38,7 @@ void upd(bk_ctx* ctx, int64_t n, int k, double* out, int64_t ldo, double a, cons
 
 int dirk_impl(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k, const double* A1h,
               const double* A2h, const double* B, const double* B0, int64_t ldb, double* Y, int64_t ldy,
-              int max_outer, double outer_tol, const bk_solve_opts* inner, bk_dirk_report* rep) {
+              int max_outer, double outer_tol, const bk_solve_opts* inner, bk_dirk_report* rep, bool correction) {
     cudaStream_t st = ctx->stream;
     const int64_t n = L->n_local;
     cudaEvent_t e0, e1;
@@ -65,6 +65,8 @@ int dirk_impl(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double
     double* Rhs = (double*)ws_get(ctx, WS_DIRK + 2, vb);
     double* Yp = (double*)ws_get(ctx, WS_DIRK + 3, vb);
     double* D = (double*)ws_get(ctx, WS_DIRK + 4, vb);
+    double* Ds = (double*)ws_get(ctx, WS_DIRK + 5, vb);
+    double* hsm = (double*)ctx->h_pinned + 8192;   // pinned staging for the column scales
     // R0 = B0 + B A2^T (fixed part of every right-hand side)
     if (n > 0) {
         upd(ctx, n, k, R0, k, 1.0, B0, ldb, 1.0, B, ldb, k, dA2T);
@@ -79,9 +81,63 @@ int dirk_impl(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double
     o.x0_is_zero = 1;
     memset(rep, 0, sizeof *rep);
     rep->status = BK_OK;
-    double change = 0.0;
+    double change = 0.0, ff0 = 0.0;
     int j = 0;
-    for (; j < max_outer; ++j) {
+    for (; j < max_outer && correction; ++j) {
+        // defect correction (loose inner tolerance, the outer iterations refresh the
+        // right-hand side): F = Rhs(Y) - L Y; L D = F (x0 = 0, inner rtol relative to F); Y += D.
+        // Columns of F are scaled to unit norm first (converged stages have tiny defects; the
+        // block methods do not deflate, R6); a block breakdown falls back to column-wise solves.
+        if (n > 0) {
+            upd(ctx, n, k, Rhs, k, 1.0, R0, k, 1.0, Y, ldy, k, dC1);
+            r = cuda_check(ctx, cudaGetLastError(), "dirk rhs");
+            if (r) return r;
+        }
+        r = spmm_dev(ctx, K, k, Y, ldy, dC2, k, -1.0, 1.0, Rhs, k);
+        if (!r) r = spmm_dev(ctx, L, k, Y, ldy, nullptr, k, -1.0, 1.0, Rhs, k);   // F = Rhs - L Y
+        if (!r) r = gram_dev(ctx, n, k, k, Rhs, k, Rhs, k, G, ctx->nranks > 1);
+        if (!r) r = gram_dev(ctx, n, k, k, Y, ldy, Y, ldy, G + k * k, ctx->nranks > 1);
+        if (r) return r;
+        if ((r = cuda_check(ctx, cudaMemcpyAsync(hsm, G, 2 * (size_t)k * k * sizeof(double), cudaMemcpyDeviceToHost,
+                                                 st), "dirk defect")))
+            return r;
+        if ((r = cuda_check(ctx, cudaStreamSynchronize(st), "dirk sync"))) return r;
+        double ff = 0.0, yy = 0.0;
+        std::vector<double> sc(2 * (size_t)k * k, 0.0);
+        for (int c = 0; c < k; ++c) {
+            const double fc = std::sqrt(std::max(hsm[c * k + c], 0.0));
+            ff += hsm[c * k + c];
+            yy += hsm[k * k + c * k + c];
+            sc[c * k + c] = fc > 0.0 ? 1.0 / fc : 1.0;
+            sc[k * k + c * k + c] = fc > 0.0 ? fc : 0.0;
+        }
+        // outer test on the defect reduction ||F^j||_F / ||F^0||_F (before solving)
+        if (j == 0) ff0 = ff;
+        change = ff0 > 0.0 ? std::sqrt(ff / ff0) : 0.0;
+        if (j > 0 && outer_tol > 0.0 && change <= outer_tol) break;
+        double* dsc = G + 2 * k * k;
+        if ((r = cuda_check(ctx, cudaMemcpyAsync(dsc, sc.data(), sc.size() * sizeof(double), cudaMemcpyHostToDevice,
+                                                 st), "dirk scales")))
+            return r;
+        if (n > 0) upd(ctx, n, k, Ds, k, 0.0, nullptr, k, 1.0, Rhs, k, k, dsc);   // Fs = F S^-1
+        bk_solve_report sr;
+        r = solve_impl(ctx, L, k, Ds, k, D, k, &o, &sr);
+        if (r == BK_ERR_CUDA || r == BK_ERR_NCCL || r == BK_ERR_OOM || r == BK_ERR_ARG) return r;
+        rep->inner_iterations_total += sr.iterations;
+        rep->last_inner_status = sr.status;
+        if (sr.status == BK_BREAKDOWN) {   // rank-deficient defect block: one column at a time
+            for (int c = 0; c < k; ++c) {
+                r = solve_impl(ctx, L, 1, Ds + c, k, D + c, k, &o, &sr);
+                if (r == BK_ERR_CUDA || r == BK_ERR_NCCL || r == BK_ERR_OOM || r == BK_ERR_ARG) return r;
+                rep->inner_iterations_total += sr.iterations;
+                if (sr.status == BK_BREAKDOWN) { rep->status = BK_BREAKDOWN; break; }
+            }
+            if (rep->status == BK_BREAKDOWN) { ++j; break; }
+        }
+        if (n > 0) upd(ctx, n, k, Y, ldy, 1.0, Y, ldy, 1.0, D, k, k, dsc + k * k);   // Y += D S
+        (void)yy;
+    }
+    for (; j < max_outer && !correction; ++j) {
         if (n > 0) {
             // Rhs = R0 + Y C1 - K Y C2   (one update pass + one coupled apply)
             upd(ctx, n, k, Rhs, k, 1.0, R0, k, 1.0, Y, ldy, k, dC1);

@@ -32,6 +32,7 @@ ap.add_argument("--precond", default="none")
 ap.add_argument("--inner-rtol", type=float, default=None,
                 help="window inner tolerance (the paper's policy for s > 1: 1e-2, outer 1e-8; default --rtol)")
 ap.add_argument("--outer-tol", type=float, default=1e-9)
+ap.add_argument("--correction", action="store_true", help="bk_dirk_solve_dc (defect-correction form)")
 a = ap.parse_args()
 v = (0.0, 0.0) if a.sym else (1.0, 0.5)
 irtol = a.rtol if a.inner_rtol is None else a.inner_rtol
@@ -63,12 +64,13 @@ for s in [int(x) for x in a.s.split(",")]:
     # ---- window (all stages of s steps at once)
     Y = torch.zeros(N, k, dtype=torch.float64, device=dev)
     bk.dirk_solve(ctx, L, K, mass, tau, A1.numpy(), A2.numpy(), B, B0, Y, max_outer=4 * k, outer_tol=a.outer_tol,
-                  method=a.method, rtol=irtol, max_iters=2000, precond=a.precond)   # warm-up
+                  method=a.method, rtol=irtol, max_iters=2000, precond=a.precond, correction=a.correction)  # warm-up
     Y.zero_()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     st, rep = bk.dirk_solve(ctx, L, K, mass, tau, A1.numpy(), A2.numpy(), B, B0, Y, max_outer=4 * k,
-                            outer_tol=a.outer_tol, method=a.method, rtol=irtol, max_iters=2000, precond=a.precond)
+                            outer_tol=a.outer_tol, method=a.method, rtol=irtol, max_iters=2000, precond=a.precond,
+                            correction=a.correction)
     torch.cuda.synchronize()
     t_win = (time.perf_counter() - t0) * 1e3
     # ---- sequential stepping: (M/tau + a_ii K) y_i = M y_n / tau + a_ii b_i + sum_{j<i} a_ij (b_j - K y_j)
@@ -103,7 +105,7 @@ for s in [int(x) for x in a.s.split(",")]:
     t_seq = (time.perf_counter() - t0) * 1e3
     diff = float(torch.linalg.norm(Y - Ys) / torch.linalg.norm(Ys))
     print(json.dumps({"n": n, "s": s, "k": k, "method": a.method, "precond": a.precond, "sym": a.sym,
-                      "rtol": a.rtol, "inner_rtol": irtol, "outer_tol": a.outer_tol, "window_status": st,
+                      "rtol": a.rtol, "inner_rtol": irtol, "correction": a.correction, "outer_tol": a.outer_tol, "window_status": st,
                       "outer": rep["outer_iterations"], "inner_window": rep["inner_iterations_total"],
                       "window_ms": round(t_win, 2), "inner_sequential": inner_seq,
                       "sequential_ms": round(t_seq, 2), "speedup": round(t_seq / t_win, 2),
