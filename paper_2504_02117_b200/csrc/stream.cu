@@ -188,13 +188,14 @@ __device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* c
 #pragma unroll
         for (int nb = 0; nb < NK; ++nb) {
             const int c = 8 * nb + 2 * kq;
+            const bool cin = rin && c < k;   // (k % 8 == 4: the last block is half outside)
             double d0 = 0.0, d1 = 0.0;
-            if (rin && Xt) {
+            if (cin && Xt) {
                 const double2 x = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
                 d0 = U.a * x.x;
                 d1 = U.a * x.y;
             }
-            if (rin && Wt) {
+            if (cin && Wt) {
                 const double2 w = *reinterpret_cast<const double2*>(Wt + (int64_t)r * k + c);
                 d0 = fma(wv, w.x, d0);
                 d1 = fma(wv, w.y, d1);
@@ -202,7 +203,7 @@ __device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* c
             // D(row = mg, cols 2kq, 2kq+1): the accumulator layout of m8n8k4
 #pragma unroll
             for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], bf[ks][nb]);
-            if (rin) *reinterpret_cast<double2*>(U.out + (r0 + r) * U.ldo + c) = make_double2(d0, d1);
+            if (cin) *reinterpret_cast<double2*>(U.out + (r0 + r) * U.ldo + c) = make_double2(d0, d1);
         }
     }
 }
@@ -226,7 +227,10 @@ __global__ void __launch_bounds__(NC + 32, 2) upd_stream_mma_kernel(const UpdStr
 #pragma unroll
     for (int ks = 0; ks < NQ; ++ks)
 #pragma unroll
-        for (int nb = 0; nb < NK; ++nb) bf[ks][nb] = U.s * U.C[(4 * ks + (lane & 3)) * U.k + 8 * nb + (lane >> 2)];
+        for (int nb = 0; nb < NK; ++nb) {   // (k a multiple of 4: columns >= k are zero)
+            const int oc = 8 * nb + (lane >> 2);
+            bf[ks][nb] = oc < U.k ? U.s * U.C[(4 * ks + (lane & 3)) * U.k + oc] : 0.0;
+        }
     const double wv = U.iW >= 0 ? (U.w_dev ? U.w_host * *U.w_dev : U.w_host) : 0.0;
     int i = 0;
     for (int tile = blockIdx.x; tile < U.S.ntiles; tile += gridDim.x, ++i) {
@@ -1270,8 +1274,8 @@ bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
         const char* e = getenv("BK_UPD");
         mma = (e && strcmp(e, "fma") == 0) ? 0 : 1;
     }
-    if (mma && u.kp > 0 && u.k % 8 == 0 && u.kp % 4 == 0) {
-        const int nq = u.kp / 4, nk = u.k / 8;
+    if (mma && u.kp > 0 && u.k % 4 == 0 && u.kp % 4 == 0) {   // (k = 12, 20, 28: padded last block)
+        const int nq = u.kp / 4, nk = (u.k + 7) / 8;
 #define BK_UM(Q, K)                                                                            \
     if (nq == Q && nk == K) {                                                                  \
         static bool at = false;                                                                \
