@@ -511,8 +511,11 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     const double tol = S.o->breakdown_tol;
     const double* om = &S.ds->omega;
     const double* nom = &S.ds->neg_omega;
-    const bool fused = fused_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
-                       ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
+    // (k a multiple of 4: the tail pads its last 8-column block; the column dots ride in the
+    // RtT pass only when k divides 32, else they take one coldot pass before it)
+    const bool fused = fused_enabled() && use_stream_kernels() && S.n > 0 && k % 4 == 0 && k <= 16 &&
+                       ldx == k && ((uintptr_t)X % 16) == 0;
+    const bool dots_fused = (32 % k) == 0;
     // one rank: the k x k steps run in the epilogue of the pass that produces their
     // input (no separate small-kernel launches); p > 1: after the allreduce
     // (BK_EPI=0: separate one-warp kernels instead of the epilogues -- A/B timing)
@@ -545,7 +548,9 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
             double* const blk[3][2] = {{RtT, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
             const int dp[2][2] = {{2, 1}, {2, 2}};   // <T,S>, <T,T> per column
             double* const dots[2] = {ts, tt};
-            TRY(S.gram_multi(1, xs, 1, ys, 3, arr, blk, 2, dp, dots, epi ? &e_be : nullptr, BK_K_FUSED_DOTS));
+            if (!dots_fused) TRY(S.coldot(T, k, Sv, k, T, k, ts, tt));   // before the pass whose epilogue uses them
+            TRY(S.gram_multi(1, xs, 1, ys, 3, arr, blk, dots_fused ? 2 : 0, dp, dots, epi ? &e_be : nullptr,
+                             BK_K_FUSED_DOTS));
             if (!epi) {
                 sd_omega(ts, tt, k, S.ds, S.st);
                 sd_lu_resolve(LUf, piv, RtT, be, k, k, -1.0, S.ds, S.st);   // same M1: no new breakdown

@@ -951,8 +951,9 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
     for (int ks = 0; ks < NQ; ++ks)
 #pragma unroll
         for (int nb = 0; nb < NK; ++nb) {
-            s_ba[(ks * NK + nb) * 32 + lane] = U.al[(4 * ks + kq) * k + 8 * nb + mg];
-            s_bb[(ks * NK + nb) * 32 + lane] = U.be[(4 * ks + kq) * k + 8 * nb + mg];
+            const bool oc = 8 * nb + mg < k;   // (k % 8 == 4: the last block is half padding)
+            s_ba[(ks * NK + nb) * 32 + lane] = oc ? U.al[(4 * ks + kq) * k + 8 * nb + mg] : 0.0;
+            s_bb[(ks * NK + nb) * 32 + lane] = oc ? U.be[(4 * ks + kq) * k + 8 * nb + mg] : 0.0;
         }
     __syncwarp();
     const double w = *U.w_dev;
@@ -985,8 +986,9 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
 #pragma unroll
             for (int nb = 0; nb < NK; ++nb) {
                 const int c = 8 * nb + 2 * kq;
+                const bool cin = rin && c < k;
                 double x0 = 0.0, x1 = 0.0, r0v = 0.0, r1v = 0.0;
-                if (rin) {
+                if (cin) {
                     const double2 xv = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
                     const double2 sv = *reinterpret_cast<const double2*>(St + (int64_t)r * k + c);
                     const double2 tv = *reinterpret_cast<const double2*>(Tt + (int64_t)r * k + c);
@@ -1001,7 +1003,7 @@ __global__ void __launch_bounds__(NC + 32, 2) bcg_tail_stream_kernel(const BcgTa
                     dmma(x0, x1, ap[ks], s_ba[(ks * NK + nb) * 32 + lane]);
                     dmma(p0, p1, aq[ks], s_bb[(ks * NK + nb) * 32 + lane]);
                 }
-                if (rin) {
+                if (cin) {
                     const int64_t o = (r0 + r) * k + c;
                     *reinterpret_cast<double2*>(U.X + o) = make_double2(x0, x1);
                     *reinterpret_cast<double2*>(U.R + o) = make_double2(r0v, r1v);
@@ -1439,7 +1441,7 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
         return true;                                                                             \
     }
     // kw <= 8: (1..3) x (1..2) blocks of 8; kw = 16: (2..6) x (2..4)
-    BK_GM(1, 1) BK_GM(1, 2) BK_GM(2, 1) BK_GM(3, 1) BK_GM(2, 2) BK_GM(3, 2)
+    BK_GM(1, 1) BK_GM(1, 2) BK_GM(2, 1) BK_GM(3, 1) BK_GM(2, 2) BK_GM(3, 2) BK_GM(2, 3)
     BK_GM(2, 4) BK_GM(4, 2) BK_GM(6, 2) BK_GM(4, 4)
 #undef BK_GM
     return false;
@@ -1449,7 +1451,7 @@ bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, c
                             const double* V, const double* al, const double* be, const double* w_dev, double* rr,
                             const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st,
                             const SmallEpi* epi) {
-    if (n <= 0 || k % 8 != 0 || k > 32) return false;
+    if (n <= 0 || k % 4 != 0 || k > 32) return false;
     const double* arr[5] = {X, P, S, T, V};
     BcgTail U{};
     for (int q = 0; q < 5; ++q) {
@@ -1463,15 +1465,16 @@ bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, c
     U.red.part = part; U.red.ticket = ticket; U.red.G = rr; U.red.G2 = nullptr;
     if (epi) U.red.epi = *epi;
     const int grid = grid_for(U.S.ntiles, num_sms);
-    const int smem = NSTAGE * STAGE_BYTES + 128 + 2 * (k / 4) * (k / 8) * 32 * 8;
+    const int nq = k / 4, nk = (k + 7) / 8;
+    const int smem = NSTAGE * STAGE_BYTES + 128 + 2 * nq * nk * 32 * 8;
 #define BK_BT(Q, K)                                                                              \
-    if (k == 8 * K) {                                                                            \
+    if (nq == Q && nk == K) {                                                                    \
         static bool at = false;                                                                  \
         if (!at) { set_smem((const void*)bcg_tail_stream_kernel<Q, K>, smem); at = true; }       \
         BK_KERNEL(bcg_tail_stream_kernel<Q, K><<<grid, NC + 32, smem, st>>>(U));                  \
         return true;                                                                             \
     }
-    BK_BT(2, 1) BK_BT(4, 2) BK_BT(6, 3) BK_BT(8, 4)
+    BK_BT(1, 1) BK_BT(2, 1) BK_BT(3, 2) BK_BT(4, 2) BK_BT(6, 3) BK_BT(8, 4)
 #undef BK_BT
     return false;
 }

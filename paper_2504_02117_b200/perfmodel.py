@@ -73,8 +73,8 @@ def coldot_bytes(n: int, k: int, n_y: int = 1) -> int:
 
 
 def bicgstab_fused(k: int) -> bool:
-    """Whether solve.cpp takes the fused BiCGStab passes (k % 8 == 0, k <= 16)."""
-    return k % 8 == 0 and k <= 16
+    """Whether solve.cpp takes the fused BiCGStab passes (k % 4 == 0, k <= 16)."""
+    return k % 4 == 0 and k <= 16
 
 
 def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> int:
@@ -87,7 +87,8 @@ def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> 
         fused = bicgstab_fused(k)
     if fused:
         v = 8 * n * k
-        return 2 * spmm_bytes(n, nnz, k) + 3 * v + update_bytes(n, k, k) + 3 * v + 8 * v
+        dots = 0 if 32 % k == 0 else coldot_bytes(n, k, 2)   # <T,S>, <T,T> in their own pass
+        return 2 * spmm_bytes(n, nnz, k) + 3 * v + update_bytes(n, k, k) + 3 * v + 8 * v + dots
     b = 2 * spmm_bytes(n, nnz, k)                     # V = A P, T = A S
     b += 3 * gram_bytes(n, k, k)                      # Rt^T V, Rt^T R, Rt^T T
     b += coldot_bytes(n, k, 2) + coldot_bytes(n, k, 1)  # <T,S>, <T,T>; ||R||
@@ -99,8 +100,14 @@ def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> 
     return b
 
 
-def cg_iter_bytes(n: int, nnz: int, k: int) -> int:
-    """One block CG iteration (unpreconditioned) as enqueued by solve.cpp (O4)."""
+def cg_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> int:
+    """One block CG iteration (unpreconditioned) as enqueued by solve.cpp (O4).  Fused (k = 8, 16):
+    apply + P^T Q (2 reads) + tail X, P, R, Q -> X, R with R^T R (4 reads, 2 writes) + P update."""
+    if fused is None:
+        fused = k % 8 == 0 and k <= 16
+    if fused:
+        v = 8 * n * k
+        return spmm_bytes(n, nnz, k) + 2 * v + 6 * v + update_bytes(n, k, k)
     return (spmm_bytes(n, nnz, k) + gram_bytes(n, k, k) + 2 * update_bytes(n, k, k)
             + gram_bytes(n, k, k, same=True) + update_bytes(n, k, k))
 

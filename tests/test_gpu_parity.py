@@ -309,6 +309,8 @@ SOLVES = [("cg", "c1s", {}), ("gmres", "c1", {"restart": 100}), ("gmres", "c1", 
 # (GMRES(20) at k = 16 stagnates on c1 in the oracle as well: not a parity case.)
 SOLVE_CASES = [(m, c, kw, k) for (m, c, kw) in SOLVES for k in (1, 4, 8, 16)
                if not (m == "gmres" and kw.get("restart") == 20 and k == 16)]
+# k = 12: the fused BiCGStab with a padded tail block and a separate column-dot pass
+SOLVE_CASES += [("bicgstab", "c1", {}, 12), ("gmres", "c1", {"restart": 100}, 12), ("cg", "c1s", {}, 12)]
 
 
 @pytest.mark.parametrize("method,cfg,kw,k", SOLVE_CASES)
