@@ -409,8 +409,8 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     // fused pass structure: Q = A P ; PQ = P^T Q (al solve in its epilogue) ;
     // X += P al, R -= Q al, RZn = R^T R in one pass (test, be solve, RZ roll-over in its
     // epilogue) ; P = R + P be.  13 N x k passes per iteration instead of 14, 4 launches instead of 9.
-    const bool fused = !jac && fused_enabled() && use_stream_kernels() && S.n > 0 && k % 8 == 0 && k <= 16 &&
-                       ldx == k && ((uintptr_t)X % 16) == 0 && (32 % k) == 0;
+    const bool fused = !jac && fused_enabled() && use_stream_kernels() && S.n > 0 && k % 4 == 0 && k <= 16 &&
+                       ldx == k && ((uintptr_t)X % 16) == 0;
     // (BK_EPI=0: separate one-warp kernels instead of the epilogues -- A/B timing)
     static const int epi_env = env_int("BK_EPI", 1);
     const bool epi = fused && !S.allred && epi_env != 0;

@@ -1071,7 +1071,8 @@ __global__ void __launch_bounds__(NC + 32, 2) cg_tail_stream_kernel(const CgTail
 #pragma unroll
     for (int ks = 0; ks < NQ; ++ks)
 #pragma unroll
-        for (int nb = 0; nb < NK; ++nb) s_ba[(ks * NK + nb) * 32 + lane] = U.al[(4 * ks + kq) * k + 8 * nb + mg];
+        for (int nb = 0; nb < NK; ++nb)   // (k % 8 == 4: the last block is half padding)
+            s_ba[(ks * NK + nb) * 32 + lane] = 8 * nb + mg < k ? U.al[(4 * ks + kq) * k + 8 * nb + mg] : 0.0;
     __syncwarp();
     double g[NK][NK][2];
 #pragma unroll
@@ -1103,8 +1104,9 @@ __global__ void __launch_bounds__(NC + 32, 2) cg_tail_stream_kernel(const CgTail
 #pragma unroll
             for (int nb = 0; nb < NK; ++nb) {
                 const int c = 8 * nb + 2 * kq;
+                const bool cin = rin && c < k, cok = c < k;
                 double x0 = 0.0, x1 = 0.0, q0 = 0.0, q1 = 0.0;
-                if (rin) {
+                if (cin) {
                     const double2 xv = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
                     const double2 rv = dir ? *reinterpret_cast<const double2*>(Rg + (int64_t)r * k + c)
                                            : *reinterpret_cast<const double2*>(Rt + (int64_t)r * k + c);
@@ -1116,12 +1118,12 @@ __global__ void __launch_bounds__(NC + 32, 2) cg_tail_stream_kernel(const CgTail
                     dmma(x0, x1, ap[ks], b);
                     dmma(q0, q1, aq[ks], b);
                 }
-                if (rin) {
+                if (cin) {
                     const int64_t o = (r0 + r) * k + c;
                     *reinterpret_cast<double2*>(U.X + o) = make_double2(x0, x1);
                     *reinterpret_cast<double2*>(U.R + o) = make_double2(q0, q1);
                 }
-                if (!dir) *reinterpret_cast<double2*>(Rt + (int64_t)(rb + mg) * k + c) =
+                if (!dir && cok) *reinterpret_cast<double2*>(Rt + (int64_t)(rb + mg) * k + c) =
                     rin ? make_double2(q0, q1) : make_double2(0.0, 0.0);
             }
             // Gram of the block's new rows (this warp wrote them): two k-steps of 4 rows
@@ -1132,7 +1134,7 @@ __global__ void __launch_bounds__(NC + 32, 2) cg_tail_stream_kernel(const CgTail
                 const int rr = rb + 4 * h + kq;
                 double a[NK];
 #pragma unroll
-                for (int i = 0; i < NK; ++i) a[i] = rr < nr ? Rn[(int64_t)rr * k + 8 * i + mg] : 0.0;
+                for (int i = 0; i < NK; ++i) a[i] = (rr < nr && 8 * i + mg < k) ? Rn[(int64_t)rr * k + 8 * i + mg] : 0.0;
 #pragma unroll
                 for (int i = 0; i < NK; ++i)
 #pragma unroll
@@ -1482,7 +1484,7 @@ bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, c
 bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double* P, const double* Q,
                            const double* al, double* G, const int* halt, double* part, int* ticket, int num_sms,
                            cudaStream_t st, const SmallEpi* epi) {
-    if (n <= 0 || k % 8 != 0 || k > 32) return false;
+    if (n <= 0 || k % 4 != 0 || k > 32) return false;
     const double* arr[4] = {X, P, R, Q};
     CgTail U{};
     for (int q = 0; q < 4; ++q) {
@@ -1495,15 +1497,16 @@ bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double*
     U.red.part = part; U.red.ticket = ticket; U.red.G = G; U.red.G2 = nullptr; U.red.ka = k; U.red.kb = k;
     if (epi) U.red.epi = *epi;
     const int grid = grid_for(U.S.ntiles, num_sms);
-    const int smem = NSTAGE * STAGE_BYTES + 128 + (k / 4) * (k / 8) * 32 * 8;
+    const int nq = k / 4, nk = (k + 7) / 8;
+    const int smem = NSTAGE * STAGE_BYTES + 128 + nq * nk * 32 * 8;
 #define BK_CT(Q, K)                                                                              \
-    if (k == 8 * K) {                                                                            \
+    if (nq == Q && nk == K) {                                                                    \
         static bool at = false;                                                                  \
         if (!at) { set_smem((const void*)cg_tail_stream_kernel<Q, K>, smem); at = true; }        \
         BK_KERNEL(cg_tail_stream_kernel<Q, K><<<grid, NC + 32, smem, st>>>(U));                   \
         return true;                                                                             \
     }
-    BK_CT(2, 1) BK_CT(4, 2) BK_CT(6, 3) BK_CT(8, 4)
+    BK_CT(1, 1) BK_CT(2, 1) BK_CT(3, 2) BK_CT(4, 2) BK_CT(6, 3) BK_CT(8, 4)
 #undef BK_CT
     return false;
 }

@@ -101,10 +101,10 @@ def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> 
 
 
 def cg_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> int:
-    """One block CG iteration (unpreconditioned) as enqueued by solve.cpp (O4).  Fused (k = 8, 16):
+    """One block CG iteration (unpreconditioned) as enqueued by solve.cpp (O4).  Fused (k % 4 == 0, <= 16):
     apply + P^T Q (2 reads) + tail X, P, R, Q -> X, R with R^T R (4 reads, 2 writes) + P update."""
     if fused is None:
-        fused = k % 8 == 0 and k <= 16
+        fused = k % 4 == 0 and k <= 16
     if fused:
         v = 8 * n * k
         return spmm_bytes(n, nnz, k) + 2 * v + 6 * v + update_bytes(n, k, k)
