@@ -81,13 +81,27 @@ class Clocks:
         try:
             self.f = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                          "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
+            self._wait_lines(1, 5.0)       # sampler running before the timed region starts
+            self.n0 = self._lines()
         except Exception:
             self.proc = None
         return self
 
+    def _lines(self):
+        try:
+            return sum(1 for ln in open(self.path) if ln.strip())
+        except Exception:
+            return 0
+
+    def _wait_lines(self, n, timeout):
+        t0 = time.time()
+        while self._lines() < n and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
     def __exit__(self, *a):
         if self.proc:
+            self._wait_lines(self.n0 + 1, 1.0)   # at least one sample taken during the region
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
