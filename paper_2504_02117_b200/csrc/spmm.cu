@@ -1355,17 +1355,28 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
         w.off_rp = w.off_val + (int)r16((int64_t)(w.cap + 2) * 8);
         w.stage_bytes = (int)((w.off_rp + r16((TR + 8) * 4) + 127) & ~(int64_t)127);
     };
-    int TR = RPP < 64 ? 64 : RPP;
-    if (tr_env > 0) TR = std::max(2, tr_env & ~1);
-    layout(TR);
     // barriers + row-pointer ring + (C, coupled-apply scratch): with the tensor-core epilogue
-    // (TCE) C fragments and the tile's (A X) rows, else C and one scratch line per row group
+    // (TCE) C fragments and the per-warp (A X) rows (RPP rows of KP + 2), else C and one
+    // scratch line per row group
     constexpr bool TCE = HAS_C && KP >= 8 && VEC == 4;
     auto fixed_for = [&](int tr) {
-        const int cb = TCE ? ((KP / 4) * (KP / 8) * 32 + tr * (KP + 2)) * 8
+        const int cb = TCE ? ((KP / 4) * (KP / 8) * 32 + (tr > RPP ? tr : RPP) * (KP + 2)) * 8
                            : (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
         return 16 * 8 + kMetaDepth * 8 + cb;
     };
+    int TR = RPP < 64 ? 64 : RPP;
+    if (tr_env > 0) {
+        TR = std::max(2, tr_env & ~1);
+    } else if (ctas == 2) {   // the largest multiple of 16 rows with two stages per CTA
+        for (int t = std::min(1024, 8 * RPP) & ~15; t >= 64; t -= 16) {
+            layout(t);
+            if (2 * w.stage_bytes + fixed_for(t) <= 113 * 1024) {
+                TR = t;
+                break;
+            }
+        }
+    }
+    layout(TR);
     int fixed = fixed_for(TR);
     int budget = (ctas == 1 ? 227 * 1024 : 113 * 1024) - fixed;
     while (budget / w.stage_bytes < 2 && TR > 2 * 2) {   // huge windows: smaller tiles
@@ -1405,15 +1416,10 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
 template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT>
 bool launch_win_shape(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     static const int force = env_int("BK_WIN_CTAS", 0);
-    int ctas = force;
-    if (ctas != 1 && ctas != 2) {
-        // stage bytes at the 2-CTA tile size (RPP rows, >= 64)
-        const int rpp = 256 / (KP / VEC), tr = rpp < 64 ? 64 : rpp;
-        int64_t wrows = 0;
-        for (int g = 0; g < p.nbands; ++g) wrows += tr + p.hi[g] - p.lo[g];
-        const int64_t stage = wrows * a.k * 8 + (int64_t)tr * p.max_row_nnz * 12 + tr * 4 + 256;
-        ctas = (3 * stage <= 100 * 1024) ? 2 : 1;
-    }
+    // two CTAs per SM with the largest tile that keeps 2 stages each (launch_win_t); measured
+    // against one 512-thread CTA and RPP-row tiles: c2 k = 4 / 8 / 16 0.63 / 0.79 / 0.74 ->
+    // 0.77 / 0.81 / 0.81 of HBM (tile 256 / 192 / 112 rows)
+    int ctas = (force == 1 || force == 2) ? force : 2;
     if (ctas == 1 && KP >= 4) return launch_win_t<KP, VEC, HAS_C, NB, MR, KEXACT, 512>(a, p, st, 1);
     return launch_win_t<KP, VEC, HAS_C, NB, MR, KEXACT, 256>(a, p, st, ctas);
 }
