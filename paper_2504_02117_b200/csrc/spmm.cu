@@ -1331,7 +1331,7 @@ bool launch_roll_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
 
 
 template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT, int NC>
-bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int ctas) {
+bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int ctas, bool big_tiles = true) {
     constexpr int LANES = KP / VEC;
     constexpr int RPP = NC / LANES;
     static const int tr_env = env_int("BK_WIN_TR", 0);
@@ -1367,7 +1367,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     int TR = RPP < 64 ? 64 : RPP;
     if (tr_env > 0) {
         TR = std::max(2, tr_env & ~1);
-    } else if (ctas == 2) {   // the largest multiple of 16 rows with two stages per CTA
+    } else if (ctas == 2 && big_tiles) {   // the largest multiple of 16 rows with two stages per CTA
         for (int t = std::min(1024, 8 * RPP) & ~15; t >= 64; t -= 16) {
             layout(t);
             if (2 * w.stage_bytes + fixed_for(t) <= 113 * 1024) {
@@ -1420,6 +1420,16 @@ bool launch_win_shape(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     // against one 512-thread CTA and RPP-row tiles: c2 k = 4 / 8 / 16 0.63 / 0.79 / 0.74 ->
     // 0.77 / 0.81 / 0.81 of HBM (tile 256 / 192 / 112 rows)
     int ctas = (force == 1 || force == 2) ? force : 2;
+    if (force != 1 && force != 2 && HAS_C) {
+        // coupled applies keep the earlier shape rule (3 stages of RPP-row tiles in 100 KB ->
+        // 2 CTAs, else one 512-thread CTA): c2 k = 4 / 16 coupled 0.63 / 0.64 vs 0.48 / 0.60
+        const int rpp = 256 / (KP / VEC), tr = rpp < 64 ? 64 : rpp;
+        int64_t wrows = 0;
+        for (int g = 0; g < p.nbands; ++g) wrows += tr + p.hi[g] - p.lo[g];
+        const int64_t stage = wrows * a.k * 8 + (int64_t)tr * p.max_row_nnz * 12 + tr * 4 + 256;
+        ctas = (3 * stage <= 100 * 1024) ? 2 : 1;
+        if (ctas == 2) return launch_win_t<KP, VEC, HAS_C, NB, MR, KEXACT, 256>(a, p, st, 2, false);
+    }
     if (ctas == 1 && KP >= 4) return launch_win_t<KP, VEC, HAS_C, NB, MR, KEXACT, 512>(a, p, st, 1);
     return launch_win_t<KP, VEC, HAS_C, NB, MR, KEXACT, 256>(a, p, st, ctas);
 }
