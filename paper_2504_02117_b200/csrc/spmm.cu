@@ -595,6 +595,8 @@ void launch_t(const SpmmArgs& a, cudaStream_t st) {
             }
         }
         // (round-1 A/B of ring depth / CTAs per SM / tile size: DESIGN.md §4.1)
+        // (2 CTAs x 2 stages x 512-row tiles or 2 x 3 x 256 measured 15-45 % slower on c3 / c4:
+        // the gathers need the third CTA's warps for latency hiding)
         launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304>(a, num_sms_cached(), st);
     }
 }
