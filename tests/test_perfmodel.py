@@ -34,3 +34,18 @@ def test_algorithmic_bytes():
     assert pm.gram_bytes(10, 3, 2) == 8 * 10 * 5 and pm.gram_bytes(10, 3, 3, same=True) == 240
     assert pm.update_bytes(10, 4, 4) == 8 * 10 * 12 and pm.update_bytes(10, 4, 4, a_nonzero=False) == 640
     assert pm.spmm_flops(100, 4) == 800 and pm.spmm_flops(100, 4, 10, coupled=True) == 800 + 320
+
+
+def test_fused_solver_pass_counts():
+    """The solver byte models count the N x k passes solve.cpp enqueues:
+    fused BiCGStab = 2 applies + 17 passes (+ 3 for the separate column dots when k does not
+    divide 32); fused CG = 1 apply + 11 passes; unfused BiCGStab for k = 3."""
+    from paper_2504_02117_b200 import perfmodel as pm
+    n, nnz = 1000, 5000
+    for k, extra in ((4, 0), (8, 0), (12, 3), (16, 0)):
+        v = 8 * n * k
+        assert pm.bicgstab_iter_bytes(n, nnz, k) == 2 * pm.spmm_bytes(n, nnz, k) + (17 + extra) * v
+    for k in (4, 8, 12, 16):
+        assert pm.cg_iter_bytes(n, nnz, k) == pm.spmm_bytes(n, nnz, k) + 11 * 8 * n * k
+    assert not pm.bicgstab_fused(3) and not pm.bicgstab_fused(32)
+    assert pm.cg_iter_bytes(n, nnz, 3) > pm.spmm_bytes(n, nnz, 3) + 11 * 8 * n * 3
