@@ -463,12 +463,14 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
         static const int walk = env_int("BK_PIPE_WALK", 0);
         if (walk && A->band.nbands >= 3) a.walk_line = -(int64_t)A->band.dmin[A->band.nbands / 2 - 1];
         // 3-D lattice whose z-neighbour planes do not stay in L2 across two planes of streaming
-        // (c5: 512 x 512 planes): y-slab tile order, opt-in (BK_SLAB=1: k <= 16, 2: every k).
-        // ncu c5 k = 16: DRAM reads 20.3 -> 16.5 GB (14.5 GB algorithmic), but repeated sweeps
-        // give 0.68 vs 0.68-0.71 of HBM -- not a reliable gain yet
-        static const int slab = env_int("BK_SLAB", 0);
+        // (c5: 512 x 512 planes): y-slab tile order.  ncu c5 k = 16: DRAM reads 20.3 -> 16.5 GB
+        // (14.5 GB algorithmic); three repeated sweeps: k = 16 0.665-0.675 -> 0.693-0.717 of
+        // HBM, k = 8 0.818 -> 0.812, k = 32 no gain.  Default 12 <= k <= 16 (BK_SLAB=0 off,
+        // 1 every k <= 16, 2 every k)
+        static const int slab = env_int("BK_SLAB", -1);
         const BandPlan& bp = A->band;
-        if (slab && (slab == 2 || k <= 16) && bp.nbands == 5 && bp.dmin[0] == bp.dmax[0] && bp.dmin[1] == bp.dmax[1] && bp.dmin[1] < 0 &&
+        const bool slab_k = slab == 2 || (slab == 1 && k <= 16) || (slab < 0 && k >= 12 && k <= 16);
+        if (slab_k && bp.nbands == 5 && bp.dmin[0] == bp.dmax[0] && bp.dmin[1] == bp.dmax[1] && bp.dmin[1] < 0 &&
             bp.dmin[0] < bp.dmin[1] && a.row0 == bp.row0 && a.nrows == bp.nrows) {
             const int64_t nx = -(int64_t)bp.dmin[1], plane = -(int64_t)bp.dmin[0];
             if (plane % nx == 0 && a.nrows % plane == 0) {
