@@ -37,6 +37,17 @@ UPD_SCALE = 1e-3
 NX = 1024
 
 
+def load_perfmodel():
+    """perfmodel.py (host-only byte model) loaded by path: importing the package would map
+    libbk.so, which the reference (oracle) arm must not load."""
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bk_perfmodel", os.path.join(ROOT, "paper_2504_02117_b200",
+                                                                                 "perfmodel.py"))
+    m = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(m)
+    return m
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -58,11 +69,10 @@ def step_bytes(pm, n, nnz, ks=KS, solve_k=SOLVE_K, solve_iters=SOLVE_ITERS, n_gh
                         gram_flops=pm.gram_flops(n, k, k), update_flops=pm.update_flops(n, k, k))
         b += sb + gb + ub
         f += parts[k]["spmm_flops"] + parts[k]["gram_flops"] + parts[k]["update_flops"]
-    # solve: x0 = 0 -> R = B (copy), ||R||, Rt = R, P = R, iterations, final true residual
-    k = solve_k
-    sb = (16 * n * k + pm.coldot_bytes(n, k) + 2 * 16 * n * k
-          + solve_iters * pm.bicgstab_iter_bytes(n, nnz, k)
-          + 16 * n * k + pm.spmm_bytes(n, nnz, k, beta_nonzero=True) + pm.coldot_bytes(n, k))
+    # solve: x0 = 0 -> R = B (copy), ||R||, Rt aliases B (no copy), P = R, iterations, final
+    # true residual -- only the passes solve.cpp enqueues (the library reports the same count as
+    # bk_solve_report.alg_bytes; run_ours checks the two agree)
+    sb = pm.bicgstab_solve_bytes(n, nnz, solve_k, solve_iters)
     parts["solve"] = dict(bytes=sb)
     b += sb
     return b, f, parts
@@ -132,8 +142,8 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_2504_02117_b200 as bk
-    from paper_2504_02117_b200 import perfmodel as pm
     import synth
+    pm = load_perfmodel()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -205,9 +215,11 @@ def run_ours(args):
         return rep
 
     # warm-up
+    rep_w = None
     for _ in range(args.warmup):
-        one_step()
+        rep_w = one_step()
     torch.cuda.synchronize()
+    solve_bytes_lib = rep_w["alg_bytes"] if rep_w else None
     if getattr(args, "profile_step", False):
         # one step between cudaProfilerStart/Stop, for `ncu --profile-from-start off`
         flush_l2()
@@ -259,6 +271,9 @@ def run_ours(args):
     ms_per_step = total_ms / args.steps
     n_ghost = info["n_ghost"]
     bytes_rank, flops_rank, parts = step_bytes(pm, n, nnz, n_ghost_rows=n_ghost)
+    if solve_bytes_lib is not None and solve_bytes_lib != parts["solve"]["bytes"]:
+        raise RuntimeError(f"byte model of the solve ({parts['solve']['bytes']}) != the solver's own count "
+                           f"({solve_bytes_lib})")
     bytes_all = bytes_rank * world
     value = bytes_all / (ms_per_step * 1e-3) / 1e9
 
@@ -456,6 +471,7 @@ def run_ours(args):
                        "grid": f"{NX}x{ny}", "rows_per_gpu": n, "nnz_per_gpu": nnz, "ks": list(KS),
                        "solve": f"block BiCGStab k={SOLVE_K}, {SOLVE_ITERS} iterations",
                        "step_alg_bytes_per_gpu": bytes_rank, "step_flops_per_gpu": flops_rank,
+                       "solve_alg_bytes_reported_by_library": solve_bytes_lib,
                        "l2": "flushed (512 MiB write, then read: clean L2) before every timed step and every swept kernel",
                        "parallelism": "single GPU" if world == 1 else f"row partition x{world}, NCCL halo + allreduce"},
             "gpu_launches": launches,
@@ -520,19 +536,83 @@ def oracle_step_fn(rows):
     return step, n, A.nnz
 
 
-def cpu_baseline(rows=262144, reps=1):
-    from paper_2504_02117_b200 import perfmodel as pm
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def oracle_timing(rows, procs, reps, warmup=0):
+    """Run in a fresh interpreter with every BLAS / OpenMP pool at one thread (bench.py
+    --oracle-timing): build the oracle step on the leading `rows`-row principal block of c2, fork
+    `procs` workers that run it concurrently (each worker one core: the oracle is plain
+    single-threaded C + numpy), `warmup` + `reps` rounds separated by a barrier.  Returns the
+    per-round wall time of the slowest worker (seconds) and the step's algorithmic bytes."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               NUMEXPR_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
+    r = subprocess.run([sys.executable, os.path.abspath(__file__), "--oracle-timing", str(rows), str(procs), str(reps),
+                        str(warmup)], env=env, capture_output=True, text=True, timeout=3600)
+    if r.returncode != 0:
+        raise RuntimeError(r.stderr[-800:])
+    return json.loads(r.stdout.strip().splitlines()[-1])
+
+
+def _oracle_timing_main(rows, procs, reps, warmup):
+    import multiprocessing as mp
     step, n, nnz = oracle_step_fn(rows)
-    ts = []
-    for _ in range(reps):
-        t0 = time.perf_counter()
-        step()
-        ts.append(time.perf_counter() - t0)
-    t = statistics.median(ts)
+    pm = load_perfmodel()
     by, _, _ = step_bytes(pm, n, nnz)
-    return {"value": by / t / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": f"same step on the leading {n}-row principal block of c2 ({nnz} nnz), {reps} rep(s), "
-                      f"{t:.2f} s/step; oracle = plain C (gcc -O2, 1 thread) + numpy solver"}
+    ctx = mp.get_context("fork")
+    bar = ctx.Barrier(procs)
+    q = ctx.Queue()
+
+    def worker(i):
+        ts = []
+        for _ in range(warmup + reps):
+            bar.wait()
+            t0 = time.perf_counter()
+            step()
+            ts.append(time.perf_counter() - t0)
+        q.put((i, ts[warmup:]))
+
+    ps = [ctx.Process(target=worker, args=(i,)) for i in range(procs)]
+    for p in ps:
+        p.start()
+    res = dict(q.get() for _ in ps)
+    for p in ps:
+        p.join()
+    rounds = [max(res[i][j] for i in range(procs)) for j in range(reps)]
+    print(json.dumps({"rows": n, "nnz": nnz, "bytes": by, "procs": procs, "round_s": rounds}))
+
+
+def cpu_baseline(rows=65536, reps=1):
+    """The oracle as it stands on the host: 1 core, and every core of the job's affinity mask
+    (one independent oracle process per core on the same sample: the oracle is single
+    threaded, so all-core throughput = cores x sample bytes / slowest process)."""
+    cores = host_cores()
+    one = oracle_timing(rows, 1, reps)
+    t1 = statistics.median(one["round_s"])
+    allc = oracle_timing(rows, cores, reps) if cores > 1 else one
+    ta = statistics.median(allc["round_s"])
+    by, n, nnz = one["bytes"], one["rows"], one["nnz"]
+    return {"value": cores * by / ta / 1e9, "unit": "GB/s", "cores": cores, "kind": "oracle",
+            "cpu_model": cpu_model(),
+            "single_core": {"value": by / t1 / 1e9, "unit": "GB/s", "cores": 1, "s_per_step": t1},
+            "all_cores": {"value": cores * by / ta / 1e9, "unit": "GB/s", "cores": cores, "s_per_step": ta},
+            "sample": f"same step on the leading {n}-row principal block of c2 ({nnz} nnz), {reps} rep(s); "
+                      f"all cores = {cores} concurrent single-threaded oracle processes (plain C, gcc -O2, + numpy "
+                      f"solver, BLAS at 1 thread), 1 core = one such process"}
 
 
 def run_reference(args):
@@ -540,27 +620,22 @@ def run_reference(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    from paper_2504_02117_b200 import perfmodel as pm
     rows = 32768
-    step, n, nnz = oracle_step_fn(rows)
-    for _ in range(args.warmup):
-        step()
-    ts = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step()
-        ts.append(time.perf_counter() - t0)
-    ms = sum(ts) / len(ts) * 1e3
-    by, _, _ = step_bytes(pm, n, nnz)
-    v = by / (ms * 1e-3) / 1e9
+    cores = host_cores()
+    r = oracle_timing(rows, cores, args.steps, args.warmup)
+    ms = statistics.mean(r["round_s"]) * 1e3
+    n, nnz = r["rows"], r["nnz"]
+    v = cores * r["bytes"] / (ms * 1e-3) / 1e9
     sample = (f"same step (bspmm/gram/update at k=1,2,4,8,16 + 5 block-BiCGStab its at k=16) on the leading "
-              f"{n}-row principal block of c2 ({nnz} nnz)")
+              f"{n}-row principal block of c2 ({nnz} nnz), run by {cores} concurrent single-threaded oracle "
+              f"processes (one per host core); step time = slowest process")
     print(json.dumps({
         "impl": "reference", "metric": "block-SpMM GB/s & GFLOP/s (fraction of HBM peak) vs k; block-Krylov solve time",
         "value": v, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": "c2" if world == 1 else f"c2-weak-{world}", "sample_rows": n},
-        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "GB/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+                         "sample": sample},
         "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
@@ -575,8 +650,13 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the c3/c4/c5 side measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-reps", type=int, default=2)
+    ap.add_argument("--cpu-reps", type=int, default=1)
+    ap.add_argument("--oracle-timing", nargs=4, type=int, metavar=("ROWS", "PROCS", "REPS", "WARMUP"),
+                    help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.oracle_timing:
+        _oracle_timing_main(*args.oracle_timing)
+        return
     if args.warmup < 3 and args.impl == "ours":
         print("note: warmup < 3 violates the timing rules; using 3", file=sys.stderr)
         args.warmup = 3

@@ -214,6 +214,10 @@ typedef struct bk_solve_report {
     int64_t n_spmm, n_gram, n_update, n_small, n_allreduce;
     double  t_class_ms[BK_NKCLASS];  /* opts->timing: summed event time per kernel class */
     int64_t n_class[BK_NKCLASS];     /* launches timed per class                        */
+    int64_t alg_bytes;        /* ALGORITHMIC bytes of every N x k pass and apply this
+                                 call enqueued (CSR streamed once, each operand read /
+                                 written once per pass): the numerator of
+                                 the solver's GB/s, counted where the passes are issued */
 } bk_solve_report;
 
 void bk_solve_opts_default(bk_solve_opts *opts);

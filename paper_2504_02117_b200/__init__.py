@@ -58,7 +58,7 @@ class SolveReport(ctypes.Structure):
                 ("true_relres", ctypes.c_double * BK_MAX_K), ("t_total_ms", ctypes.c_double),
                 ("n_spmm", ctypes.c_int64), ("n_gram", ctypes.c_int64), ("n_update", ctypes.c_int64),
                 ("n_small", ctypes.c_int64), ("n_allreduce", ctypes.c_int64),
-                ("t_class_ms", ctypes.c_double * 7), ("n_class", ctypes.c_int64 * 7)]
+                ("t_class_ms", ctypes.c_double * 7), ("n_class", ctypes.c_int64 * 7), ("alg_bytes", ctypes.c_int64)]
 
 
 class CsrInfo(ctypes.Structure):
@@ -348,7 +348,7 @@ def block_krylov_solve(ctx: Context, A: Matrix, B, X, **opts):
            "n_spmm": rep.n_spmm, "n_gram": rep.n_gram, "n_update": rep.n_update, "n_small": rep.n_small,
            "n_allreduce": rep.n_allreduce,
            "t_class_ms": {c: rep.t_class_ms[i] for i, c in enumerate(KCLASSES)},
-           "n_class": {c: rep.n_class[i] for i, c in enumerate(KCLASSES)}}
+           "n_class": {c: rep.n_class[i] for i, c in enumerate(KCLASSES)}, "alg_bytes": rep.alg_bytes}
     return st, out
 
 

@@ -460,8 +460,6 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
     if (ctx->nranks == 1 || A->n_ghost == 0) {
         a.row0 = 0;
         a.nrows = A->n_local;
-        static const int walk = env_int("BK_PIPE_WALK", 0);
-        if (walk && A->band.nbands >= 3) a.walk_line = -(int64_t)A->band.dmin[A->band.nbands / 2 - 1];
         // 3-D lattice whose z-neighbour planes do not stay in L2 across two planes of streaming
         // (c5: 512 x 512 planes): y-slab tile order.  ncu c5 k = 16: DRAM reads 20.3 -> 16.5 GB
         // (14.5 GB algorithmic); three repeated sweeps: k = 16 0.665-0.675 -> 0.693-0.717 of

@@ -60,7 +60,6 @@ struct SpmmArgs {
     double alpha, beta;
     double* Y;
     int64_t ldy;
-    int64_t walk_line;      // pipe kernel: grid line length for the y-walk tile order (0: interleaved)
     // pipe kernel, 3-D lattices: y-slab tile order (sl_S > 0): slab s of sl_L lines, then z,
     // then the line, then the x block (sl_tpl tiles per line) -- keeps the z-neighbour planes
     // of the rows in flight L2-resident when whole planes do not fit
@@ -108,9 +107,6 @@ void launch_gram_mma(int64_t n, int ka, int kb, const double* X, int64_t ldx, co
 // (strided / > 32-wide operands), the caller then uses the generic kernels.
 size_t stream_part_doubles(int num_sms);
 bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st);
-// out = a Xin + s [P_0 .. P_{np-1}] C for np <= 4 contiguous n x k arrays (block-major GMRES basis)
-bool launch_update_multi(int64_t n, int k, int np, const double* const* P, const double* C, double a,
-                         const double* Xin, double s, double* out, const int* halt, int num_sms, cudaStream_t st);
 bool launch_gram_stream(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                         double* G, double* part, int* ticket, int num_sms, cudaStream_t st);
 bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,

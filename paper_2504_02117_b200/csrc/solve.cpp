@@ -152,6 +152,9 @@ struct Solver {
             pw = vec();
             paz = vec();
         }
+        if (o->precond == BK_PRECOND_JACOBI) ab(2 * vb() + 8 * n);
+        if (o->precond == BK_PRECOND_CHEBYSHEV)
+            ab(3 * vb() + 8 * n + (int64_t)(o->cheb_steps - 1) * (spmm_b(false) + 7 * vb() + 8 * n));
         tb();
         const int r = prec_core(ctx, A, k, o, R, k, Z, k, pw, paz, &rep->n_spmm);
         te(BK_K_UPDATE);
@@ -169,13 +172,13 @@ struct Solver {
         const int maxit = o->max_iters, ce = o->check_every;
         bool graphs = o->use_graphs && !allred && !o->timing && n > 0;
         cudaGraphExec_t exec = nullptr;
-        int64_t dl = 0, dsp = 0, dgr = 0, dup = 0, dsm = 0;   // per replay: launches, counters
+        int64_t dl = 0, dsp = 0, dgr = 0, dup = 0, dsm = 0, dab = 0;   // per replay: launches, counters
         auto due = [&](int done) { return done % ce == 0 || done == maxit; };
         int it = 0, r = 0;
         while (it < maxit) {
             if (graphs && !exec && it >= period && maxit - it >= period) {
                 const int64_t l0 = g_launches.load(), s0 = rep->n_spmm, g0 = rep->n_gram, u0 = rep->n_update,
-                              m0 = rep->n_small;
+                              m0 = rep->n_small, b0 = rep->alg_bytes;
                 cudaGraph_t gph = nullptr;
                 // capture on a private non-blocking stream (the ctx stream may be the legacy
                 // default stream, which cannot be captured); replays go to the ctx stream
@@ -192,7 +195,8 @@ struct Solver {
                 dl = g_launches.load() - l0;   // captured, not launched yet
                 g_launches -= dl;
                 dsp = rep->n_spmm - s0; dgr = rep->n_gram - g0; dup = rep->n_update - u0; dsm = rep->n_small - m0;
-                rep->n_spmm = s0; rep->n_gram = g0; rep->n_update = u0; rep->n_small = m0;
+                dab = rep->alg_bytes - b0;
+                rep->n_spmm = s0; rep->n_gram = g0; rep->n_update = u0; rep->n_small = m0; rep->alg_bytes = b0;
                 if (!ok) {   // fall back to eager launches
                     if (exec) cudaGraphExecDestroy(exec);
                     exec = nullptr;
@@ -204,6 +208,7 @@ struct Solver {
             if (exec && maxit - it >= period) {
                 if ((r = cuda_check(ctx, cudaGraphLaunch(exec, st), "graph launch"))) break;
                 rep->n_spmm += dsp; rep->n_gram += dgr; rep->n_update += dup; rep->n_small += dsm;
+                rep->alg_bytes += dab;
                 g_launches += dl;
                 bool p = false;
                 for (int q = 1; q <= period; ++q) p = p || due(it + q);
@@ -225,8 +230,15 @@ struct Solver {
         return r;
     }
 
+    // algorithmic bytes of the passes this solve enqueues -> rep->alg_bytes
+    int64_t vb() const { return 8 * n * k; }
+    int64_t spmm_b(bool beta) const {
+        return 12 * A->nnz + 4 * (n + 1) + 8 * (int64_t)k * (n + A->n_ghost) + vb() * (beta ? 2 : 1);
+    }
+    void ab(int64_t b) { rep->alg_bytes += b; }
     int spmm(const double* X, int64_t ldx, double* Y, int64_t ldy, double alpha = 1.0, double beta = 0.0) {
         rep->n_spmm++;
+        ab(spmm_b(beta != 0.0));
         tb();
         const int r = spmm_dev(ctx, A, k, X, ldx, nullptr, k, alpha, beta, Y, ldy);
         te(BK_K_SPMM);
@@ -234,6 +246,7 @@ struct Solver {
     }
     int gram(const double* X, int64_t ldx, int ka, const double* Y, int64_t ldy, double* G) {
         rep->n_gram++;
+        ab(8 * n * (X == Y && ka == k ? ka : ka + k));
         if (allred) rep->n_allreduce++;
         tb();
         const int r = gram_dev(ctx, n, ka, k, X, ldx, Y, ldy, G, allred);
@@ -250,6 +263,7 @@ struct Solver {
     int coldot_(const double* X, int64_t ldx, const double* Y, int64_t ldy, const double* Y2, int64_t ldy2,
                 double* d, double* d2) {
         rep->n_gram++;
+        ab(vb() * (1 + (Y != X) + (Y2 != nullptr && Y2 != X && Y2 != Y)));
         double* part = (double*)ws_get(ctx, WS_COLDOT_PART, coldot_ws_doubles(n, k, ctx->num_sms) * sizeof(double));
         double* spart = use_stream_kernels()
                             ? (double*)ws_get(ctx, WS_COLDOT_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double))
@@ -277,6 +291,7 @@ struct Solver {
                    double* const (*blk)[2], int ndot = 0, const int (*dp)[2] = nullptr, double* const* dots = nullptr,
                    const SmallEpi* epi = nullptr, int cls = BK_K_FUSED_GRAM) {
         rep->n_gram++;
+        ab(vb() * nin);
         double* spart = (double*)ws_get(ctx, WS_GRAM_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double));
         tb();
         if (!launch_gram_multi_stream(n, k, nxa, xs, nya, ys, nin, arrays, blk, spart, ctx->d_tickets,
@@ -302,6 +317,7 @@ struct Solver {
             int64_t ldp, int kp, const double* C, const double* W = nullptr, int64_t ldw = 0, double w_host = 0.0,
             const double* w_dev = nullptr, bool halted = true) {
         rep->n_update++;
+        ab(8 * n * ((P && kp > 0 ? kp : 0) + k + (a != 0.0 && Xin ? k : 0) + (W ? k : 0)));
         UpdArgs u{};
         u.n = n; u.kp = kp; u.k = k;
         u.a = a; u.Xin = Xin; u.ldxin = ldxin;
@@ -315,6 +331,7 @@ struct Solver {
         return launched("update");
     }
     int copy(double* dst, int64_t ldd, const double* src, int64_t lds) {
+        ab(2 * vb());
         tb();
         const int r = copy_(dst, ldd, src, lds);
         te(BK_K_COPY);
@@ -428,6 +445,7 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
         S.rep->n_update += 2;
         S.rep->n_gram++;
         double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
+        S.ab(6 * S.vb());   // X, P, R, Q read; X, R written
         S.tb();
         if (!launch_cg_tail_stream(S.n, k, X, R, P, Q, al, RZn, &S.ds->halt, spart, S.ctx->d_tickets,
                                    S.ctx->num_sms, S.st, epi ? &e_be : nullptr))
@@ -558,6 +576,7 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
             S.rep->n_update += 3;
             S.rep->n_gram++;
             double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
+            S.ab(8 * S.vb());   // X, P, S, T, V read; X, R, P written
             S.tb();
             if (!launch_bcg_tail_stream(S.n, k, X, R, P, Sv, T, V, al, be, om, nr, &S.ds->halt, spart,
                                         S.ctx->d_tickets, S.ctx->num_sms, S.st, epi ? &e_cv : nullptr))
@@ -590,29 +609,12 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
 }
 
 // ---------------------------------------------------------------- O5 block GMRES(m)
-// block-major GMRES basis (V_j contiguous n x k blocks): chunk of basis blocks one
-// multi-operand Gram pass can take (the generic kernel's (row, column) block pairs; kw = 16
-// takes the panel kernel), DESIGN.md §4.2
-static int gram_chunk(int kw) {
-    for (int ch = 3; ch >= 1; --ch) {
-        if (kw == 16) return 3;
-        const int na = (ch * kw + 7) / 8, nb = (kw + 7) / 8;
-        const bool ok = nb == 1 ? (na >= 1 && na <= 3) : (na == 2 || na == 3 || na == 4 || na == 6);
-        if (ok) return ch;
-    }
-    return 1;
-}
-
 int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
     const int k = S.k, m = S.o->restart;
-    // block-major basis (opt-in, BK_GMRES_BM=1; contiguous n x k blocks: windowed applies,
-    // multi-operand Gram / update passes in chunks of 3 / 4 blocks) or one row-major
-    // n x (m+1)k array (default: the chunked passes re-read W, c3 GMRES(6) 2.11 vs 1.79 ms)
-    static const int bm_env = env_int("BK_GMRES_BM", 0);
-    const bool bm = bm_env && S.n >= 65536 && use_stream_kernels() && k % 2 == 0 && k <= 16;
-    const int64_t ldv = bm ? k : (int64_t)(m + 1) * k;
+    // basis: one row-major n x (m+1)k array, V_j = columns [jk, (j+1)k)
+    const int64_t ldv = (int64_t)(m + 1) * k;
     double* Vb = S.vec((int)((m + 1) * k));
-    auto Vblk = [&](int j) { return bm ? Vb + (int64_t)j * S.n * k : Vb + (int64_t)j * k; };
+    auto Vblk = [&](int j) { return Vb + (int64_t)j * k; };
     double* W = S.vec();
     const size_t hk = (size_t)(m + 1) * k * k;
     double* Hcol = S.small(hk);
@@ -633,48 +635,14 @@ int block_gmres(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx,
     const double tol = S.o->breakdown_tol;
     // (small systems are launch-bound: there the two-pass in-place form with one launch fewer)
     const bool small_n = S.n < 65536;
-    // [V_0 .. V_{nb-1}]^T Wm -> Hout (nb k x k), one pass per chunk of basis blocks
-    const int gch = gram_chunk(k);
+    // [V_0 .. V_{nb-1}]^T Wm -> Hout (nb k x k): one strided multi-Gram
     auto gram_basis = [&](int nb, const double* Wm, double* Hout) -> int {
-        if (!bm) return S.gram(Vb, ldv, nb * k, Wm, k, Hout);
-        for (int a0 = 0; a0 < nb; a0 += gch) {
-            const int nc = std::min(gch, nb - a0);
-            const double* arr[4];
-            int xs[3];
-            double* blk[3][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-            for (int i = 0; i < nc; ++i) {
-                arr[i] = Vblk(a0 + i);
-                xs[i] = i;
-                blk[i][0] = Hout + (int64_t)(a0 + i) * k * k;
-            }
-            arr[nc] = Wm;
-            const int ys[1] = {nc};
-            TRY(S.gram_multi(nc, xs, 1, ys, nc + 1, arr, blk, 0, nullptr, nullptr, nullptr, BK_K_GRAM));
-        }
-        return 0;
+        return S.gram(Vb, ldv, nb * k, Wm, k, Hout);
     };
-    // out = a Xin + s [V_0 .. V_{nb-1}] Hc (nb k x k), in passes of <= 4 blocks
+    // out = a Xin + s [V_0 .. V_{nb-1}] Hc (nb k x k): one strided multi-update
     auto upd_basis = [&](double* out, int64_t ldo, double a, const double* Xin, double s, int nb, const double* Hc,
                          bool halted) -> int {
-        if (!bm) return S.upd(out, ldo, a, Xin, ldo, s, Vb, ldv, nb * k, Hc, nullptr, 0, 0.0, nullptr, halted);
-        for (int a0 = 0; a0 < nb; a0 += 4) {
-            const int nc = std::min(4, nb - a0);
-            const double* P[4];
-            for (int i = 0; i < nc; ++i) P[i] = Vblk(a0 + i);
-            const double* xin = a0 == 0 ? Xin : out;
-            const double aa = a0 == 0 ? a : 1.0;
-            S.rep->n_update++;
-            S.tb();
-            const bool ok = ldo == k && launch_update_multi(S.n, k, nc, P, Hc + (int64_t)a0 * k * k, aa, xin, s, out,
-                                                            halted ? &S.ds->halt : nullptr, S.ctx->num_sms, S.st);
-            S.te(BK_K_UPDATE);
-            TRY(S.launched("update_multi"));
-            if (!ok)   // one block at a time
-                for (int i = 0; i < nc; ++i)
-                    TRY(S.upd(out, ldo, (a0 + i == 0) ? a : 1.0, (a0 + i == 0) ? Xin : out, ldo, s, Vblk(a0 + i), k, k,
-                              Hc + (int64_t)(a0 + i) * k * k, nullptr, 0, 0.0, nullptr, halted));
-        }
-        return 0;
+        return S.upd(out, ldo, a, Xin, ldo, s, Vb, ldv, nb * k, Hc, nullptr, 0, 0.0, nullptr, halted);
     };
     auto cholqr2 = [&](const double* Wm, double* Vout, double* Rprod) -> int {
         TRY(S.gram(Wm, k, k, Wm, k, G1));

@@ -9,17 +9,16 @@
 //    policy), so the matrix is read exactly once and several tiles are always
 //    in flight; eight CONSUMER warps compute tile t while t+1 lands;
 //  * a group of LANES = KP/VEC consumer threads owns one row; lane l holds
-//    columns [l*VEC, l*VEC+VEC) (VEC = 4 -> two 16-byte gathers of X per
+//    columns [l*VEC, l*VEC+VEC) (VEC = 4 -> one 256-bit gather of X per
 //    nonzero); a row's gathers are issued in batches (B*VEC = 16 doubles)
 //    before any FMA (memory-level parallelism for the L2-resident stencil
-//    neighbours).  Variants (tile kernel, stage/CTA counts, VEC, row pairing)
-//    are selectable with BK_SPMM_KERNEL / BK_SPMM_VEC for A/B runs;
+//    neighbours);
 //  * Y is written once with streaming (evict-first) stores;
 //  * the optional k x k_out coupling C is applied in the epilogue
-//    from shared memory, so the coupled apply costs no extra HBM pass.
-// A simpler one-tile-per-CTA kernel (load, sync, compute) is kept as the
-// `BK_SPMM_KERNEL=tile` variant for A/B measurements; row lists (boundary rows
-// of a partitioned matrix) use a direct, unstaged kernel.
+//    (FP64 tensor cores for k >= 8), so the coupled apply costs no extra HBM pass.
+// Band-structured matrices (stencils) take the windowed kernel (X band segments
+// staged by TMA); row lists (boundary rows of a partitioned matrix) use a
+// direct, unstaged kernel.
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
@@ -33,7 +32,6 @@ namespace {
 
 constexpr int kThreads = 256;    // consumer threads
 constexpr int kTileRows = 256;   // rows per CSR tile
-constexpr int kCap = 2304;       // staged nonzeros per tile (9 per row); larger tiles load directly
 // X gathers in flight per row and thread: B rows of X (VEC doubles each), B*VEC = 16
 template <int VEC>
 struct Batch { static constexpr int B = VEC >= 8 ? 2 : (VEC >= 4 ? 4 : 8); };
@@ -60,20 +58,6 @@ __device__ __forceinline__ void ld_x(const double* __restrict__ p, double (&x)[V
             x[t + 1] = v.y;
         }
     }
-}
-
-// streaming 16-byte load of CSR data (read once: do not pollute L1)
-__device__ __forceinline__ int4 ld_stream_i4(const int4* p) {
-    int4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ double2 ld_stream_d2(const double2* p) {
-    double2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-    return r;
 }
 
 template <int VEC>
@@ -117,49 +101,6 @@ __device__ __forceinline__ void row_accumulate(const SpmmArgs& a, const int* col
         for (int u = 0; u < kBatch; ++u)
 #pragma unroll
             for (int t = 0; t < VEC; ++t) acc[t] = fma(v[u], x[u][t], acc[t]);
-    }
-}
-
-// Two rows per thread group at once: both rows' gathers (up to B each) are in
-// flight together (memory-level parallelism at 2 columns per thread, where a
-// warp instruction covers whole 128-byte X lines).
-template <int VEC>
-__device__ __forceinline__ void row_accumulate2(const SpmmArgs& a, const int* col, const double* val, int sA, int eA,
-                                                int sB, int eB, int c0, bool lane_in, double (&accA)[VEC],
-                                                double (&accB)[VEC]) {
-    constexpr int kBatch = Batch<VEC>::B;
-    int pA = sA, pB = sB;
-    while (pA < eA || pB < eB) {
-        double xa[kBatch][VEC], xb[kBatch][VEC];
-        double va[kBatch], vb[kBatch];
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u) {
-            if (pA + u < eA && lane_in) {
-                va[u] = val[pA + u];
-                ld_x(xrow<false>(a, col[pA + u]) + c0, xa[u]);
-            } else {
-                va[u] = 0.0;
-#pragma unroll
-                for (int t = 0; t < VEC; ++t) xa[u][t] = 0.0;
-            }
-            if (pB + u < eB && lane_in) {
-                vb[u] = val[pB + u];
-                ld_x(xrow<false>(a, col[pB + u]) + c0, xb[u]);
-            } else {
-                vb[u] = 0.0;
-#pragma unroll
-                for (int t = 0; t < VEC; ++t) xb[u][t] = 0.0;
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < kBatch; ++u)
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) {
-                accA[t] = fma(va[u], xa[u][t], accA[t]);
-                accB[t] = fma(vb[u], xb[u][t], accB[t]);
-            }
-        pA += kBatch;
-        pB += kBatch;
     }
 }
 
@@ -214,28 +155,12 @@ __device__ __forceinline__ void load_C(const SpmmArgs& a, double* s_C, int tid, 
 // All passes over one tile's rows (NC consumer threads).  Called separately
 // with shared-memory and with global col/val pointers so the compiler emits
 // LDS (not generic loads) for the staged case.
-template <int KP, int VEC, bool HAS_C, int NC = kThreads, int TR = kTileRows, bool PAIR = false>
+template <int KP, int VEC, bool HAS_C, int NC = kThreads, int TR = kTileRows>
 __device__ __forceinline__ void tile_rows(const SpmmArgs& a, const int* col, const double* val, const int* s_rp,
                                           int nr, int64_t r0, int grp, int c0, bool lane_in, const double* s_C,
                                           double* t_row) {
     constexpr int RPP = NC / (KP / VEC);
     constexpr int PASSES = (TR + RPP - 1) / RPP;
-    if constexpr (PAIR) {
-        constexpr int HALF = (PASSES + 1) / 2;
-#pragma unroll 1
-        for (int pass = 0; pass < HALF; ++pass) {
-            const int r = pass * RPP + grp, r2 = (pass + HALF) * RPP + grp;
-            const bool act = r < nr, act2 = (pass + HALF < PASSES) && r2 < nr;
-            double acc[VEC], acc2[VEC];
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) { acc[t] = 0.0; acc2[t] = 0.0; }
-            row_accumulate2<VEC>(a, col, val, act ? s_rp[r] : 0, act ? s_rp[r + 1] : 0, act2 ? s_rp[r2] : 0,
-                                 act2 ? s_rp[r2 + 1] : 0, c0, lane_in, acc, acc2);
-            row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, act, r0 + r, acc);
-            row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, act2, r0 + r2, acc2);
-        }
-        return;
-    }
 #pragma unroll 1
     for (int pass = 0; pass < PASSES; ++pass) {
         const int r = pass * RPP + grp;
@@ -337,23 +262,12 @@ __device__ __forceinline__ int slab_tile(const SpmmArgs& a, int t) {
     return ((z * a.sl_ny + s * a.sl_L + yl) * a.sl_tpl) + xb;
 }
 
-template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP, bool PAIR>
+template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP>
 __global__ void __launch_bounds__(NC + 32, MINB)
-bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
+bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
     using L = PipeCfg<NC, NS, MINB, TR, CAP>;
-    // tile order: interleaved over the CTAs (walk = 0, default), or a walk along y
-    // (walk = tiles per grid line w): CTA b takes x block b % w and walks a contiguous
-    // range of lines, so the X rows of the centre / y-1 bands were gathered by its own
-    // previous tiles (L1).  w = 1 is one contiguous chunk per CTA.  (BK_PIPE_WALK /
-    // BK_PIPE_CHUNK)
-    int tb = (int)blockIdx.x, te = ntiles, tstep = (int)gridDim.x;
-    if (walk > 0) {
-        const int nl = ntiles / walk, nch = (int)gridDim.x / walk, xb = (int)blockIdx.x % walk,
-                  ch = (int)blockIdx.x / walk;
-        tb = (int)((int64_t)ch * nl / nch) * walk + xb;
-        te = (int)((int64_t)(ch + 1) * nl / nch) * walk + xb;
-        tstep = walk;
-    }
+    // tiles interleaved over the persistent CTAs (optionally permuted: slab_tile)
+    const int tb = (int)blockIdx.x, te = ntiles, tstep = (int)gridDim.x;
     constexpr int LANES = KP / VEC;
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + NS * L::STAGE_BYTES);
@@ -442,30 +356,28 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles, int walk) {
         } else if (staged) {
             const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
             const double* sval = reinterpret_cast<const double*>(st + L::RP_BYTES + L::COL_BYTES) + off - p0;
-            tile_rows<KP, VEC, HAS_C, NC, TR, PAIR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, t_row);
+            tile_rows<KP, VEC, HAS_C, NC, TR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, t_row);
         } else {
-            tile_rows<KP, VEC, HAS_C, NC, TR, PAIR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, t_row);
+            tile_rows<KP, VEC, HAS_C, NC, TR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, t_row);
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(&empty[s]);
     }
 }
 
-template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP, bool PAIR = false>
+template <int KP, int VEC, bool HAS_C, int NC, int NS, int MINB, int TR, int CAP>
 void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
     using L = PipeCfg<NC, NS, MINB, TR, CAP>;
     const int64_t ntiles = (a.nrows + TR - 1) / TR;
     const int smem = L::bytes(KP, NC / (KP / VEC), HAS_C);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR>,
+        cudaFuncSetAttribute(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
     const int64_t cap = (int64_t)MINB * num_sms;
-    int64_t grid = ntiles < cap ? ntiles : cap;
-    static const int chunked = env_int("BK_PIPE_CHUNK", 0) > 0;
-    int walk = chunked ? 1 : 0;
+    const int64_t grid = ntiles < cap ? ntiles : cap;
     SpmmArgs b = a;
     if (b.sl_S > 0) {   // slab order needs whole tiles per line and a permutation of all tiles
         const int64_t line = (int64_t)b.sl_tpl;   // (host passed the line length here)
@@ -476,60 +388,8 @@ void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
             b.sl_L = b.sl_ny / b.sl_S;
         }
     }
-    if (a.walk_line > 0 && a.walk_line % TR == 0) {   // y walk: tiles per line, whole lines only
-        const int w = (int)(a.walk_line / TR);
-        if (ntiles % w == 0 && cap >= w) {
-            walk = w;
-            grid = (cap / w) * w;
-            if (grid > ntiles) grid = ntiles;
-        }
-    }
-    BK_KERNEL(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP, PAIR><<<(unsigned)grid, NC + 32, smem, st>>>(
-        b, (int)ntiles, walk));
-}
-
-// ------------------------------------------------------------------ simple tile kernel (A/B variant)
-template <int KP, int VEC, bool HAS_C>
-__global__ void __launch_bounds__(kThreads)
-bspmm_tile_kernel(const SpmmArgs a) {
-    constexpr int LANES = KP / VEC;
-    constexpr int RPP = kThreads / LANES;
-    constexpr int PASSES = kTileRows / RPP;
-    __shared__ int32_t s_rp[kTileRows + 1];
-    __shared__ __align__(16) int32_t s_col[kCap + 8];
-    __shared__ __align__(16) double s_val[kCap + 8];
-    __shared__ double s_C[HAS_C ? KP * KP : 1];
-    __shared__ double s_t[HAS_C ? RPP * (KP + 1) : 1];
-    const int tid = threadIdx.x, grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
-    load_C<KP, HAS_C>(a, s_C, tid, kThreads);
-    const int64_t tile0 = a.row0 + (int64_t)blockIdx.x * kTileRows;
-    const int nr = (int)((a.row0 + a.nrows - tile0) < kTileRows ? (a.row0 + a.nrows - tile0) : kTileRows);
-    for (int i = tid; i <= nr; i += kThreads) s_rp[i] = a.rp[tile0 + i];
-    __syncthreads();
-    const int p0 = s_rp[0];
-    const int nnz = s_rp[nr] - p0;
-    const bool staged = nnz <= kCap;
-    const int pa = p0 & ~3;
-    const int off = p0 - pa;
-    if (staged) {
-        const int n4 = (off + nnz + 3) >> 2;
-        const int4* gc = reinterpret_cast<const int4*>(a.col + pa);
-        const double2* gv = reinterpret_cast<const double2*>(a.val + pa);
-        int4* sc = reinterpret_cast<int4*>(s_col);
-        double2* sv = reinterpret_cast<double2*>(s_val);
-        for (int i = tid; i < n4; i += kThreads) {
-            sc[i] = ld_stream_i4(gc + i);
-            sv[2 * i] = ld_stream_d2(gv + 2 * i);
-            sv[2 * i + 1] = ld_stream_d2(gv + 2 * i + 1);
-        }
-    }
-    __syncthreads();
-    const bool lane_in = c0 < a.k;
-    if (staged)
-        tile_rows<KP, VEC, HAS_C>(a, s_col + off - p0, s_val + off - p0, s_rp, nr, tile0, grp, c0, lane_in, s_C,
-                                  s_t + grp * (KP + 1));
-    else
-        tile_rows<KP, VEC, HAS_C>(a, a.col, a.val, s_rp, nr, tile0, grp, c0, lane_in, s_C, s_t + grp * (KP + 1));
+    BK_KERNEL(bspmm_pipe_kernel<KP, VEC, HAS_C, NC, NS, MINB, TR, CAP><<<(unsigned)grid, NC + 32, smem, st>>>(
+        b, (int)ntiles));
 }
 
 // ------------------------------------------------------------------ explicit row list
@@ -555,17 +415,6 @@ bspmm_rows_kernel(const SpmmArgs a) {
 }
 
 // ------------------------------------------------------------------ dispatch
-int variant() {
-    static int v = -1;
-    if (v < 0) {
-        const char* e = getenv("BK_SPMM_KERNEL");
-        // default = 3 CTAs/SM x 8 consumer warps, 2 stages, 256-row tiles (A/B: tools/ab_spmm.sh)
-        v = 0;
-        if (e && strcmp(e, "tile") == 0) v = 1;
-    }
-    return v;
-}
-
 int num_sms_cached() {
     static int n = 0;
     if (!n) {
@@ -587,13 +436,6 @@ void launch_t(const SpmmArgs& a, cudaStream_t st) {
         return;
     }
     if constexpr (!GHOST) {
-        if constexpr (!HAS_C) {   // A/B variant (static smem: uncoupled apply only)
-            if (variant() == 1) {
-                const int64_t ntiles = (a.nrows + kTileRows - 1) / kTileRows;
-                BK_KERNEL(bspmm_tile_kernel<KP, VEC, false><<<(unsigned)ntiles, kThreads, 0, st>>>(a));
-                return;
-            }
-        }
         // (round-1 A/B of ring depth / CTAs per SM / tile size: DESIGN.md §4.1)
         // (2 CTAs x 2 stages x 512-row tiles or 2 x 3 x 256 measured 15-45 % slower on c3 / c4:
         // the gathers need the third CTA's warps for latency hiding)
@@ -661,8 +503,6 @@ struct BandArgs {
     int stage_bytes, off_col, off_val, off_rp;
     int ntiles;
     int64_t ncols;      // rows of X
-    int dbg;            // diagnostics (BK_WIN_DEBUG, timing only; results invalid):
-                        // 1 consumers skip the rows, 2 only the top band is copied
 };
 constexpr int kMetaDepth = 8;   // tiles whose row-pointer bounds are in flight
 
@@ -802,7 +642,7 @@ bspmm_win_kernel(const BandArgs w) {
             for (int g = 0; g < NB; ++g) {
                 sb[g] = 0;
                 sa[g] = 0;
-                if (g < w.G && (!(w.dbg & 2) || g == w.G - 1)) {
+                if (g < w.G) {
                     const int64_t lo = r0 + w.lo[g];
                     const int64_t a0 = lo < 0 ? 0 : lo;
                     int64_t b0 = r0 + nr + w.hi[g];
@@ -815,6 +655,9 @@ bspmm_win_kernel(const BandArgs w) {
                             const double* src = a.X + (b0 - 1) * k;
                             double* d1 = dst + (b0 - 1 - a0) * k;
                             for (int t = 0; t < k; ++t) d1[t] = src[t];
+                            // generic stores into a stage that later ring phases fill
+                            // through the async proxy (cp.async.bulk): order them
+                            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                         }
                         sa[g] = a0;
                         sb[g] = b;
@@ -869,7 +712,7 @@ bspmm_win_kernel(const BandArgs w) {
             fo[g] = on ? (int)(w.wb[g] - (r0 + w.lo[g])) : 0;
         }
 #pragma unroll 1
-        for (int pass = 0; pass < (w.dbg & 1 ? 0 : passes); ++pass) {
+        for (int pass = 0; pass < passes; ++pass) {
             const int r = pass * RPP + grp;
             const bool active = r < nr;
             double acc[VEC];
@@ -938,400 +781,6 @@ bspmm_win_kernel(const BandArgs w) {
 }
 
 
-// ------------------------------------------------------------------ rolling-window apply (lattice stencils)
-// DESIGN.md §4.1.  For a band plan with lattice structure (2-D: bands -nx, [-1,1], +nx;
-// 3-D: also -+nx*ny) the row range is a grid of lines; a tile is Tx consecutive rows of
-// one line, and each CTA walks SEQUENCES of tiles along y (fixed x block, z).  The
-// X rows of lines y-1, y, y+1 (Tx + 4 rows each) stay in a shared-memory RUN RING:
-// each tile loads only line y+1 (three at a sequence start), so every X row comes
-// from L2 about once (2-D; the band kernel fetched it once per band) -- plus, in
-// 3-D, the lines z-1, z+1 of the tile ("side runs").  The consumers are the band
-// kernel's: the window element of column c is (c - r0) k + H_g + c0 for the band g
-// picked by c - r0 >= lo_g, with H_g (per tile, from the stage header) pointing
-// into the run ring / the stage's side runs.
-struct RollArgs {
-    SpmmArgs a;
-    int G;
-    int lo[BK_BAND_MAX];     // band select thresholds (relative to the tile's first row)
-    int sg[BK_BAND_MAX];     // band offset: 0 (centre), +-s1, +-s2
-    int role[BK_BAND_MAX];   // 0 centre run, -1/+1 rolling run y-1/y+1, -2/+2 side run z-1/z+1
-    int nx, ny, nz;          // lattice: row = row0 + (z ny + y) nx + x
-    int Tx, Ly, nxb, nyseg, nseq;
-    int ns, rr;              // stages, run-ring slots
-    int run_dbl;             // doubles per run buffer
-    int stage_bytes, off_side, off_col, off_val, off_rp;   // stage: H header | side runs | col | val | rp
-    int ring_off;            // byte offset of the run ring
-    int cap;                 // staged nonzeros per tile
-};
-
-template <int VEC, int NB, int MR>
-__device__ __forceinline__ void roll_accumulate(const double* sm, const int* col, const double* val, int s, int e,
-                                               int r0, const int (&lo)[NB], const int (&H)[NB], int kk, int c0,
-                                               int sw, double (&acc)[VEC]) {
-    constexpr int B = MR > 0 ? MR : 4;
-    for (int p = s; p < e; p += B) {
-        double x[B][VEC];
-        double v[B];
-#pragma unroll
-        for (int u = 0; u < B; ++u) {
-            const int q = (p + u < e) ? p + u : e - 1;
-            const int cl = col[q] - r0;
-            v[u] = (p + u < e) ? val[q] : 0.0;
-            int h = H[0];
-#pragma unroll
-            for (int g = 1; g < NB; ++g) h = (cl >= lo[g]) ? H[g] : h;
-            win_load<VEC>(sm + (cl * kk + h + c0), sw, x[u]);
-        }
-#pragma unroll
-        for (int u = 0; u < B; ++u)
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) acc[t] = fma(v[u], x[u][t], acc[t]);
-        if constexpr (MR > 0) break;
-    }
-    if constexpr (VEC == 4) {
-        if (sw) {
-            const double t0 = acc[0], t1 = acc[1];
-            acc[0] = acc[2]; acc[1] = acc[3]; acc[2] = t0; acc[3] = t1;
-        }
-    }
-}
-
-// (sequence, line) iterator shared by the producer, its row-pointer prefetch and the consumers
-struct RollIt {
-    int seq, y, yb;
-    int64_t lbase;   // first row of line (y, z) relative to row0, plus x0
-    int z, x0, ya;
-    __device__ __forceinline__ void start(const RollArgs& w, int q) {
-        seq = q;
-        if (q >= w.nseq) return;
-        const int xb = q % w.nxb, rest = q / w.nxb;
-        const int ys = rest % w.nyseg;
-        z = rest / w.nyseg;
-        x0 = xb * w.Tx;
-        ya = ys * w.Ly;
-        y = ya;
-        yb = min(ya + w.Ly, w.ny);
-    }
-    __device__ __forceinline__ bool valid(const RollArgs& w) const { return seq < w.nseq; }
-    __device__ __forceinline__ int64_t r0(const RollArgs& w) const {
-        return w.a.row0 + ((int64_t)z * w.ny + y) * w.nx + x0;
-    }
-    __device__ __forceinline__ void next(const RollArgs& w) {
-        if (++y >= yb) start(w, seq + gridDim.x);
-    }
-};
-
-template <int KP, int VEC, bool HAS_C, int NC, int NB, int MR, bool KEXACT>
-__global__ void __launch_bounds__(NC + 32, 2)
-bspmm_roll_kernel(const RollArgs w) {
-    const SpmmArgs& a = w.a;
-    constexpr int LANES = KP / VEC;
-    constexpr int RPP = NC / LANES;
-    extern __shared__ __align__(128) unsigned char smem[];
-    const int fixed_off = w.ring_off + w.rr * w.run_dbl * 8;
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + fixed_off);
-    uint64_t* empty = full + 8;
-    int2* s_pp = reinterpret_cast<int2*>(empty + 8);
-    double* s_C = reinterpret_cast<double*>(s_pp + kMetaDepth);
-    double* s_t = s_C + KP * KP;
-    const int tid = threadIdx.x, warp = tid >> 5, lane32 = tid & 31;
-    if (tid == 0) {
-        for (int s = 0; s < w.ns; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], NC / 32);
-        }
-        mbar_fence_init();
-    }
-    if (tid < NC) load_C<KP, HAS_C>(a, s_C, tid, NC);
-    __syncthreads();
-    const int k = a.k;
-    const double* ring = reinterpret_cast<const double*>(smem + w.ring_off);
-    if (warp == NC / 32) {
-        // ------------------------------------------------ producer (one thread)
-        if (lane32 != 0) return;
-        const uint64_t pol_once = evict_first_policy();
-        const uint64_t pol_x = evict_normal_policy();
-        const uint32_t kb = (uint32_t)k * 8u;
-        const int Tx = w.Tx;
-        // row-pointer bounds kMetaDepth tiles ahead (look-ahead iterator)
-        RollIt la;
-        la.start(w, blockIdx.x);
-        int lcount = 0;
-        auto fetch = [&]() {
-            if (la.valid(w)) {
-                const int64_t r0 = la.r0(w);
-                const uint32_t dst = smem_u32(s_pp + (lcount % kMetaDepth));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst), "l"(a.rp + r0) : "memory");
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(dst + 4), "l"(a.rp + r0 + Tx) : "memory");
-                la.next(w);
-            }
-            asm volatile("cp.async.commit_group;" ::: "memory");
-            ++lcount;
-        };
-        for (int d = 0; d < kMetaDepth; ++d) fetch();
-        // one run (line yl, zl) into ring slot / side buffer `dst` (row 0 = X row of x0 - 2)
-        // a run exists if its line is inside the lattice in y and its X rows inside X: the
-        // planes z = -1 / nz of an interior row range are the (local) boundary planes
-        auto run_ok = [&](int yl, int zl) -> bool {
-            if (yl < 0 || yl >= w.ny) return false;
-            const int64_t first = a.row0 + ((int64_t)zl * w.ny + yl) * w.nx;
-            return first >= 0 && first + w.nx <= (int64_t)a.ncol_local;
-        };
-        auto run_bytes = [&](int yl, int zl, int x0) -> uint32_t {
-            if (!run_ok(yl, zl)) return 0u;
-            const int xs = max(x0 - 2, 0), xe = min(x0 + Tx + 2, w.nx);
-            return (uint32_t)(xe - xs) * kb;
-        };
-        auto run_copy = [&](int yl, int zl, int x0, double* dst, uint64_t* bar) {
-            if (!run_ok(yl, zl)) return;
-            const int xs = max(x0 - 2, 0), xe = min(x0 + Tx + 2, w.nx);
-            const int64_t src = a.row0 + ((int64_t)zl * w.ny + yl) * w.nx + xs;
-            bulk_g2s(dst + (int64_t)(xs - (x0 - 2)) * k, a.X + src * k, (uint32_t)(xe - xs) * kb, bar, pol_x);
-        };
-        RollIt it;
-        it.start(w, blockIdx.x);
-        int s = 0, i = 0, next_slot = 0;
-        uint32_t ph = 0;
-        int slot_m = -1, slot_c = -1, slot_p = -1;   // ring slots of lines y-1, y, y+1
-        while (it.valid(w)) {
-            asm volatile("cp.async.wait_group %0;" ::"n"(kMetaDepth - 1) : "memory");
-            const int2 pp = s_pp[i % kMetaDepth];
-            fetch();
-            if (i >= w.ns) mbar_wait(&empty[s], ph ^ 1u);
-            unsigned char* st = smem + s * w.stage_bytes;
-            const int64_t r0 = it.r0(w);
-            const int p0 = pp.x, p1 = pp.y;
-            const int64_t ra = r0 & ~(int64_t)3;
-            const uint32_t rp_bytes = (uint32_t)((((r0 - ra) + Tx + 1 + 3) & ~3) * 4);
-            const int pc = p0 & ~3, pv = p0 & ~1;
-            const uint32_t col_bytes = p1 > p0 ? (uint32_t)(((p1 - pc + 3) & ~3) * 4) : 0u;
-            const uint32_t val_bytes = p1 > p0 ? (uint32_t)(((p1 - pv + 1) & ~1) * 8) : 0u;
-            // run ring: a new sequence loads lines y-1, y, y+1; later tiles only y+1
-            const bool fresh = it.y == it.ya;
-            int new_m = slot_m, new_c = slot_c, new_p;
-            uint32_t bytes = rp_bytes + col_bytes + val_bytes;
-            if (fresh) {
-                new_m = next_slot; next_slot = (next_slot + 1) % w.rr;
-                new_c = next_slot; next_slot = (next_slot + 1) % w.rr;
-                bytes += run_bytes(it.y - 1, it.z, it.x0) + run_bytes(it.y, it.z, it.x0);
-            } else {
-                new_m = slot_c;
-                new_c = slot_p;
-            }
-            new_p = next_slot; next_slot = (next_slot + 1) % w.rr;
-            bytes += run_bytes(it.y + 1, it.z, it.x0);
-            double* side = reinterpret_cast<double*>(st + w.off_side);
-            bool has_side = false;
-#pragma unroll
-            for (int g = 0; g < NB; ++g)
-                if (g < w.G && (w.role[g] == -2 || w.role[g] == 2)) has_side = true;
-            if (has_side) bytes += run_bytes(it.y, it.z - 1, it.x0) + run_bytes(it.y, it.z + 1, it.x0);
-            // header: H_g = (buffer start in doubles) - (s_g - 2) k
-            int* hdr = reinterpret_cast<int*>(st);
-            const int ring_dbl = w.ring_off / 8;
-#pragma unroll
-            for (int g = 0; g < NB; ++g) {
-                if (g >= w.G) break;
-                int base;
-                switch (w.role[g]) {
-                    case -1: base = ring_dbl + new_m * w.run_dbl; break;
-                    case 1: base = ring_dbl + new_p * w.run_dbl; break;
-                    case -2: base = (s * w.stage_bytes + w.off_side) / 8; break;
-                    case 2: base = (s * w.stage_bytes + w.off_side) / 8 + w.run_dbl; break;
-                    default: base = ring_dbl + new_c * w.run_dbl; break;
-                }
-                hdr[g] = base - (w.sg[g] - 2) * k;
-            }
-            mbar_expect_tx(&full[s], bytes);
-            bulk_g2s(st + w.off_rp, a.rp + ra, rp_bytes, &full[s], pol_once);
-            if (col_bytes) {
-                bulk_g2s(st + w.off_col, a.col + pc, col_bytes, &full[s], pol_once);
-                bulk_g2s(st + w.off_val, a.val + pv, val_bytes, &full[s], pol_once);
-            }
-            double* rg = const_cast<double*>(ring);
-            if (fresh) {
-                run_copy(it.y - 1, it.z, it.x0, rg + (int64_t)new_m * w.run_dbl, &full[s]);
-                run_copy(it.y, it.z, it.x0, rg + (int64_t)new_c * w.run_dbl, &full[s]);
-            }
-            run_copy(it.y + 1, it.z, it.x0, rg + (int64_t)new_p * w.run_dbl, &full[s]);
-            if (has_side) {
-                run_copy(it.y, it.z - 1, it.x0, side, &full[s]);
-                run_copy(it.y, it.z + 1, it.x0, side + w.run_dbl, &full[s]);
-            }
-            slot_m = new_m; slot_c = new_c; slot_p = new_p;
-            ++i;
-            if (++s == w.ns) { s = 0; ph ^= 1u; }
-            it.next(w);
-        }
-        asm volatile("cp.async.wait_group 0;" ::: "memory");
-        return;
-    }
-    // ---------------------------------------------------- consumer warps
-    const int grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
-    const int kk = KEXACT ? KP : k;
-    double* t_row = s_t + grp * (KP + 1);
-    const int passes = (w.Tx + RPP - 1) / RPP;
-    const double* sm = reinterpret_cast<const double*>(smem);
-    int lo[NB];
-#pragma unroll
-    for (int g = 0; g < NB; ++g) lo[g] = g < w.G ? w.lo[g] : INT_MAX;
-    RollIt it;
-    it.start(w, blockIdx.x);
-    int s = 0;
-    uint32_t ph = 0;
-    while (it.valid(w)) {
-        mbar_wait(&full[s], ph);
-        const unsigned char* st = smem + s * w.stage_bytes;
-        const int64_t r0 = it.r0(w);
-        const int* s_rp = reinterpret_cast<const int*>(st + w.off_rp) + (int)(r0 & 3);
-        const int p0 = s_rp[0];
-        const int* scol = reinterpret_cast<const int*>(st + w.off_col) + (p0 & 3) - p0;
-        const double* sval = reinterpret_cast<const double*>(st + w.off_val) + (p0 & 1) - p0;
-        int H[NB];
-        const int* hdr = reinterpret_cast<const int*>(st);
-#pragma unroll
-        for (int g = 0; g < NB; ++g) H[g] = g < w.G ? hdr[g] : 0;
-#pragma unroll 1
-        for (int pass = 0; pass < passes; ++pass) {
-            const int r = pass * RPP + grp;
-            const bool active = r < w.Tx;
-            double acc[VEC];
-#pragma unroll
-            for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
-            if (active) {
-                const int rs = s_rp[r], re = s_rp[r + 1];
-                if (re > rs) {
-                    const int gr = (int)(r0 + r);
-                    const int sw = (kk <= 16) ? (((gr * kk) >> 4) & 1) : (gr & 1);
-                    roll_accumulate<VEC, NB, MR>(sm, scol, sval, rs, re, (int)r0, lo, H, kk, c0, sw, acc);
-                }
-            }
-            row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
-        }
-        __syncwarp();
-        if (lane32 == 0) mbar_arrive(&empty[s]);
-        if (++s == w.ns) { s = 0; ph ^= 1u; }
-        it.next(w);
-    }
-}
-
-// Lattice of a band plan (2-D: bands {-s1}, centre within [-1,1], {+s1}; 3-D: also {-s2}, {+s2}
-// with s1 | s2) over nrows rows; false if the bands do not have that shape.
-bool roll_lattice(const BandPlan& p, int64_t nrows, int& nx, int& ny, int& nz, int64_t& s1, int64_t& s2) {
-    const int G = p.nbands;
-    if (G != 3 && G != 5) return false;
-    const int gc = G / 2;
-    if (p.dmin[gc] < -1 || p.dmax[gc] > 1 || p.dmin[gc] > 0 || p.dmax[gc] < 0) return false;
-    for (int g = 0; g < G; ++g)
-        if (g != gc && p.dmin[g] != p.dmax[g]) return false;
-    s1 = p.dmin[gc + 1];
-    if (p.dmin[gc - 1] != -s1 || s1 < 16) return false;
-    if (G == 5) {
-        s2 = p.dmin[gc + 2];
-        if (p.dmin[gc - 2] != -s2 || s2 % s1 != 0 || nrows % s2 != 0) return false;
-        nx = (int)s1;
-        ny = (int)(s2 / s1);
-        nz = (int)(nrows / s2);
-    } else {
-        s2 = 0;
-        if (nrows % s1 != 0) return false;
-        nx = (int)s1;
-        ny = (int)(nrows / s1);
-        nz = 1;
-    }
-    return nx % 2 == 0 && ny >= 1 && nz >= 1;
-}
-
-// Opt-in (BK_SPMM_ROLL=1): correct (tests force it) but measured slower than the band
-// kernel -- one producer thread spends ~1 us per tile (~350 instructions) and 3-D rings
-// fit only one CTA per SM (c2 k=16: 76 vs 68 us; profiles/r01_summary.md).
-bool roll_enabled() {
-    static const int v = env_int("BK_SPMM_ROLL", 0);
-    return v != 0;
-}
-
-template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT>
-bool launch_roll_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
-    constexpr int NC = 256;
-    constexpr int LANES = KP / VEC;
-    constexpr int RPP = NC / LANES;
-    int nx, ny, nz;
-    int64_t s1, s2;
-    if (!roll_lattice(p, a.nrows, nx, ny, nz, s1, s2)) return false;
-    RollArgs w{};
-    w.a = a;
-    w.G = p.nbands;
-    w.nx = nx; w.ny = ny; w.nz = nz;
-    const int gc = w.G / 2;
-    for (int g = 0; g < w.G; ++g) {
-        w.lo[g] = p.lo[g];
-        w.sg[g] = g == gc ? 0 : p.dmin[g];
-        w.role[g] = g == gc ? 0 : (g == gc - 1 ? -1 : (g == gc + 1 ? 1 : (g < gc ? -2 : 2)));
-    }
-    // tile: Tx rows of one line, Tx | nx, Tx <= RPP (one pass), s1 >= Tx + 6 (bands separable)
-    static const int tx_env = env_int("BK_ROLL_TX", 0);
-    int Tx = tx_env > 0 ? tx_env : RPP;
-    while (Tx > 8 && (nx % Tx != 0 || nx < Tx + 6)) Tx /= 2;
-    if (Tx < 8 || nx % Tx != 0 || nx < Tx + 6 || Tx * LANES < 64) return false;
-    w.Tx = Tx;
-    w.nxb = nx / Tx;
-    // sequences of Ly lines: >= 8 lines (run-ring reuse bound), about 16 sequences per SM
-    const int nsm = num_sms_cached();
-    const int64_t want = 16ll * nsm;
-    const int64_t cols = (int64_t)w.nxb * nz;
-    const int lwant = (int)std::max<int64_t>(8, (cols * ny + want - 1) / want);
-    const int nyseg = std::max(1, ny / lwant);          // balanced segments, each >= lwant lines
-    w.Ly = (ny + nyseg - 1) / nyseg;
-    w.nyseg = (ny + w.Ly - 1) / w.Ly;
-    const int64_t nseq = cols * w.nyseg;
-    if (nseq >= (1ll << 31)) return false;
-    w.nseq = (int)nseq;
-    // shared memory: stages (header | side runs | col | val | rp) + run ring
-    auto r16 = [](int64_t x) { return (x + 15) & ~(int64_t)15; };
-    w.run_dbl = (int)(r16((int64_t)(Tx + 4) * a.k * 8) / 8);
-    w.cap = Tx * p.max_row_nnz;
-    const bool side = w.G == 5;
-    w.off_side = 128;
-    w.off_col = w.off_side + (side ? 2 * w.run_dbl * 8 : 0);
-    w.off_val = w.off_col + (int)r16((int64_t)(w.cap + 4) * 4);
-    w.off_rp = w.off_val + (int)r16((int64_t)(w.cap + 2) * 8);
-    w.stage_bytes = (int)((w.off_rp + r16((Tx + 8) * 4) + 127) & ~(int64_t)127);
-    const int fixed = 16 * 8 + kMetaDepth * 8 + (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
-    // run ring: the producer at tile t reuses slots only after tiles <= t - ns are consumed;
-    // the unconsumed tiles reference runs loaded by tiles t - ns - 1 .. t (1 per tile, 3 at
-    // a sequence start, at most one start per ns + 2 <= 8 tiles when sequences have >= 8
-    // lines): ns + 4 slots, else 3 (ns + 2)
-    const int min_len = ny / w.nyseg;
-    auto ring_slots = [&](int n) { return (min_len >= 8 && n + 2 <= min_len) ? n + 4 : 3 * (n + 2); };
-    auto need = [&](int n) { return (int64_t)n * w.stage_bytes + (int64_t)ring_slots(n) * w.run_dbl * 8; };
-    // two CTAs per SM (two producer threads: the single producer's ~1 us per tile is the
-    // limit otherwise) when >= 3 stages fit in half the shared memory
-    static const int ctas_env = env_int("BK_ROLL_CTAS", 0);
-    int ctas = 0, ns = 0;
-    for (int c = (ctas_env ? ctas_env : 2); c >= 1 && !ctas; --c) {
-        const int budget = (c == 2 ? 113 * 1024 : 227 * 1024) - fixed;
-        int n = 6;
-        while (n > 2 && need(n) > budget) --n;
-        if (need(n) <= budget && (n >= 3 || c == 1)) { ctas = c; ns = n; }
-        if (ctas_env) break;
-    }
-    if (!ctas) return false;
-    w.ns = ns;
-    w.rr = ring_slots(ns);
-    w.ring_off = ns * w.stage_bytes;
-    const int smem = (int)need(ns) + fixed;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(bspmm_roll_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
-    }
-    const int grid = (int)std::min<int64_t>(nseq, (int64_t)ctas * nsm);
-    BK_KERNEL(bspmm_roll_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT><<<grid, NC + 32, smem, st>>>(w));
-    return true;
-}
-
-
 template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT, int NC>
 bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int ctas, bool big_tiles = true) {
     constexpr int LANES = KP / VEC;
@@ -1395,8 +844,6 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     if (ntiles >= (1ll << 31)) return false;
     w.ntiles = (int)ntiles;
     w.ncols = a.ncol_local;
-    static const int dbg = env_int("BK_WIN_DEBUG", 0);
-    w.dbg = dbg;
     const int smem = ns * w.stage_bytes + fixed;
     static bool attr = false;
     if (!attr) {
@@ -1438,13 +885,6 @@ bool launch_win_shape(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
 
 template <int KP, int VEC, bool HAS_C, int NB, int MR>
 bool launch_win_ke(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
-    if constexpr (NB == 3 || NB == 5) {   // lattice stencils: rolling window (X rows reused across tiles)
-        if (roll_enabled() && !(HAS_C && KP >= 8 && VEC == 4)) {
-            const bool ok = a.k == KP ? launch_roll_t<KP, VEC, HAS_C, NB, MR, true>(a, p, st)
-                                      : launch_roll_t<KP, VEC, HAS_C, NB, MR, false>(a, p, st);
-            if (ok) return true;
-        }
-    }
     return a.k == KP ? launch_win_shape<KP, VEC, HAS_C, NB, MR, true>(a, p, st)
                      : launch_win_shape<KP, VEC, HAS_C, NB, MR, false>(a, p, st);
 }

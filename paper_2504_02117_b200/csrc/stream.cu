@@ -89,8 +89,6 @@ struct UpdStream {
     Streams S;          // 0 = P (kp), 1 = Xin (k, if a != 0), 2 = W (k, if present)
     int iX, iW;         // stream index of Xin / W, -1 if absent
     int iP;             // stream index of P (-1 when kp == 0: out = a Xin + w W)
-    int np;             // P arrays: 1, or 2..4 arrays of k columns at iP .. iP+np-1 whose
-                        // concatenation is the kp = np k wide P (block-major GMRES basis)
     int kp, k, cw;      // cw = columns per thread (1, 2 or 4)
     double a, s, w_host;
     const double* w_dev;
@@ -100,46 +98,28 @@ struct UpdStream {
     const int* halt;
 };
 
-// row-0 pointers of the P operand for one tile: staged (stage base st) or global (direct);
-// one array: Pa[i] = P + 8 i (so Pa[ia][r kp + 4 ks - 8 ia ...] is column 4 ks of row r);
-// np arrays: Pa[i] = array i
-__device__ __forceinline__ void p_rows(const UpdStream& U, const unsigned char* st, int64_t r0, bool direct,
-                                       const double* (&Pa)[4]) {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) Pa[i] = nullptr;
-    if (U.iP < 0) return;
-    if (U.np > 1) {
-#pragma unroll
-        for (int i = 0; i < 4; ++i)
-            if (i < U.np)
-                Pa[i] = direct ? U.S.p[U.iP + i] + r0 * U.k
-                               : reinterpret_cast<const double*>(st + U.S.off[U.iP + i]);
-    } else {
-        const double* P0 = direct ? U.S.p[U.iP] + r0 * U.kp : reinterpret_cast<const double*>(st + U.S.off[U.iP]);
-        const int k8 = 8 * ((U.k + 7) / 8);
-#pragma unroll
-        for (int i = 0; i < 4; ++i) Pa[i] = P0 + i * k8;
-    }
+// row-0 pointer of the P operand for one tile: staged (stage base st) or global (direct)
+__device__ __forceinline__ const double* p_rows(const UpdStream& U, const unsigned char* st, int64_t r0, bool direct) {
+    if (U.iP < 0) return nullptr;
+    return direct ? U.S.p[U.iP] + r0 * U.kp : reinterpret_cast<const double*>(st + U.S.off[U.iP]);
 }
 
 template <int CW>
-__device__ __forceinline__ void upd_tile(const UpdStream& U, const double* const (&Pa)[4], const double* Xt,
+__device__ __forceinline__ void upd_tile(const UpdStream& U, const double* Pt, const double* Xt,
                                          const double* Wt, const double* sC, int nr, int64_t r0, double wv) {
     const int k = U.k, kp = U.kp;
     const int tpr = k / CW;
-    const int npl = U.np > 1 ? U.np : 1, qn = U.np > 1 ? k : kp;   // P arrays, columns of each
     for (int idx = threadIdx.x; idx < nr * tpr; idx += NC) {
         const int r = idx / tpr, cb = (idx - r * tpr) * CW;
         double acc[CW];
 #pragma unroll
         for (int j = 0; j < CW; ++j) acc[j] = 0.0;
-        for (int ia = 0; ia < npl; ++ia) {
-            const double* pr = (ia == 0 ? Pa[0] : ia == 1 ? Pa[1] : ia == 2 ? Pa[2] : Pa[3]) + (int64_t)r * qn;
-            const double* cr = sC + ia * qn * k;
-            for (int q = 0; q < qn; ++q) {
+        if (Pt) {
+            const double* pr = Pt + (int64_t)r * kp;
+            for (int q = 0; q < kp; ++q) {
                 const double p = pr[q];
 #pragma unroll
-                for (int j = 0; j < CW; ++j) acc[j] = fma(p, cr[q * k + cb + j], acc[j]);
+                for (int j = 0; j < CW; ++j) acc[j] = fma(p, sC[q * k + cb + j], acc[j]);
             }
         }
         double o[CW];
@@ -166,25 +146,18 @@ __device__ __forceinline__ void upd_tile(const UpdStream& U, const double* const
 // fragments (m8n8k4: lane holds P[row 4g+.., q]), s C as B fragments held in
 // registers for the whole kernel.  Needs k % 8 == 0 and kp % 4 == 0.
 template <int NQ, int NK>
-__device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* const (&Pa)[4], const double* Xt,
+__device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* Pt, const double* Xt,
                                              const double* Wt, const double (&bf)[NQ][NK], int nr, int64_t r0,
                                              double wv) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int kq = lane & 3, mg = lane >> 2;
-    const int k = U.k;
-    constexpr int K8 = 8 * NK;   // == k on this path
-    // column 4 ks + kq of the (virtual) P row: array ia = 4 ks / K8 (compile time), row stride
-    // kp (one array; Pa[ia] = P + ia K8) or K8 (np arrays of k columns)
-    const int prs = U.np > 1 ? K8 : U.kp;
+    const int k = U.k, kp = U.kp;
     for (int rb = 8 * warp; rb < nr; rb += 8 * (NC / 32)) {
         const int r = rb + mg;
         const bool rin = r < nr;
         double af[NQ];
 #pragma unroll
-        for (int ks = 0; ks < NQ; ++ks) {
-            const int ia = (4 * ks) / K8;
-            af[ks] = rin ? Pa[ia][(int64_t)r * prs + (4 * ks - ia * K8) + kq] : 0.0;
-        }
+        for (int ks = 0; ks < NQ; ++ks) af[ks] = rin ? Pt[(int64_t)r * kp + 4 * ks + kq] : 0.0;
 #pragma unroll
         for (int nb = 0; nb < NK; ++nb) {
             const int c = 8 * nb + 2 * kq;
@@ -240,17 +213,13 @@ __global__ void __launch_bounds__(NC + 32, 2) upd_stream_mma_kernel(const UpdStr
         const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
         if (!s_direct[s]) {
             const unsigned char* st = smem + s * STAGE_BYTES;
-            const double* Pa[4];
-            p_rows(U, st, r0, false, Pa);
             const double* Xt = U.iX >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iX]) : nullptr;
             const double* Wt = U.iW >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iW]) : nullptr;
-            upd_tile_mma<NQ, NK>(U, Pa, Xt, Wt, bf, nr, r0, wv);
+            upd_tile_mma<NQ, NK>(U, p_rows(U, st, r0, false), Xt, Wt, bf, nr, r0, wv);
         } else {
-            const double* Pa[4];
-            p_rows(U, nullptr, r0, true, Pa);
             const double* Xt = U.iX >= 0 ? U.S.p[U.iX] + r0 * U.k : nullptr;
             const double* Wt = U.iW >= 0 ? U.S.p[U.iW] + r0 * U.k : nullptr;
-            upd_tile_mma<NQ, NK>(U, Pa, Xt, Wt, bf, nr, r0, wv);
+            upd_tile_mma<NQ, NK>(U, p_rows(U, nullptr, r0, true), Xt, Wt, bf, nr, r0, wv);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -282,17 +251,13 @@ __global__ void __launch_bounds__(NC + 32, 2) upd_stream_kernel(const UpdStream 
         const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
         if (!s_direct[s]) {
             const unsigned char* st = smem + s * STAGE_BYTES;
-            const double* Pa[4];
-            p_rows(U, st, r0, false, Pa);
             const double* Xt = U.iX >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iX]) : nullptr;
             const double* Wt = U.iW >= 0 ? reinterpret_cast<const double*>(st + U.S.off[U.iW]) : nullptr;
-            upd_tile<CW>(U, Pa, Xt, Wt, sC, nr, r0, wv);
+            upd_tile<CW>(U, p_rows(U, st, r0, false), Xt, Wt, sC, nr, r0, wv);
         } else {
-            const double* Pa[4];
-            p_rows(U, nullptr, r0, true, Pa);
             const double* Xt = U.iX >= 0 ? U.S.p[U.iX] + r0 * U.k : nullptr;
             const double* Wt = U.iW >= 0 ? U.S.p[U.iW] + r0 * U.k : nullptr;
-            upd_tile<CW>(U, Pa, Xt, Wt, sC, nr, r0, wv);
+            upd_tile<CW>(U, p_rows(U, nullptr, r0, true), Xt, Wt, sC, nr, r0, wv);
         }
         __syncwarp();
         if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
@@ -304,6 +269,7 @@ struct GramStream {
     Streams S;          // 0 = X (ka), 1 = Y (kb) (absent when X == Y), 2 = Y2 for coldot
     int ka, kb;
     int same;           // Y == X
+    int y2x;            // coldot: Y2 == X (read from X's tile, not streamed twice)
     double* part;       // [gridDim.x][NOUT]
     int* ticket;
     double* G;          // gram: ka x kb; coldot: d[k]
@@ -606,7 +572,9 @@ __global__ void __launch_bounds__(NC + 32, 2) coldot_stream_kernel(const GramStr
         const bool dir = s_direct[s] != 0;
         const double* Xt = dir ? Gs.S.p[0] + r0 * k : reinterpret_cast<const double*>(st + Gs.S.off[0]);
         const double* Yt = Gs.same ? Xt : (dir ? Gs.S.p[1] + r0 * k : reinterpret_cast<const double*>(st + Gs.S.off[1]));
-        const double* Y2t = two ? (dir ? Gs.S.p[2] + r0 * k : reinterpret_cast<const double*>(st + Gs.S.off[2])) : nullptr;
+        const double* Y2t = !two ? nullptr
+                            : Gs.y2x ? Xt
+                                     : (dir ? Gs.S.p[2] + r0 * k : reinterpret_cast<const double*>(st + Gs.S.off[2]));
         if (flat) {
             const int ne = nr * k;
             for (int e = threadIdx.x; e < ne; e += NC) {
@@ -1142,6 +1110,9 @@ __global__ void __launch_bounds__(NC + 32, 2) cg_tail_stream_kernel(const CgTail
             }
             __syncwarp();
         }
+        // the new R rows went into the stage with generic stores; the producer's next bulk
+        // copy into this stage is an async-proxy write: order them (PTX memory model)
+        if (!dir) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -1189,56 +1160,6 @@ size_t stream_part_doubles(int num_sms) { return (size_t)(2 * num_sms + 40) * 20
 
 static void stream_geom(Streams& S, int nin, int64_t n);
 
-// out = a Xin + s [P_0 .. P_{np-1}] C, np <= 4 contiguous n x k arrays (C: np k x k row-major),
-// Xin contiguous (may be out), out contiguous; false = not applicable
-bool launch_update_multi(int64_t n, int k, int np, const double* const* P, const double* C, double a,
-                         const double* Xin, double s, double* out, const int* halt, int num_sms, cudaStream_t st) {
-    if (n <= 0 || np < 1 || np > 4 || k < 1 || k > 32 || np * k * k > 1024) return false;
-    if ((uintptr_t)out & 15) return false;
-    UpdStream U{};
-    int nin = 0;
-    U.iP = 0;
-    for (int i = 0; i < np; ++i) {
-        if (((uintptr_t)P[i] & 15) || (const double*)out == P[i]) return false;
-        U.S.p[nin] = P[i]; U.S.w[nin] = k; ++nin;
-    }
-    U.iX = -1; U.iW = -1;
-    if (a != 0.0) {
-        if (!Xin || ((uintptr_t)Xin & 15)) return false;
-        U.iX = nin; U.S.p[nin] = Xin; U.S.w[nin] = k; ++nin;
-    }
-    stream_geom(U.S, nin, n);
-    U.np = np; U.kp = np * k; U.k = k; U.cw = (k % 4 == 0) ? 4 : ((k % 2 == 0) ? 2 : 1);
-    U.a = a; U.s = s; U.w_host = 0.0; U.w_dev = nullptr;
-    U.C = C; U.out = out; U.ldo = k; U.halt = halt;
-    const int smem = NSTAGE * STAGE_BYTES + 128 + 32 * 32 * 8;
-    const int grid = grid_for(U.S.ntiles, num_sms);
-    if (k % 8 == 0 && np * k <= 32) {   // DMMA: the np arrays feed consecutive K steps
-        const int nq = np * k / 4, nk = k / 8;
-#define BK_UMM(Q, K)                                                                           \
-    if (nq == Q && nk == K) {                                                                  \
-        static bool at = false;                                                                \
-        if (!at) { set_smem((const void*)upd_stream_mma_kernel<Q, K>, smem); at = true; }       \
-        BK_KERNEL(upd_stream_mma_kernel<Q, K><<<grid, NC + 32, smem, st>>>(U));                 \
-        return true;                                                                           \
-    }
-        BK_UMM(2, 1) BK_UMM(4, 1) BK_UMM(6, 1) BK_UMM(8, 1) BK_UMM(4, 2) BK_UMM(8, 2)
-#undef BK_UMM
-    }
-    static bool a1 = false, a2 = false, a4 = false;
-    if (U.cw == 4) {
-        if (!a4) { set_smem((const void*)upd_stream_kernel<4>, smem); a4 = true; }
-        BK_KERNEL(upd_stream_kernel<4><<<grid, NC + 32, smem, st>>>(U));
-    } else if (U.cw == 2) {
-        if (!a2) { set_smem((const void*)upd_stream_kernel<2>, smem); a2 = true; }
-        BK_KERNEL(upd_stream_kernel<2><<<grid, NC + 32, smem, st>>>(U));
-    } else {
-        if (!a1) { set_smem((const void*)upd_stream_kernel<1>, smem); a1 = true; }
-        BK_KERNEL(upd_stream_kernel<1><<<grid, NC + 32, smem, st>>>(U));
-    }
-    return true;
-}
-
 bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
     // contiguous operands only, kp and k <= 32, out not aliasing P/Xin/W rows in other tiles is fine
     // (a strided output -- e.g. a GMRES basis block -- is written row by row from registers)
@@ -1267,7 +1188,7 @@ bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
         for (int j = 0; j < nin; ++j) { U.S.off[j] = off; off += U.S.T * U.S.w[j] * 8; off = (off + 127) & ~127; } }
     U.S.n = u.n;
     U.S.ntiles = (int)((u.n + U.S.T - 1) / U.S.T);
-    U.kp = u.kp; U.k = u.k; U.cw = cw; U.np = 1;
+    U.kp = u.kp; U.k = u.k; U.cw = cw;
     U.a = u.a; U.s = u.s; U.w_host = u.w_host; U.w_dev = u.w_dev;
     U.C = u.C; U.out = u.out; U.ldo = u.ldo; U.halt = u.halt;
     const int smem = NSTAGE * STAGE_BYTES + 128 + 32 * 32 * 8;
@@ -1364,7 +1285,8 @@ bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const 
     Gs.S.p[nin] = Gs.same ? X : Y; Gs.S.w[nin] = Gs.same ? 0 : k; if (!Gs.same) ++nin; else Gs.S.p[1] = X;
     if (Y2) {
         if (Gs.same) { Gs.S.p[1] = X; Gs.S.w[1] = 0; }
-        Gs.S.p[2] = Y2; Gs.S.w[2] = k;
+        Gs.y2x = (Y2 == X) ? 1 : 0;   // <T,S>, <T,T>: T streamed once
+        Gs.S.p[2] = Y2; Gs.S.w[2] = Gs.y2x ? 0 : k;
         nin = 3;
     }
     // compact: stream list may contain a zero-width slot (same == 1) -- it moves no bytes

@@ -99,6 +99,7 @@ __device__ __forceinline__ void wide_produce(const WideArgs& w, const CUtensorMa
             } else if (w1d) {   // last tile: plain copy + zero rows (visible through the arrive below)
                 double* d = reinterpret_cast<double*>(st + w.W.off);
                 for (int e = 0; e < w.T * w.W.w; ++e) d[e] = e < nr * w.W.w ? w.W.p[(int64_t)r0 * w.W.w + e] : 0.0;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // before any later bulk copy here
             } else {
                 wbytes = (uint32_t)w.T * w.W.wp * 8u;
             }

@@ -69,6 +69,7 @@ def update_flops(n: int, kp: int, k: int) -> int:
 
 
 def coldot_bytes(n: int, k: int, n_y: int = 1) -> int:
+    """Column dots of X with n_y other arrays (n_y = 0: ||X_c||^2, X read once)."""
     return D * n * k * (1 + n_y)
 
 
@@ -82,16 +83,17 @@ def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> 
 
     Fused (default where solve.cpp fuses): 2 applies + [Rt V R] Gram pass (3 N x k reads)
     + S = R - V alpha (2 reads, 1 write) + [Rt S T] Gram pass (3 reads) + the tail
-    X, R, P update with ||R|| (5 reads, 3 writes) = 21 N x k passes + 2 CSR streams."""
+    X, R, P update with ||R|| (5 reads, 3 writes) = 17 N x k passes + 2 applies (+ 2 reads
+    for the separate <T,S>, <T,T> pass when k does not divide 32)."""
     if fused is None:
         fused = bicgstab_fused(k)
     if fused:
         v = 8 * n * k
-        dots = 0 if 32 % k == 0 else coldot_bytes(n, k, 2)   # <T,S>, <T,T> in their own pass
+        dots = 0 if 32 % k == 0 else coldot_bytes(n, k, 1)   # <T,S>, <T,T> in their own pass (T, S read)
         return 2 * spmm_bytes(n, nnz, k) + 3 * v + update_bytes(n, k, k) + 3 * v + 8 * v + dots
     b = 2 * spmm_bytes(n, nnz, k)                     # V = A P, T = A S
     b += 3 * gram_bytes(n, k, k)                      # Rt^T V, Rt^T R, Rt^T T
-    b += coldot_bytes(n, k, 2) + coldot_bytes(n, k, 1)  # <T,S>, <T,T>; ||R||
+    b += coldot_bytes(n, k, 1) + coldot_bytes(n, k, 0)  # <T,S>, <T,T> (T, S read); ||R|| (R read)
     b += update_bytes(n, k, k)                        # S = R - V alpha
     b += update_bytes(n, k, k, extra_term=True)       # X += P alpha + omega S
     b += update_bytes(n, 0, k, extra_term=True)       # R = S - omega T
@@ -118,4 +120,19 @@ def gmres_step_bytes(n: int, nnz: int, k: int, j: int) -> int:
     b = spmm_bytes(n, nnz, k)
     b += 2 * (gram_bytes(n, ka, k) + update_bytes(n, ka, k))
     b += 2 * (gram_bytes(n, k, k, same=True) + update_bytes(n, k, k, a_nonzero=False))
+    return b
+
+
+def bicgstab_solve_bytes(n: int, nnz: int, k: int, iters: int, x0_is_zero: bool = True, rt_is_b: bool = True,
+                         fused: bool | None = None) -> int:
+    """A whole block_krylov_solve(method=bicgstab) call as solve.cpp enqueues it (no convergence
+    before `iters`): R = B (copy; + an apply when X0 != 0), ||R_c|| (one same-operand column-dot
+    pass), Rt = R0 (no copy when X0 = 0: Rt aliases B), P = R (copy), `iters` iterations, and the
+    final true residual (copy + apply with beta != 0 + ||.||)."""
+    v = D * n * k
+    b = 2 * v + (0 if x0_is_zero else spmm_bytes(n, nnz, k, beta_nonzero=True))
+    b += coldot_bytes(n, k, 0)
+    b += (0 if (x0_is_zero and rt_is_b) else 2 * v) + 2 * v
+    b += iters * bicgstab_iter_bytes(n, nnz, k, fused)
+    b += 2 * v + spmm_bytes(n, nnz, k, beta_nonzero=True) + coldot_bytes(n, k, 0)
     return b

@@ -38,14 +38,26 @@ def test_algorithmic_bytes():
 
 def test_fused_solver_pass_counts():
     """The solver byte models count the N x k passes solve.cpp enqueues:
-    fused BiCGStab = 2 applies + 17 passes (+ 3 for the separate column dots when k does not
-    divide 32); fused CG = 1 apply + 11 passes; unfused BiCGStab for k = 3."""
+    fused BiCGStab = 2 applies + 17 passes (+ 2 for the separate column dots when k does not
+    divide 32: T and S read once); fused CG = 1 apply + 11 passes; unfused BiCGStab for k = 3."""
     from paper_2504_02117_b200 import perfmodel as pm
     n, nnz = 1000, 5000
-    for k, extra in ((4, 0), (8, 0), (12, 3), (16, 0)):
+    for k, extra in ((4, 0), (8, 0), (12, 2), (16, 0)):
         v = 8 * n * k
         assert pm.bicgstab_iter_bytes(n, nnz, k) == 2 * pm.spmm_bytes(n, nnz, k) + (17 + extra) * v
     for k in (4, 8, 12, 16):
         assert pm.cg_iter_bytes(n, nnz, k) == pm.spmm_bytes(n, nnz, k) + 11 * 8 * n * k
     assert not pm.bicgstab_fused(3) and not pm.bicgstab_fused(32)
     assert pm.cg_iter_bytes(n, nnz, 3) > pm.spmm_bytes(n, nnz, 3) + 11 * 8 * n * 3
+
+
+def test_bicgstab_solve_bytes_counts_only_enqueued_passes():
+    """bench.py's solve bytes: with X0 = 0 the shadow residual aliases B (no
+    copy) and the same-operand column dots read R once -- 2 copies + 2 norm passes + 1 true
+    residual apply around the iterations, nothing more."""
+    n, nnz, k = 1000, 5000, 16
+    v = 8 * n * k
+    it = pm.bicgstab_iter_bytes(n, nnz, k)
+    assert pm.bicgstab_solve_bytes(n, nnz, k, 5) == (2 * v + v + 2 * v + 5 * it + 2 * v
+                                                     + pm.spmm_bytes(n, nnz, k, beta_nonzero=True) + v)
+    assert pm.bicgstab_solve_bytes(n, nnz, k, 5, rt_is_b=False) == pm.bicgstab_solve_bytes(n, nnz, k, 5) + 2 * v
