@@ -187,39 +187,44 @@ __device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col,
     constexpr int RPP = NC / LANES;
     constexpr int PASSES = (TR + RPP - 1) / RPP;
     constexpr int WR = 32 / LANES;                  // rows per warp per pass
-    constexpr int NB8 = (WR + 7) / 8;               // 8-row DMMA blocks per pass
+    constexpr int PP = WR < 8 ? 8 / WR : 1;         // passes per DMMA block (k > 16: 2, full m8 blocks)
+    constexpr int NR = PP * WR, NB8 = (NR + 7) / 8; // scratch rows, 8-row DMMA blocks
     constexpr int NQ = KP / 4, NKO = KP / 8, TS = KP + 2;
     const int lane32 = threadIdx.x & 31, mg = lane32 >> 2, kq = lane32 & 3;
     const int lrow = lane32 / LANES;                // row of this lane inside the warp's share
     const int wrow0 = grp - lrow;                   // first group index of the warp
 #pragma unroll 1
-    for (int pass = 0; pass < PASSES; ++pass) {
-        const int r = pass * RPP + grp;
-        const bool active = r < nr;
-        double acc[VEC];
+    for (int pass0 = 0; pass0 < PASSES; pass0 += PP) {
 #pragma unroll
-        for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
-        if (active) row_accumulate<VEC, false>(a, col, val, s_rp[r], s_rp[r + 1], c0, lane_in, acc);
-        double* tp = w_scr + lrow * TS + c0;
-        const bool keep = active && lane_in;
-        reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
-        reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+        for (int q = 0; q < PP; ++q) {
+            const int r = (pass0 + q) * RPP + grp;
+            const bool active = pass0 + q < PASSES && r < nr;
+            double acc[VEC];
+#pragma unroll
+            for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
+            if (active) row_accumulate<VEC, false>(a, col, val, s_rp[r], s_rp[r + 1], c0, lane_in, acc);
+            double* tp = w_scr + (q * WR + lrow) * TS + c0;
+            const bool keep = active && lane_in;
+            reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
+            reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+        }
         __syncwarp();
 #pragma unroll
         for (int b = 0; b < NB8; ++b) {
             const int lr = 8 * b + mg;                  // scratch row of the fragment
-            const bool rv = lr < WR;
+            const bool rv = lr < NR;
             double af[NQ];
 #pragma unroll
             for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
-            const int row = pass * RPP + wrow0 + lr;
+            const int pq = pass0 + lr / WR;
+            const int row = pq * RPP + wrow0 + lr % WR;
 #pragma unroll
             for (int nb = 0; nb < NKO; ++nb) {
                 double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                 for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
                 const int c = 8 * nb + 2 * kq;
-                if (rv && row < nr && c < a.kout) {
+                if (rv && pq < PASSES && row < nr && c < a.kout) {
                     double* yp = a.Y + (r0 + row) * a.ldy + c;
                     double v0 = a.alpha * d0, v1 = a.alpha * d1;
                     if (a.beta != 0.0) {
@@ -231,7 +236,7 @@ __device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col,
                 }
             }
         }
-        __syncwarp();                                   // scratch reused by the next pass
+        __syncwarp();                                   // scratch reused by the next passes
     }
 }
 
@@ -247,8 +252,9 @@ struct PipeCfg {
     static constexpr int STAGE_BYTES = RP_BYTES + COL_BYTES + VAL_BYTES;
     // ring + barriers/meta + (C and one scratch line per row group when coupled)
     static constexpr int bytes(int kp, int rpp, bool has_c) {
-        // (TCE: C fragments = kp*kp doubles, per-warp scratch (32/lanes rows of kp+2) <= rpp*(kp+2))
-        return NS * STAGE_BYTES + 64 * 8 + (has_c ? (kp * kp + rpp * (kp + 2)) * 8 : 0);
+        // (TCE: C fragments = kp*kp doubles, per-warp scratch of max(32/lanes, 8) rows of kp+2:
+        // <= max(rpp, 8 warps) rows)
+        return NS * STAGE_BYTES + 64 * 8 + (has_c ? (kp * kp + (rpp > 8 * (NC / 32) ? rpp : 8 * (NC / 32)) * (kp + 2)) * 8 : 0);
     }
 };
 
@@ -345,7 +351,7 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
         const int off = p0 & 3;
         const bool staged = s_staged[s] != 0;
         if constexpr (TCE) {
-            double* w_scr = s_t + warp * (32 / LANES) * (KP + 2);
+            double* w_scr = s_t + warp * ((32 / LANES) < 8 ? 8 : (32 / LANES)) * (KP + 2);
             if (staged) {
                 const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
                 const double* sval = reinterpret_cast<const double*>(st + L::RP_BYTES + L::COL_BYTES) + off - p0;
@@ -453,30 +459,22 @@ void launch_kv(const SpmmArgs& a, cudaStream_t st) {
     }
 }
 
-int max_vec() {
-    static int v = 0;
-    if (!v) {
-        const char* e = getenv("BK_SPMM_VEC");
-        v = e ? atoi(e) : 4;   // 4 columns per thread measured best (tools/ab_spmm.sh)
-        if (v != 2 && v != 4 && v != 8) v = 4;
-    }
-    return v;
-}
-
-// columns per thread: VEC = min(KP, max_vec()) when 16-byte vector access is legal
+// columns per thread: VEC = 4 when 256-bit gathers are legal (32-byte aligned X rows, k and
+// k_out multiples of 4), else 2 (16-byte) or 1
 template <int KP>
 void launch_k(const SpmmArgs& a, cudaStream_t st, bool vec2) {
-    // a lane's VEC columns must lie inside the row: k, k_out multiples of VEC
-    const int mv0 = max_vec();
-    // 4- and 8-column lanes gather with 256-bit loads: 32-byte aligned X (and ghost) rows
     const bool al32 = ((uintptr_t)a.X % 32 == 0) && (a.ldx % 4 == 0) &&
                       (a.Xg == nullptr || (((uintptr_t)a.Xg % 32 == 0) && a.ldg % 4 == 0));
-    const int mv = al32 ? mv0 : 2;
-    if constexpr (KP >= 8) {
-        if (vec2 && mv >= 8 && a.k % 8 == 0 && a.kout % 8 == 0) return launch_kv<KP, 8>(a, st);
+    if constexpr (KP == 16) {
+        // k = 12: three 4-column lanes per row (KP = 16 would leave one lane of four idle in
+        // the gather-bound loop); 288 consumers = 96 rows per pass, 288-row tiles = 3 passes
+        if (vec2 && al32 && a.k == 12 && a.kout == 12 && !a.C && !a.Xg && !a.rows && a.nrows > 0) {
+            launch_pipe<12, 4, false, 288, 2, 3, 288, 2592>(a, num_sms_cached(), st);
+            return;
+        }
     }
     if constexpr (KP >= 4) {
-        if (vec2 && mv >= 4 && a.k % 4 == 0 && a.kout % 4 == 0) return launch_kv<KP, 4>(a, st);
+        if (vec2 && al32 && a.k % 4 == 0 && a.kout % 4 == 0) return launch_kv<KP, 4>(a, st);
     }
     if constexpr (KP >= 2) {
         if (vec2) return launch_kv<KP, 2>(a, st);
@@ -522,12 +520,15 @@ __device__ __forceinline__ void win_load(const double* xp, int sw, double (&x)[V
     }
 }
 
-// acc += sum_{p in [s,e)} val[p] X[col[p], c0 : c0+VEC] with X from the staged
-// window (window row of column c: c + fo[g] for the last band g with
-// c >= thr[g]).  MR > 0: every row has <= MR nonzeros (the plan's bound), one
-// branch-free pass with clamped indices and zero weights; MR == 0: batches of 4.
-// Lanes with c0 >= k compute on in-bounds garbage that is never stored.
-template <int VEC, int NB, int MR>
+// acc += sum_{p in [s,e)} val[p] X[col[p], cols] with X from the staged window (window row of
+// column c: c + fo[g] for the last band g with c >= thr[g]).  MR > 0: every row has <= MR
+// nonzeros (the plan's bound), one branch-free pass with clamped indices and zero weights;
+// MR == 0: batches of 4.  Column sets: VEC consecutive columns at c0 (16-byte chunks in the
+// order sw), or (SPLIT, k > 16) the chunks at cA and cB = cA + 16: the 8 lanes of a row then
+// read 128 contiguous bytes per LDS.128 -- one wavefront per row, no bank conflicts (the
+// consecutive-column map read 16-byte chunks 32 bytes apart: 2-way conflicts).
+// Lanes whose columns lie beyond k compute on in-bounds garbage that is never stored.
+template <int VEC, int NB, int MR, bool SPLIT = false>
 __device__ __forceinline__ void band_accumulate(const double* s_win, const int* col, const double* val, int s, int e,
                                                 const int (&thr)[NB], const int (&fo)[NB], int kk, int c0, int sw,
                                                 double (&acc)[VEC]) {
@@ -543,7 +544,14 @@ __device__ __forceinline__ void band_accumulate(const double* s_win, const int* 
             int f = fo[0];
 #pragma unroll
             for (int g = 1; g < NB; ++g) f = (c >= thr[g]) ? fo[g] : f;
-            win_load<VEC>(s_win + (c + f) * kk + c0, sw, x[u]);
+            if constexpr (SPLIT) {
+                const double* xr = s_win + (c + f) * kk + c0;
+                const double2 lo = *reinterpret_cast<const double2*>(xr);
+                const double2 hi = *reinterpret_cast<const double2*>(xr + 16);
+                x[u][0] = lo.x; x[u][1] = lo.y; x[u][2] = hi.x; x[u][3] = hi.y;
+            } else {
+                win_load<VEC>(s_win + (c + f) * kk + c0, sw, x[u]);
+            }
         }
 #pragma unroll
         for (int u = 0; u < B; ++u)
@@ -551,11 +559,28 @@ __device__ __forceinline__ void band_accumulate(const double* s_win, const int* 
             for (int t = 0; t < VEC; ++t) acc[t] = fma(v[u], x[u][t], acc[t]);
         if constexpr (MR > 0) break;
     }
-    if constexpr (VEC == 4) {
+    if constexpr (VEC == 4 && !SPLIT) {
         if (sw) {   // chunks were accumulated in swapped order
             const double t0 = acc[0], t1 = acc[1];
             acc[0] = acc[2]; acc[1] = acc[3]; acc[2] = t0; acc[3] = t1;
         }
+    }
+}
+
+// Y[row, cA:cA+2] and Y[row, cB:cB+2] = alpha acc + beta Y (SPLIT column map, no coupling)
+__device__ __forceinline__ void store_split(const SpmmArgs& a, int64_t row, int cA, int cB, const double (&acc)[4]) {
+    const int cs[2] = {cA, cB};
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        const int c = cs[h];
+        if (c >= a.kout) continue;
+        double* yp = a.Y + row * a.ldy + c;
+        double v0 = a.alpha * acc[2 * h], v1 = a.alpha * acc[2 * h + 1];
+        if (a.beta != 0.0) {
+            v0 = fma(a.beta, yp[0], v0);
+            v1 = fma(a.beta, yp[1], v1);
+        }
+        __stcs(reinterpret_cast<double2*>(yp), make_double2(v0, v1));
     }
 }
 
@@ -687,10 +712,18 @@ bspmm_win_kernel(const BandArgs w) {
         return;
     }
     // ---------------------------------------------------- consumer warps
-    const int grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
+    // column map: VEC consecutive columns at c0, or (SPLIT: k > 16, 8 lanes per row) the
+    // 16-byte chunks at cA = 2 lane and cB = cA + 16 (conflict-free window loads)
+    constexpr bool SPLIT = KP == 32 && VEC == 4;
+    const int grp = tid / LANES, lane = tid % LANES, c0 = SPLIT ? 2 * lane : lane * VEC;
+    const int cA = c0, cB = SPLIT ? c0 + 16 : c0 + 2;
     const int kk = KEXACT ? KP : k;
     double* t_row = s_t + grp * (KP + 1);
     const int passes = (w.TR + RPP - 1) / RPP;
+    // coupled (TCE): WR rows per warp and pass; k > 16 has WR = 4, so PP = 2 passes fill one
+    // 8-row DMMA block (half-empty blocks doubled the epilogue's tensor-core work)
+    constexpr int WR = 32 / LANES;
+    constexpr int PP = (TCE && WR < 8) ? 8 / WR : 1;
     int s = 0;
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < w.ntiles; tile += gridDim.x) {
@@ -712,48 +745,61 @@ bspmm_win_kernel(const BandArgs w) {
             fo[g] = on ? (int)(w.wb[g] - (r0 + w.lo[g])) : 0;
         }
 #pragma unroll 1
-        for (int pass = 0; pass < passes; ++pass) {
-            const int r = pass * RPP + grp;
-            const bool active = r < nr;
-            double acc[VEC];
+        for (int pass0 = 0; pass0 < passes; pass0 += PP) {
 #pragma unroll
-            for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
-            if (active) {
-                const int rs = s_rp[r], re = s_rp[r + 1];
-                if (re > rs) {
-                    const int gr = (int)(r0 + r);
-                    const int sw = (kk <= 16) ? (((gr * kk) >> 4) & 1) : (gr & 1);
-                    band_accumulate<VEC, NB, MR>(s_win, scol, sval, rs, re, thr, fo, kk, c0, sw, acc);
+            for (int q = 0; q < PP; ++q) {
+                const int pass = pass0 + q;
+                const int r = pass * RPP + grp;
+                const bool active = pass < passes && r < nr;
+                double acc[VEC];
+#pragma unroll
+                for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
+                if (active) {
+                    const int rs = s_rp[r], re = s_rp[r + 1];
+                    if (re > rs) {
+                        const int gr = (int)(r0 + r);
+                        const int sw = (kk <= 16) ? (((gr * kk) >> 4) & 1) : (gr & 1);
+                        band_accumulate<VEC, NB, MR, SPLIT>(s_win, scol, sval, rs, re, thr, fo, kk, c0, sw, acc);
+                    }
+                }
+                if constexpr (TCE) {
+                    // this warp's rows -> its scratch (columns >= k zero: C's padded rows are
+                    // zero, and 0 x garbage could be NaN)
+                    double* w_scr = s_tT + warp * (PP * WR) * TS;
+                    const int lrow = q * WR + lane32 / LANES;
+                    double* tp = w_scr + lrow * TS;
+                    reinterpret_cast<double2*>(tp + cA)[0] =
+                        (active && cA < a.k) ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
+                    reinterpret_cast<double2*>(tp + cB)[0] =
+                        (active && cB < a.k) ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+                } else if constexpr (SPLIT) {
+                    if (active) store_split(a, r0 + r, cA, cB, acc);
+                } else {
+                    row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
                 }
             }
             if constexpr (TCE) {
-                // this warp's rows of the pass -> its scratch (padded columns zero), then
-                // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA by the warp itself: no
-                // CTA barrier, so other warps keep gathering
-                constexpr int WR = 32 / (KP / VEC), NB8 = (WR + 7) / 8;
-                double* w_scr = s_tT + warp * WR * TS;
-                const int lrow = lane32 / (KP / VEC);
-                double* tp = w_scr + lrow * TS + c0;
-                const bool keep = active && c0 < a.k;
-                reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
-                reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+                // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA by the warp itself: no CTA
+                // barrier, so the other warps keep gathering
+                constexpr int NR = PP * WR, NB8 = (NR + 7) / 8;
+                const double* w_scr = s_tT + warp * NR * TS;
                 __syncwarp();
                 const int mg = lane32 >> 2, kq = lane32 & 3;
 #pragma unroll
                 for (int b = 0; b < NB8; ++b) {
                     const int lr = 8 * b + mg;
-                    const bool rv = lr < WR;
+                    const bool rv = lr < NR;
                     double af[NQ];
 #pragma unroll
                     for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
-                    const int row = pass * RPP + warp * WR + lr;
+                    const int row = (pass0 + lr / WR) * RPP + warp * WR + lr % WR;
 #pragma unroll
                     for (int nb = 0; nb < NKO; ++nb) {
                         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                         for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
                         const int c = 8 * nb + 2 * kq;
-                        if (rv && row < nr && c < a.kout) {
+                        if (rv && pass0 + lr / WR < passes && row < nr && c < a.kout) {
                             double* yp = a.Y + (r0 + row) * a.ldy + c;
                             double v0 = a.alpha * d0, v1 = a.alpha * d1;
                             if (a.beta != 0.0) {
@@ -766,8 +812,6 @@ bspmm_win_kernel(const BandArgs w) {
                     }
                 }
                 __syncwarp();
-            } else {
-                row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
             }
         }
         __syncwarp();
@@ -811,7 +855,10 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     // scratch line per row group
     constexpr bool TCE = HAS_C && KP >= 8 && VEC == 4;
     auto fixed_for = [&](int tr) {
-        const int cb = TCE ? ((KP / 4) * (KP / 8) * 32 + (tr > RPP ? tr : RPP) * (KP + 2)) * 8
+        // TCE scratch: (NC / 32) warps x max(WR, 8) rows (k > 16 pairs two passes per warp)
+        constexpr int scr_rows = (NC / 32) * ((32 / LANES) < 8 ? 8 : (32 / LANES));
+        (void)tr;
+        const int cb = TCE ? ((KP / 4) * (KP / 8) * 32 + scr_rows * (KP + 2)) * 8
                            : (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
         return 16 * 8 + kMetaDepth * 8 + cb;
     };
@@ -949,7 +996,9 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     static const int w3 = env_int("BK_WIN_3D", -1);
     // Coupled applies (per-warp DMMA epilogue in both kernels) follow the same rule: c2 k = 16
     // 0.64 band vs 0.52 gather, c4 k = 8 / 16 0.71 / 0.53 gather vs 0.63 / 0.49 band.
-    if (w3 < 0 && (p.nbands >= 5 || a.k > 16)) return false;
+    // k > 16 on 2-D lattices: the conflict-free split column map (SPLIT) -- A/B: BK_WIN_3D=0
+    if (w3 < 0 && p.nbands >= 5) return false;
+    if (w3 == 0 && a.k > 16) return false;
     if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
     // the window copies contiguous X rows: packed X (ldx == k), 16-byte aligned
     if (a.ldx != a.k || ((uintptr_t)a.X % 16) != 0) return false;
