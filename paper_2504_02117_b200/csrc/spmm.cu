@@ -179,10 +179,14 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs& a, const int* col, con
 // pass (32 / LANES of them) go to a per-warp scratch (TS doubles per row), then
 // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA with C as B fragments
 // ([ks][nb][lane] in shared memory); blocks of 8 rows, rows beyond the warp's share are zero.
+template <int KP>
+struct CfRegs { static constexpr int N = (KP <= 16 && KP >= 8) ? (KP / 4) * (KP / 8) : 1; };
+
 template <int KP, int VEC, int NC, int TR>
 __device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col, const double* val, const int* s_rp,
                                               int nr, int64_t r0, int grp, int c0, bool lane_in,
-                                              const double* s_Cf, double* w_scr) {
+                                              const double* s_Cf, const double (&cf)[CfRegs<KP>::N], double* w_scr) {
+    constexpr int NCF = CfRegs<KP>::N;
     constexpr int LANES = KP / VEC;
     constexpr int RPP = NC / LANES;
     constexpr int PASSES = (TR + RPP - 1) / RPP;
@@ -222,7 +226,8 @@ __device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col,
             for (int nb = 0; nb < NKO; ++nb) {
                 double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                for (int ks = 0; ks < NQ; ++ks)
+                    dmma(d0, d1, af[ks], KP <= 16 ? cf[(ks * NKO + nb) % NCF] : s_Cf[(ks * NKO + nb) * 32 + lane32]);
                 const int c = 8 * nb + 2 * kq;
                 if (rv && pq < PASSES && row < nr && c < a.kout) {
                     double* yp = a.Y + (r0 + row) * a.ldy + c;
@@ -338,6 +343,10 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
     const int grp = tid / LANES, lane = tid % LANES, c0 = lane * VEC;
     const bool lane_in = c0 < a.k;
     double* t_row = s_t + grp * (KP + 1);
+    // coupled k <= 16: C's B fragments in registers for the whole kernel
+    double cf[CfRegs<KP>::N];
+#pragma unroll
+    for (int q = 0; q < CfRegs<KP>::N; ++q) cf[q] = (TCE && KP <= 16) ? s_C[q * 32 + (tid & 31)] : 0.0;
     int i = 0;
     for (int tile = tb; tile < te; tile += tstep, ++i) {
         const int s = i % NS;
@@ -355,9 +364,9 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
             if (staged) {
                 const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
                 const double* sval = reinterpret_cast<const double*>(st + L::RP_BYTES + L::COL_BYTES) + off - p0;
-                tile_rows_tce<KP, VEC, NC, TR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, w_scr);
+                tile_rows_tce<KP, VEC, NC, TR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, cf, w_scr);
             } else {
-                tile_rows_tce<KP, VEC, NC, TR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, w_scr);
+                tile_rows_tce<KP, VEC, NC, TR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, cf, w_scr);
             }
         } else if (staged) {
             const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
@@ -724,6 +733,8 @@ bspmm_win_kernel(const BandArgs w) {
     // 8-row DMMA block (half-empty blocks doubled the epilogue's tensor-core work)
     constexpr int WR = 32 / LANES;
     constexpr int PP = (TCE && WR < 8) ? 8 / WR : 1;
+    // (C's fragments stay in shared memory here: register-resident fragments raised the k = 16
+    // kernel to 106 registers and measured 0.66 -> 0.49 of HBM; the gather kernel keeps them)
     int s = 0;
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < w.ntiles; tile += gridDim.x) {
@@ -862,7 +873,9 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
                            : (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
         return 16 * 8 + kMetaDepth * 8 + cb;
     };
-    int TR = RPP < 64 ? 64 : RPP;
+    // (coupled k > 16 pairs PP passes per DMMA block: a tile holds at least PP passes)
+    constexpr int PPm = (TCE && (32 / LANES) < 8) ? 8 / (32 / LANES) : 1;
+    int TR = std::max(64, PPm * RPP);
     if (tr_env > 0) {
         TR = std::max(2, tr_env & ~1);
     } else if (ctas == 2 && big_tiles) {   // the largest multiple of 16 rows with two stages per CTA
