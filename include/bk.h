@@ -81,6 +81,20 @@ int bk_get_nccl_unique_id(void *out128);
 int bk_ctx_set_comm(bk_ctx *ctx, const void *uid128, int nranks, int rank);
 int bk_ctx_comm_info(const bk_ctx *ctx, int *nranks, int *rank);
 
+/* Loopback transport (TEST INFRASTRUCTURE for the row-partitioned path on a one-GPU box):
+ * `nranks` virtual ranks live in ONE process, one host thread and one ctx each (any
+ * devices, typically all on device 0).  bk_ctx_set_comm_local attaches a ctx as rank `rank`
+ * of the hub instead of an NCCL communicator; every collective of the library
+ * (bk_csr_create's halo-plan exchange, the halo exchange inside bspmm_apply, the Gram
+ * allreduce, the solvers' reductions) then runs between host barriers with device-to-device
+ * copies, reductions on the device in rank order -- the same protocol, the same
+ * interior / boundary kernels, bitwise-identical results on every rank.  Every rank's thread
+ * must make the same sequence of collective calls (as with NCCL).  The hub must outlive the
+ * contexts attached to it; it holds no device memory.  Returns BK_OK or BK_ERR_ARG.      */
+int bk_local_hub_create(void **hub, int nranks);
+int bk_local_hub_destroy(void *hub);
+int bk_ctx_set_comm_local(bk_ctx *ctx, void *hub, int rank);
+
 /* ---------------------------------------------------------------- matrix
  * Local row slab [row_begin, row_begin + n_local) of an n_global x n_global
  * CSR matrix (SPEC S:26-31 invariants: row_ptr[0] = 0, non-decreasing,

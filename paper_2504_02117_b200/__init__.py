@@ -38,7 +38,8 @@ EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last
             "bk_ctx_synchronize", "bk_ctx_destroy", "bk_get_nccl_unique_id", "bk_ctx_set_comm",
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
             "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo",
-            "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply", "bk_alg1_run", "bk_dirk_solve_dc"]
+            "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply", "bk_alg1_run", "bk_dirk_solve_dc",
+            "bk_local_hub_create", "bk_local_hub_destroy", "bk_ctx_set_comm_local"]
 
 
 class SolveOpts(ctypes.Structure):
@@ -82,6 +83,9 @@ _sig = {
     "bk_get_nccl_unique_id": ([_P], _I),
     "bk_ctx_set_comm": ([_P, _P, _I, _I], _I),
     "bk_ctx_comm_info": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "bk_local_hub_create": ([ctypes.POINTER(_P), _I], _I),
+    "bk_local_hub_destroy": ([_P], _I),
+    "bk_ctx_set_comm_local": ([_P, _P, _I], _I),
     "bk_csr_create": ([_P, ctypes.POINTER(_P), _I64, _I64, _I64, _P, _P, _P, _I64], _I),
     "bk_csr_destroy": ([_P], _I),
     "bk_csr_get_info": ([_P, ctypes.POINTER(CsrInfo)], _I),
@@ -202,6 +206,11 @@ class Context:
         buf = ctypes.create_string_buffer(bytes(uid), 128)
         self.check(_lib.bk_ctx_set_comm(self._h, buf, nranks, rank), "bk_ctx_set_comm")
 
+    def set_comm_local(self, hub: "LocalHub", rank: int):
+        """Attach this ctx as virtual rank `rank` of an in-process loopback hub (test transport,
+        include/bk.h bk_ctx_set_comm_local)."""
+        self.check(_lib.bk_ctx_set_comm_local(self._h, hub.handle, rank), "bk_ctx_set_comm_local")
+
     def comm_info(self):
         n, r = _I(), _I()
         _lib.bk_ctx_comm_info(self._h, ctypes.byref(n), ctypes.byref(r))
@@ -223,6 +232,27 @@ class Context:
 
     def __exit__(self, *a):
         self.close()
+
+
+class LocalHub:
+    """bk_local_hub_create: in-process loopback transport for `nranks` virtual ranks (one host
+    thread + one Context each); test infrastructure for the row-partitioned path on one GPU."""
+
+    def __init__(self, nranks: int):
+        self._h = _P()
+        st = _lib.bk_local_hub_create(ctypes.byref(self._h), nranks)
+        if st:
+            raise BkError(st, "bk_local_hub_create")
+        self.nranks = nranks
+
+    @property
+    def handle(self):
+        return self._h
+
+    def close(self):
+        if self._h:
+            _lib.bk_local_hub_destroy(self._h)
+            self._h = _P()
 
 
 class Matrix:

@@ -489,6 +489,10 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
     // p > 1: halo exchange on the comm stream overlapped with the interior rows
     int r = halo_exchange(ctx, A, k, X, ldx);   // records ctx->ev_b when the ghosts have landed
     if (r) return r;
+    // the interior rows run while the halo is in flight: leave SMs for NCCL's send/recv kernels
+    // (a persistent grid over every SM would only let them in once the interior is done)
+    constexpr int kCommSms = 8;
+    a.grid_sms = ctx->num_sms > 2 * kCommSms ? ctx->num_sms - kCommSms : 0;
     if (A->interior_contig) {
         a.row0 = A->interior_begin;
         a.nrows = A->n_interior;
@@ -499,6 +503,7 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
     }
     if (!launch_bspmm_win(a, A->band, ctx->stream)) launch_bspmm(a, ctx->stream);
     cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
+    a.grid_sms = 0;
     a.rows = A->d_boundary_rows;
     a.nrows = A->n_boundary;
     a.Xg = (const double*)A->ghost.p;

@@ -18,6 +18,8 @@
 
 namespace bk {
 
+struct LocalHub;   // in-process loopback transport (comm.cpp)
+
 // Every kernel launch of the library goes through BK_KERNEL so the process-wide
 // count is exact (bk_kernel_launch_count(); bench.py reports it as gpu_launches).
 extern std::atomic<long long> g_launches;
@@ -64,6 +66,9 @@ struct SpmmArgs {
     // then the line, then the x block (sl_tpl tiles per line) -- keeps the z-neighbour planes
     // of the rows in flight L2-resident when whole planes do not fit
     int sl_S, sl_L, sl_tpl, sl_ny, sl_nz;
+    // persistent grids: SMs to size the grid for (0 = all).  p > 1: the interior apply leaves
+    // SMs free for NCCL's send/recv kernels while the halo is in flight (abi.cpp)
+    int grid_sms;
 };
 
 // out = a*Xin + s*(P C) + (w_host * (*w_dev)) * W     (any term may be absent)
@@ -256,6 +261,7 @@ struct bk_ctx {
 #ifndef BK_NO_NCCL
     ncclComm_t comm = nullptr;
 #endif
+    bk::LocalHub* hub = nullptr;  // loopback transport instead of NCCL (bk_ctx_set_comm_local)
 };
 
 struct bk_neighbor {

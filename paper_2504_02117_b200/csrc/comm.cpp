@@ -8,14 +8,70 @@
 // a contiguous slice of X, so slab halos need no packing.  Gram matrices are
 // summed in place with ncclAllReduce; every rank receives identical bits, so
 // the replicated small-dense stage takes identical decisions on all ranks.
+//
+// Two transports behind the same calls: NCCL (one process per GPU, the product path) and an
+// in-process LOOPBACK hub (bk_local_hub_create / bk_ctx_set_comm_local: several virtual ranks,
+// one host thread each, in one process -- e.g. all on one GPU).  The hub exists so the
+// multi-rank code (halo plan exchange, interior / boundary split, ghost-row kernels, Gram
+// allreduce, the solvers' p > 1 path) runs under the GPU parity tests on a one-GPU box; it moves
+// data with device-to-device copies between host barriers and reduces on the device in rank
+// order, so no kernel ever waits on another rank's kernel.
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "bk_internal.h"
 
 using namespace bk;
+
+namespace bk {
+// One posted point-to-point transfer of a grouped exchange.
+struct P2POp {
+    int peer;
+    bool send;
+    void* buf;
+    size_t bytes;
+};
+
+// out[i] = op over ranks q = 0..P-1 (in rank order) of stage[q * n + i]; op 0 sum, 1 max
+__global__ void hub_reduce_kernel(const double* __restrict__ stage, double* __restrict__ out, int P, int64_t n,
+                                  int op) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double v = stage[i];
+        for (int q = 1; q < P; ++q) {
+            const double w = stage[(int64_t)q * n + i];
+            v = op == 0 ? v + w : (w > v ? w : v);
+        }
+        out[i] = v;
+    }
+}
+
+struct LocalHub {
+    explicit LocalHub(int p) : P(p), ptr(p, nullptr), ops(p) {}
+    const int P;
+    std::mutex m;
+    std::condition_variable cv;
+    int arrived = 0;
+    unsigned long gen = 0;
+    std::vector<const void*> ptr;            // per rank: buffer posted to the current collective
+    std::vector<std::vector<P2POp>> ops;     // per rank: posted point-to-point transfers
+    void barrier() {
+        std::unique_lock<std::mutex> lk(m);
+        const unsigned long g = gen;
+        if (++arrived == P) {
+            arrived = 0;
+            ++gen;
+            cv.notify_all();
+        } else {
+            cv.wait(lk, [&] { return gen != g; });
+        }
+    }
+};
+}  // namespace bk
 
 namespace {
 
@@ -78,42 +134,157 @@ extern "C" int bk_ctx_set_comm(bk_ctx* ctx, const void* uid128, int nranks, int 
         ctx->comm = nullptr;
     }
     NCCL_OK(ctx, ncclCommInitRank(&ctx->comm, nranks, id, rank));
+    ctx->hub = nullptr;
     ctx->nranks = nranks;
     ctx->rank = rank;
     return BK_OK;
 #endif
 }
 
+extern "C" int bk_local_hub_create(void** hub, int nranks) {
+    if (!hub || nranks < 1 || nranks > 1024) return BK_ERR_ARG;
+    *hub = new LocalHub(nranks);
+    return BK_OK;
+}
+
+extern "C" int bk_local_hub_destroy(void* hub) {
+    delete static_cast<LocalHub*>(hub);
+    return BK_OK;
+}
+
+extern "C" int bk_ctx_set_comm_local(bk_ctx* ctx, void* hub, int rank) {
+    if (!ctx) return BK_ERR_ARG;
+    LocalHub* h = static_cast<LocalHub*>(hub);
+    if (!h || rank < 0 || rank >= h->P) return set_error(ctx, BK_ERR_ARG, "bk_ctx_set_comm_local: bad hub or rank");
+#ifndef BK_NO_NCCL
+    if (ctx->comm) {
+        ncclCommDestroy(ctx->comm);
+        ctx->comm = nullptr;
+    }
+#endif
+    ctx->hub = h;
+    ctx->nranks = h->P;
+    ctx->rank = rank;
+    return BK_OK;
+}
+
 namespace bk {
 
+namespace {
+constexpr int WS_HUB_STAGE = 120;   // workspace slot of the loopback reduction staging
+int hub_cuda(bk_ctx* ctx, cudaError_t e, const char* where) { return cuda_check(ctx, e, where); }
+
+// every rank's `send` (bytes each) -> recv[q * bytes ...] on every rank
+int hub_allgather(bk_ctx* ctx, const void* send, void* recv, size_t bytes, cudaStream_t st) {
+    LocalHub* h = ctx->hub;
+    int r = hub_cuda(ctx, cudaStreamSynchronize(st), "hub allgather");
+    h->ptr[ctx->rank] = send;
+    h->barrier();
+    for (int q = 0; q < h->P && !r; ++q)
+        r = hub_cuda(ctx, cudaMemcpy((char*)recv + (size_t)q * bytes, h->ptr[q], bytes, cudaMemcpyDefault),
+                     "hub allgather copy");
+    h->barrier();
+    return r;
+}
+
+// in-place reduction (0 sum, 1 max) of n doubles, rank order, on the device
+int hub_allreduce(bk_ctx* ctx, double* d, int64_t n, int op) {
+    LocalHub* h = ctx->hub;
+    const int P = h->P;
+    int r = hub_cuda(ctx, cudaStreamSynchronize(ctx->stream), "hub allreduce");
+    double* stage = (double*)ws_get(ctx, WS_HUB_STAGE, sizeof(double) * (size_t)P * n);
+    h->ptr[ctx->rank] = d;
+    h->barrier();
+    for (int q = 0; q < P && !r; ++q)
+        r = hub_cuda(ctx, cudaMemcpy(stage + (int64_t)q * n, h->ptr[q], sizeof(double) * n, cudaMemcpyDefault),
+                     "hub allreduce copy");
+    h->barrier();   // every rank holds every contribution: d may be overwritten now
+    if (!r) {
+        const int blocks = (int)std::min<int64_t>((n + 255) / 256, 1024);
+        BK_KERNEL(hub_reduce_kernel<<<blocks, 256, 0, ctx->stream>>>(stage, d, P, n, op));
+        r = hub_cuda(ctx, cudaGetLastError(), "hub reduce");
+    }
+    return r;
+}
+
+// grouped point-to-point transfers; the n-th send to a peer matches that peer's n-th receive from me
+int hub_p2p(bk_ctx* ctx, const std::vector<P2POp>& ops, cudaStream_t st) {
+    LocalHub* h = ctx->hub;
+    int r = hub_cuda(ctx, cudaStreamSynchronize(st), "hub p2p");
+    h->ops[ctx->rank] = ops;
+    h->barrier();
+    std::vector<int> seen(h->P, 0);
+    for (const P2POp& o : ops) {
+        if (o.send || r) continue;
+        const int nth = seen[o.peer]++;
+        int c = 0;
+        const P2POp* match = nullptr;
+        for (const P2POp& p : h->ops[o.peer])
+            if (p.send && p.peer == ctx->rank && c++ == nth) { match = &p; break; }
+        if (!match || match->bytes != o.bytes) {
+            r = set_error(ctx, BK_ERR_ARG, "hub p2p: unmatched receive");
+            break;
+        }
+        r = hub_cuda(ctx, cudaMemcpy(o.buf, match->buf, o.bytes, cudaMemcpyDefault), "hub p2p copy");
+    }
+    h->barrier();
+    return r;
+}
+}  // namespace
+
 int allreduce_sum(bk_ctx* ctx, double* d, int64_t n) {
+    if (ctx->nranks <= 1 || n == 0) return BK_OK;
+    if (ctx->hub) return hub_allreduce(ctx, d, n, 0);
 #ifdef BK_NO_NCCL
-    (void)d; (void)n;
+    (void)d;
     return set_error(ctx, BK_ERR_UNSUPPORTED, "built without NCCL");
 #else
-    if (ctx->nranks <= 1 || n == 0) return BK_OK;
     NCCL_OK(ctx, ncclAllReduce(d, d, (size_t)n, ncclDouble, ncclSum, ctx->comm, ctx->stream));
     return BK_OK;
 #endif
 }
 
 int allreduce_max(bk_ctx* ctx, double* d, int64_t n) {
-#ifdef BK_NO_NCCL
-    (void)d; (void)n;
-    return ctx->nranks <= 1 ? BK_OK : set_error(ctx, BK_ERR_UNSUPPORTED, "built without NCCL");
-#else
     if (ctx->nranks <= 1 || n == 0) return BK_OK;
+    if (ctx->hub) return hub_allreduce(ctx, d, n, 1);
+#ifdef BK_NO_NCCL
+    (void)d;
+    return set_error(ctx, BK_ERR_UNSUPPORTED, "built without NCCL");
+#else
     NCCL_OK(ctx, ncclAllReduce(d, d, (size_t)n, ncclDouble, ncclMax, ctx->comm, ctx->stream));
     return BK_OK;
 #endif
 }
 
-int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::vector<int32_t>& col_local,
-                   const std::vector<int32_t>& colg) {
+namespace {
+int xport_allgather(bk_ctx* ctx, const void* send, void* recv, size_t bytes, cudaStream_t st) {
+    if (ctx->hub) return hub_allgather(ctx, send, recv, bytes, st);
 #ifdef BK_NO_NCCL
-    (void)A; (void)rp; (void)col_local; (void)colg;
+    (void)send; (void)recv; (void)bytes; (void)st;
     return set_error(ctx, BK_ERR_UNSUPPORTED, "built without NCCL");
 #else
+    return nccl_check(ctx, ncclAllGather(send, recv, bytes, ncclChar, ctx->comm, st), "allgather");
+#endif
+}
+
+int xport_p2p(bk_ctx* ctx, const std::vector<P2POp>& ops, cudaStream_t st) {
+    if (ctx->hub) return hub_p2p(ctx, ops, st);
+#ifdef BK_NO_NCCL
+    (void)ops; (void)st;
+    return set_error(ctx, BK_ERR_UNSUPPORTED, "built without NCCL");
+#else
+    NCCL_OK(ctx, ncclGroupStart());
+    for (const P2POp& o : ops) {
+        if (o.send) ncclSend(o.buf, o.bytes, ncclChar, o.peer, ctx->comm, st);
+        else ncclRecv(o.buf, o.bytes, ncclChar, o.peer, ctx->comm, st);
+    }
+    return nccl_check(ctx, ncclGroupEnd(), "grouped send/recv");
+#endif
+}
+}  // namespace
+
+int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::vector<int32_t>& col_local,
+                   const std::vector<int32_t>& colg) {
     const int P = ctx->nranks, me = ctx->rank;
     cudaStream_t st = ctx->stream;
     // 1. allgather (row_begin, n_local) -> partition bounds
@@ -121,7 +292,7 @@ int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::
     if (cudaMalloc(&d_pair, sizeof(int64_t) * 2 * (P + 1)) != cudaSuccess) return set_error(ctx, BK_ERR_OOM, "oom");
     int64_t mine[2] = {A->row_begin, A->n_local};
     cudaMemcpy(d_pair + 2 * P, mine, sizeof mine, cudaMemcpyHostToDevice);
-    int r = nccl_check(ctx, ncclAllGather(d_pair + 2 * P, d_pair, 2, ncclInt64, ctx->comm, st), "allgather ranges");
+    int r = xport_allgather(ctx, d_pair + 2 * P, d_pair, 2 * sizeof(int64_t), st);
     std::vector<int64_t> pairs(2 * P);
     cudaStreamSynchronize(st);
     cudaMemcpy(pairs.data(), d_pair, sizeof(int64_t) * 2 * P, cudaMemcpyDeviceToHost);
@@ -153,7 +324,7 @@ int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::
     int64_t* d_cnt = nullptr;
     cudaMalloc(&d_cnt, sizeof(int64_t) * P * (P + 1));
     cudaMemcpy(d_cnt + (int64_t)P * P, need.data(), sizeof(int64_t) * P, cudaMemcpyHostToDevice);
-    r = nccl_check(ctx, ncclAllGather(d_cnt + (int64_t)P * P, d_cnt, P, ncclInt64, ctx->comm, st), "allgather counts");
+    r = xport_allgather(ctx, d_cnt + (int64_t)P * P, d_cnt, P * sizeof(int64_t), st);
     std::vector<int64_t> cnt((size_t)P * P);
     cudaStreamSynchronize(st);
     cudaMemcpy(cnt.data(), d_cnt, sizeof(int64_t) * P * P, cudaMemcpyDeviceToHost);
@@ -170,13 +341,13 @@ int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::
     if (ng) cudaMemcpy(d_req, gid.data(), sizeof(int64_t) * ng, cudaMemcpyHostToDevice);
     std::vector<int64_t> give_off(P, 0);
     for (int q = 1; q < P; ++q) give_off[q] = give_off[q - 1] + give[q - 1];
-    ncclGroupStart();
+    std::vector<P2POp> ops;
     for (int q = 0; q < P; ++q) {
         if (q == me) continue;
-        if (need[q]) ncclSend(d_req + recv_off[q], (size_t)need[q], ncclInt64, q, ctx->comm, st);
-        if (give[q]) ncclRecv(d_give + give_off[q], (size_t)give[q], ncclInt64, q, ctx->comm, st);
+        if (need[q]) ops.push_back({q, true, d_req + recv_off[q], sizeof(int64_t) * (size_t)need[q]});
+        if (give[q]) ops.push_back({q, false, d_give + give_off[q], sizeof(int64_t) * (size_t)give[q]});
     }
-    r = nccl_check(ctx, ncclGroupEnd(), "exchange halo requests");
+    r = xport_p2p(ctx, ops, st);
     std::vector<int64_t> give_ids(std::max<int64_t>(total_give, 1));
     cudaStreamSynchronize(st);
     if (total_give) cudaMemcpy(give_ids.data(), d_give, sizeof(int64_t) * total_give, cudaMemcpyDeviceToHost);
@@ -232,36 +403,32 @@ int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::
         cudaMemcpy(A->d_interior_rows, inter.data(), sizeof(int32_t) * inter.size(), cudaMemcpyHostToDevice);
     }
     return cuda_check(ctx, cudaGetLastError(), "csr_setup_comm");
-#endif
 }
 
 int halo_exchange(bk_ctx* ctx, const bk_csr* Ac, int k, const double* X, int64_t ldx) {
-#ifdef BK_NO_NCCL
-    (void)Ac; (void)k; (void)X; (void)ldx;
-    return set_error(ctx, BK_ERR_UNSUPPORTED, "built without NCCL");
-#else
     bk_csr* A = const_cast<bk_csr*>(Ac);
     cudaStream_t cs = ctx->comm_stream;
     double* ghost = (double*)grow(A->ghost, sizeof(double) * std::max<int64_t>(A->n_ghost, 1) * k, ctx->stream);
     double* sendbuf = (double*)grow(A->sendbuf, sizeof(double) * std::max<int64_t>(A->n_send_total, 1) * k, ctx->stream);
-    // X is produced on the compute stream: the comm stream waits for it
+    // X is produced on the compute stream (and the previous apply's boundary rows still read the
+    // ghost buffer there): the comm stream waits for it
     cudaEventRecord(ctx->ev_a, ctx->stream);
     cudaStreamWaitEvent(cs, ctx->ev_a, 0);
     for (const auto& nb : A->nbs)
         if (nb.send_cnt && !(nb.send_contig && ldx == k))
             launch_pack_rows(nb.send_cnt, k, nb.d_send_rows, X, ldx, sendbuf + nb.send_off * k, cs);
-    NCCL_OK(ctx, ncclGroupStart());
+    std::vector<P2POp> ops;
     for (const auto& nb : A->nbs) {
         if (nb.send_cnt) {
             const double* src = (nb.send_contig && ldx == k) ? X + nb.send_begin * ldx : sendbuf + nb.send_off * k;
-            ncclSend(src, (size_t)nb.send_cnt * k, ncclDouble, nb.rank, ctx->comm, cs);
+            ops.push_back({nb.rank, true, const_cast<double*>(src), sizeof(double) * (size_t)nb.send_cnt * k});
         }
-        if (nb.recv_cnt) ncclRecv(ghost + nb.recv_off * k, (size_t)nb.recv_cnt * k, ncclDouble, nb.rank, ctx->comm, cs);
+        if (nb.recv_cnt) ops.push_back({nb.rank, false, ghost + nb.recv_off * k, sizeof(double) * (size_t)nb.recv_cnt * k});
     }
-    NCCL_OK(ctx, ncclGroupEnd());
+    int r = xport_p2p(ctx, ops, cs);
+    if (r) return r;
     cudaEventRecord(ctx->ev_b, cs);
     return cuda_check(ctx, cudaGetLastError(), "halo_exchange");
-#endif
 }
 
 }  // namespace bk

@@ -279,12 +279,27 @@ struct Solver {
         }
         int r = launched("coldot");
         if (r) return r;
-        if (allred) {
+        std::vector<std::pair<double*, int64_t>> outs{{d, k}};
+        if (d2) outs.push_back({d2, k});
+        return reduce_outputs(outs);
+    }
+    // p > 1: sum a reduction pass's outputs over the ranks -- ONE allreduce when they are adjacent
+    // in memory (the solvers lay them out that way), else one per output
+    int reduce_outputs(std::vector<std::pair<double*, int64_t>> outs) {
+        if (!allred || outs.empty()) return BK_OK;
+        std::sort(outs.begin(), outs.end());
+        bool adjacent = true;
+        for (size_t i = 1; i < outs.size(); ++i) adjacent = adjacent && outs[i - 1].first + outs[i - 1].second == outs[i].first;
+        if (adjacent) {
             rep->n_allreduce++;
-            r = allreduce_sum(ctx, d, k);
-            if (!r && d2) r = allreduce_sum(ctx, d2, k);
+            return allreduce_sum(ctx, outs[0].first, outs.back().first + outs.back().second - outs[0].first);
         }
-        return r;
+        for (auto& o : outs) {
+            rep->n_allreduce++;
+            int r = allreduce_sum(ctx, o.first, o.second);
+            if (r) return r;
+        }
+        return BK_OK;
     }
     // fused multi-operand Gram (k x k blocks of [arrays[xs..]]^T [arrays[ys..]]), summed over ranks
     int gram_multi(int nxa, const int* xs, int nya, const int* ys, int nin, const double* const* arrays,
@@ -299,18 +314,13 @@ struct Solver {
             return set_error(ctx, BK_ERR_UNSUPPORTED, "fused gram not applicable");
         te(cls);
         int r = launched("gram_multi");
-        for (int i = 0; i < nxa && !r; ++i)
-            for (int j = 0; j < nya && !r; ++j)
-                if (allred && blk[i][j]) {
-                    rep->n_allreduce++;
-                    r = allreduce_sum(ctx, blk[i][j], (int64_t)k * k);
-                }
-        for (int q = 0; q < ndot && !r; ++q)
-            if (allred) {
-                rep->n_allreduce++;
-                r = allreduce_sum(ctx, dots[q], k);
-            }
-        return r;
+        if (r) return r;
+        std::vector<std::pair<double*, int64_t>> outs;
+        for (int i = 0; i < nxa; ++i)
+            for (int j = 0; j < nya; ++j)
+                if (blk[i][j]) outs.push_back({blk[i][j], (int64_t)k * k});
+        for (int q = 0; q < ndot; ++q) outs.push_back({dots[q], k});
+        return reduce_outputs(outs);
     }
     // out = a Xin + s P C (+ w W), optionally halted
     int upd(double* out, int64_t ldo, double a, const double* Xin, int64_t ldxin, double s, const double* P,
@@ -515,8 +525,10 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     double* T = S.vec();
     double* Tmp = S.vec();
     double* sm = S.small(8 * 32 * 32);
-    double *M1 = sm, *RR = sm + 1024, *al = sm + 2048, *RtT = sm + 3072, *be = sm + 4096, *ts = sm + 5120,
-           *tt = sm + 5120 + 32, *nr = sm + 5120 + 64, *LUf = sm + 6144;
+    // the outputs of one reduction pass are adjacent ([M1 RR], [RtT ts tt]): with p > 1 each
+    // pass is summed by ONE allreduce (Solver::reduce_outputs)
+    double *M1 = sm, *RR = sm + k * k, *RtT = sm + 2048, *ts = RtT + k * k, *tt = ts + k, *al = sm + 3200,
+           *be = sm + 4224, *nr = sm + 5248, *LUf = sm + 6144;
     int* piv = reinterpret_cast<int*>(sm + 7168);
     TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
     TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));

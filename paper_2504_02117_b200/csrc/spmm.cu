@@ -391,7 +391,7 @@ void launch_pipe(const SpmmArgs& a, int num_sms, cudaStream_t st) {
                              cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         attr = true;
     }
-    const int64_t cap = (int64_t)MINB * num_sms;
+    const int64_t cap = (int64_t)MINB * (a.grid_sms > 0 && a.grid_sms < num_sms ? a.grid_sms : num_sms);
     const int64_t grid = ntiles < cap ? ntiles : cap;
     SpmmArgs b = a;
     if (b.sl_S > 0) {   // slab order needs whole tiles per line and a permutation of all tiles
@@ -912,7 +912,8 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
                              227 * 1024);
         attr = true;
     }
-    const int64_t cap = (int64_t)ctas * num_sms_cached();
+    const int nsm = num_sms_cached();
+    const int64_t cap = (int64_t)ctas * (a.grid_sms > 0 && a.grid_sms < nsm ? a.grid_sms : nsm);
     const int64_t grid = ntiles < cap ? ntiles : cap;
     BK_KERNEL(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT><<<(unsigned)grid, NC + 32, smem, st>>>(w));
     return true;
