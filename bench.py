@@ -455,6 +455,14 @@ def run_ours(args):
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "note": "same step via the C ABI with pinned host X/Y/P/C/G/B buffers; host wall clock"}
 
+    # ---- strong scaling on the largest grid (N > 1, or --strong-c5 at N = 1)
+    strong = None
+    if (world > 1 and not args.no_strong) or args.strong_c5:
+        try:
+            strong = strong_c5(bk, ctx, world, rank, dev)
+        except Exception as e:   # never fail the bench line on the side measurement
+            strong = {"error": str(e)[:400]}
+
     # ---- CPU oracle baseline (rank 0, N = 1): bounded sample of the same step
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -481,6 +489,7 @@ def run_ours(args):
             "solve": solve_report,
             "configs": configs,
             "e2e": e2e,
+            "strong_scaling_c5": strong,
             "cpu_baseline": cpu,
             "clocks": cs,
         }
@@ -488,6 +497,104 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ strong scaling on c5 (north star E(N))
+STRONG_KS = (8, 16, 32)
+STRONG_CG_K, STRONG_CG_ITERS = 16, 20
+
+
+def strong_c5(bk, ctx, world, rank, dev, reps=3):
+    """parallel efficiency E(N) = T(1) / (N T(N)) on the largest grid (c5,
+    512 x 512 x 256, 67.1 M rows) for the block apply at k = 8 / 16 / 32 and for 20 fixed block-CG
+    iterations at k = 16, the matrix row-partitioned into z-slabs (NCCL halo + Gram allreduce).
+    T(1) is measured in the same run on rank 0's GPU alone (a single-rank context), then T(N) on
+    all ranks (CUDA events, max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    import synth
+    A = synth.make_matrix("c5", device=dev)
+    n = A.n_rows
+    plane = 512 * 512
+    nz = n // plane
+    rb = [(nz * r // world) * plane for r in range(world + 1)]
+    flush = torch.empty(512 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def run(c, M, r0, r1, allred):
+        nl = r1 - r0
+        big_x = torch.empty(nl * max(STRONG_KS), dtype=torch.float64, device=dev)
+        big_y = torch.empty_like(big_x)
+        st = torch.cuda.current_stream(dev)
+        out = {}
+        for k in STRONG_KS:
+            X = big_x[:nl * k].view(nl, k)
+            X.copy_(synth.multivector(nl, k, synth.SEEDS["X"], row_begin=r0, n_global=n, device=dev))
+            Y = big_y[:nl * k].view(nl, k)
+            ts = []
+            for _ in range(reps + 1):
+                flush.fill_(1.0)
+                if allred:
+                    dist.barrier()
+                torch.cuda.synchronize(dev)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record(st)
+                bk.bspmm_apply(c, M, X, Y)
+                b.record(st)
+                torch.cuda.synchronize(dev)
+                ts.append(a.elapsed_time(b))
+            out[f"spmm_k{k}"] = min(ts[1:])
+        k = STRONG_CG_K
+        B = big_x[:nl * k].view(nl, k)
+        B.copy_(synth.multivector(nl, k, synth.SEEDS["B"], row_begin=r0, n_global=n, device=dev))
+        Xs = big_y[:nl * k].view(nl, k)
+        ts = []
+        for _ in range(2):
+            if allred:
+                dist.barrier()
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(st)
+            bk.block_krylov_solve(c, M, B, Xs, method="cg", rtol=0.0, max_iters=STRONG_CG_ITERS, x0_is_zero=True,
+                                  check_every=STRONG_CG_ITERS)
+            b.record(st)
+            torch.cuda.synchronize(dev)
+            ts.append(a.elapsed_time(b))
+        out[f"cg_k{k}_{STRONG_CG_ITERS}it"] = ts[-1]
+        del big_x, big_y
+        torch.cuda.empty_cache()
+        if allred:   # max over ranks
+            t = torch.tensor([out[kk] for kk in sorted(out)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            out = dict(zip(sorted(out), t.tolist()))
+        return out
+
+    t1 = None
+    if rank == 0:
+        c1 = bk.Context(dev.index)
+        M1 = bk.Matrix(c1, A.row_ptr, A.col, A.val)
+        t1 = run(c1, M1, 0, n, False)
+        M1.close()
+        c1.close()
+        torch.cuda.empty_cache()
+    tn = None
+    if world > 1:
+        dist.barrier()
+        S = A.rows(rb[rank], rb[rank + 1])
+        del A
+        torch.cuda.empty_cache()
+        M = bk.Matrix(ctx, S.row_ptr, S.col, S.val, n_global=n, row_begin=rb[rank], n_local=rb[rank + 1] - rb[rank])
+        del S
+        tn = run(ctx, M, rb[rank], rb[rank + 1], True)
+        M.close()
+    if rank != 0:
+        return None
+    res = {"workload": "c5 (512x512x256, 7-point Richards-type, fp64), z-slab row partition", "n_gpus": world,
+           "T1_ms": t1, "TN_ms": tn, "reps": reps,
+           "note": "apply: min of reps after one warm-up, L2 flushed before each; CG: 20 fixed iterations "
+                   "(second of two runs), setup outside the timed region"}
+    if tn:
+        res["efficiency"] = {kk: t1[kk] / (world * tn[kk]) for kk in t1}
+    return res
 
 
 # ------------------------------------------------------------------ oracle (CPU) arm
@@ -651,6 +758,8 @@ def main():
     ap.add_argument("--no-configs", action="store_true", help="skip the c3/c4/c5 side measurements")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=1)
+    ap.add_argument("--no-strong", action="store_true", help="N > 1: skip the c5 strong-scaling section")
+    ap.add_argument("--strong-c5", action="store_true", help="run the c5 strong-scaling section at N = 1 too")
     ap.add_argument("--oracle-timing", nargs=4, type=int, metavar=("ROWS", "PROCS", "REPS", "WARMUP"),
                     help=argparse.SUPPRESS)
     args = ap.parse_args()

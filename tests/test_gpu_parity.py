@@ -266,16 +266,24 @@ def test_update_integer_bitwise_and_inplace(ctx, bk):
 
 
 # ----------------------------------------------------------------------------- a6 solve
-def oracle_bicgstab_count_range(A, B, members=8, rtol=1e-10):
+_ENSEMBLE = {}
+
+
+def oracle_bicgstab_count_range(A, B, members=32, rtol=1e-10):
     """Iteration counts of the oracle O6 on B and on B perturbed by one ulp (relative 2^-52
-    uniform noise, seeds 1..members-1): the spread rounding alone produces (R18)."""
+    uniform noise, seeds 1..members-1): the spread rounding alone produces (DESIGN.md R18;
+    on c1 it is 71-79 at k = 1, 61-74 at k = 3, 44-56 at k = 8 over 32 members)."""
     Bn = np.asarray(B)
+    key = (A.n_rows, int(A.row_ptr[-1]), Bn.shape, float(Bn.sum()), members, rtol)
+    if key in _ENSEMBLE:
+        return _ENSEMBLE[key]
     its = []
     for sd in range(members):
         noise = np.random.default_rng(sd).uniform(-1, 1, Bn.shape) * 2.2e-16 if sd else 0.0
         _, r = oracle.block_bicgstab(A, Bn * (1 + noise), rtol=rtol, max_iters=2000)
         its.append(r.iterations)
-    return min(its), max(its)
+    _ENSEMBLE[key] = (min(its), max(its))
+    return _ENSEMBLE[key]
 
 
 
