@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(HERE, "build")
 LIB = os.path.join(HERE, "lib", "libbk.so")
-SOURCES = ["spmm.cu", "blas.cu", "gram_mma.cu", "stream.cu", "dense.cu", "dense_warp.cu", "abi.cpp", "solve.cpp", "comm.cpp", "window.cpp", "dirk.cpp", "wide.cu", "nonlin.cu", "alg1.cpp"]
+SOURCES = ["spmm.cu", "blas.cu", "gram_mma.cu", "stream.cu", "dense.cu", "dense_warp.cu", "abi.cpp", "solve.cpp", "comm.cpp", "window.cpp", "dirk.cpp", "wide.cu", "nonlin.cu", "alg1.cpp", "flat.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -169,8 +169,9 @@ extern "C" int bk_ctx_create(bk_ctx** out, int device, void* cuda_stream) {
     cudaEventCreateWithFlags(&c->ev_a, cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_b, cudaEventDisableTiming);
     cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-    if (cudaMalloc(&c->d_tickets, 64 * sizeof(int)) != cudaSuccess ||
-        cudaMemset(c->d_tickets, 0, 64 * sizeof(int)) != cudaSuccess) {
+    // last-CTA tickets: [0, 33) stream Grams, [32, 65) column dots, 96 flat Grams
+    if (cudaMalloc(&c->d_tickets, 128 * sizeof(int)) != cudaSuccess ||
+        cudaMemset(c->d_tickets, 0, 128 * sizeof(int)) != cudaSuccess) {
         cudaGetLastError();
         delete c;
         return BK_ERR_CUDA;
@@ -562,7 +563,11 @@ int gram_dev(bk_ctx* ctx, int64_t n, int ka, int kb, const double* X, int64_t ld
     if (n > 0 && use_stream_kernels())
         spart = (double*)ws_get(ctx, WS_GRAM_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double));
     const bool wide = n > 0 && ka >= 16 && (ka > 32 || ldx != ka || ldy != kb);
-    if (wide && launch_gram_wide(n, ka, kb, X, ldx, Y, ldy, G,
+    if (n > 0 && launch_gram_flat(n, ka, kb, X, ldx, Y, ldy, G,
+                                  (double*)ws_get(ctx, WS_GRAM_PART + 34, flat_part_doubles(ctx->num_sms) * sizeof(double)),
+                                  ctx->d_tickets + 96, ctx->num_sms, ctx->stream)) {
+        // k <= 4: flat grid-stride Gram (flat.cu)
+    } else if (wide && launch_gram_wide(n, ka, kb, X, ldx, Y, ldy, G,
                                  (double*)ws_get(ctx, WS_GRAM_PART + 33,
                                                  gram_wide_ws_doubles(ka, kb, ctx->num_sms) * sizeof(double)),
                                  ctx->num_sms, ctx->stream)) {

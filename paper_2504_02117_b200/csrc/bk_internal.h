@@ -118,6 +118,11 @@ bool launch_coldot_stream(int64_t n, int k, const double* X, int64_t ldx, const 
                           const double* Y2, int64_t ldy2, double* d, double* d2, double* part, int* ticket,
                           int num_sms, cudaStream_t st);
 bool use_stream_kernels();
+// k <= 4 Gram / update without the TMA ring (flat.cu); false = not applicable
+size_t flat_part_doubles(int num_sms);
+bool launch_gram_flat(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
+                      double* G, double* part, int* ticket, int num_sms, cudaStream_t st);
+bool launch_update_flat(const UpdArgs& u, int num_sms, cudaStream_t st);
 // Wide / strided multi-Gram and multi-update (wide.cu; GMRES basis, ld = (m+1)k).
 size_t gram_wide_ws_doubles(int ka, int kb, int num_sms);
 bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, const double* W, int64_t ldw,

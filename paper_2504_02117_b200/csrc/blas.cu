@@ -421,6 +421,7 @@ void launch_update(const UpdArgs& a, cudaStream_t st) {
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
     }
+    if (launch_update_flat(a, nsm, st)) return;   // k, kp <= 4 (flat.cu)
     if (use_stream_kernels() && launch_update_stream(a, nsm, st)) return;
     // strided or wide P (GMRES basis): cp.async-staged DMMA multi-update
     if (a.kp >= 4 && !a.W && (a.kp > 32 || a.ldp != a.kp || a.ldo != a.k) && launch_update_wide(a, st)) return;

@@ -229,3 +229,37 @@ def test_bicgstab_fused_vs_unfused_iteration_count(k):
     lo, hi = tp.oracle_bicgstab_count_range(A, synth.multivector(A.n_rows, k, 2))
     assert lo - 1 <= i1 <= hi + 1 and lo - 1 <= i0 <= hi + 1, (i1, i0, lo, hi)
     assert np.linalg.norm(x1 - x0) / np.linalg.norm(x0) <= 1e-8
+
+
+# ----------------------------------------------------------------------------- narrow (k <= 4) flat kernels
+@pytest.mark.parametrize("ka,kb", [(1, 1), (2, 3), (3, 3), (4, 4), (4, 1), (1, 2)])
+def test_flat_gram_narrow(ctx, bk, ka, kb):
+    """k <= 4 Grams take the flat grid-stride kernel (flat.cu): R17 bar on random data at c2 size,
+    bitwise on integers, bitwise reproducible run to run."""
+    n = 1024 * 1024 + 17
+    X = synth.multivector(n, ka, 3, device="cuda")
+    Y = synth.multivector(n, kb, 4, device="cuda")
+    G = torch.empty(ka, kb, dtype=torch.float64, device="cuda")
+    bk.block_gram(ctx, X, Y, G)
+    G2 = torch.empty_like(G)
+    bk.block_gram(ctx, X, Y, G2)
+    assert torch.equal(G, G2)
+    Xc, Yc = X.cpu(), Y.cpu()
+    check_close(G.cpu().numpy(), oracle.gram(Xc, Yc), oracle.gram(Xc.abs(), Yc.abs()), what=f"flat gram {ka}x{kb}")
+    Xi = synth.multivector(n, ka, 3, integer=True)
+    Gi = torch.empty(ka, ka, dtype=torch.float64, device="cuda")
+    bk.block_gram(ctx, Xi.cuda(), Xi.cuda(), Gi)
+    ref = (Xi.numpy().astype(np.int64).T @ Xi.numpy().astype(np.int64)).astype(np.float64)
+    assert np.array_equal(Gi.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("kp,k", [(1, 1), (2, 2), (4, 4), (1, 3), (4, 1), (3, 2)])
+def test_flat_update_narrow(ctx, bk, kp, k):
+    n = 1024 * 1024 + 5
+    X0 = synth.multivector(n, k, 3, integer=True)
+    P = synth.multivector(n, kp, 5, integer=True)
+    C = synth.small_dense(kp, k, 6, integer=True)
+    for a, s in ((1.0, 1.0), (0.0, -1.0), (2.0, 0.5)):
+        X = X0.cuda()
+        bk.block_update(ctx, X, P.cuda(), C.cuda(), a=a, s=s)
+        assert np.array_equal(X.cpu().numpy(), oracle.update(X0, P, C, a, s)), (kp, k, a, s)
