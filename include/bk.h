@@ -284,6 +284,28 @@ int bk_dirk_solve_dc(bk_ctx *ctx, const bk_csr *L, const bk_csr *K, double mass,
                      double *Y, int64_t ldy, int max_outer, double outer_tol,
                      const bk_solve_opts *inner, bk_dirk_report *rep);
 
+/* Window matrices of NEXT-1 from a Butcher tableau (host only, no GPU; §2.1): s
+ * consecutive time steps of the diagonally implicit, stiffly accurate tableau A (m x m,
+ * row-major, lower triangular, c = A 1) as one matrix equation with k = s m' columns
+ * (R24): A2 = I_s (x) A', A1 = I / tau, A1[q m' + i][q m' - 1] = -1/tau
+ * for q >= 1.  An explicit first stage (a_11 = 0, e.g. the Theta-method) is eliminated first
+ * (P:128-213): A' = A[1:, 1:], m' = m - 1, and its column a_{i1} couples each step to the
+ * previous step's last stage: A2[q m' + i][q m' - 1] = a_{i+1,1} for q >= 1 (the
+ * q = 0 coupling is the B0 term of bk_dirk_b0).  Only the first stage may be explicit.
+ * A1, A2: caller-allocated k x k (k <= BK_MAX_K) row-major, overwritten.  a_elim: NULL or m'
+ * doubles, receives (a_21, ..., a_m1) (zeros without an eliminated stage).  *k_out = k.
+ * Returns BK_OK or BK_ERR_ARG (not DIRK, a later explicit stage, tau <= 0, k > 32).          */
+int bk_dirk_window(int m, const double *A, int s, double tau, int *k_out, double *A1, double *A2,
+                   double *a_elim);
+/* B0 of that window, computed on the device: column i < m' equals
+ * (mass / tau) y^n + a_{i+1,1} (b^n - K y^n) (the second term only for an eliminated explicit
+ * first stage; one apply of K), the other columns are 0.  K: the stiffness matrix (same
+ * partition as the window's unknowns; collective for nranks > 1).  y^n, b^n: n_local doubles
+ * (host or device; b^n may be NULL = 0).  B0: n_local x k (ld ldb >= k), host or device,
+ * overwritten.  Returns BK_OK or an error status.                                          */
+int bk_dirk_b0(bk_ctx *ctx, const bk_csr *K, double mass, double tau, int m, const double *A, int s,
+               const double *yn, const double *bn, double *B0, int64_t ldb);
+
 /* NEXT-3: Algorithm 1 "Block Krylov Time Stepping with Pipelining" (§2.2
  * P:600-621; eq. matrix-equation-pipelining; shift P:592-594; iota P:574-580)
  * on the nonlinear diffusion-reaction problem M y' + f(t, y) = 0 of an nx x ny x nz

@@ -525,6 +525,22 @@ def dirk_sequential(K, mass, A_tab, Bcols, y_n, tau, s):
     return Y
 
 
+def theta_stepping(K, mass, theta, b, y0, tau, s):
+    """Closed-form Theta scheme, Example ex:time-stepping-matrices:
+    (M/tau + Theta K) y^{q+1} = Theta b^{q+1} + M y^q / tau + (1 - Theta)(b^q - K y^q), q = 0..s-1,
+    M = mass I; b[:, q] = b(t^q) for q = 0..s.  Returns Y (N x s), column q = y^{q+1}.  Dense solves."""
+    Kd = _dense(K)
+    N = Kd.shape[0]
+    b = _np(b, np.float64)
+    y = _np(y0, np.float64).reshape(N).copy()
+    Y = np.zeros((N, s))
+    for q in range(s):
+        y = np.linalg.solve(mass / tau * np.eye(N) + theta * Kd,
+                            theta * b[:, q + 1] + mass / tau * y + (1.0 - theta) * (b[:, q] - Kd @ y))
+        Y[:, q] = y
+    return Y
+
+
 def dirk_all_at_once(K, mass, A1, A2, B, B0):
     """Eq. (general-system-time-steps), P:104-126 with the window matrices of P:260-288:
     [A1 (x) M + A2 (x) K] vec(Y) = [A2 (x) I_N] vec(B) + vec(B0), vec = column stacking

@@ -39,7 +39,7 @@ EXPORTED = ["bk_version", "bk_kernel_launch_count", "bk_status_string", "bk_last
             "bk_ctx_comm_info", "bk_csr_create", "bk_csr_destroy", "bk_csr_get_info", "bspmm_apply",
             "block_gram", "block_update", "bk_solve_opts_default", "block_krylov_solve", "bk_plan_halo",
             "bk_plan_bands", "bk_dirk_solve", "bk_precond_apply", "bk_alg1_run", "bk_dirk_solve_dc",
-            "bk_local_hub_create", "bk_local_hub_destroy", "bk_ctx_set_comm_local"]
+            "bk_local_hub_create", "bk_local_hub_destroy", "bk_ctx_set_comm_local", "bk_dirk_window", "bk_dirk_b0"]
 
 
 class SolveOpts(ctypes.Structure):
@@ -83,6 +83,8 @@ _sig = {
     "bk_get_nccl_unique_id": ([_P], _I),
     "bk_ctx_set_comm": ([_P, _P, _I, _I], _I),
     "bk_ctx_comm_info": ([_P, ctypes.POINTER(_I), ctypes.POINTER(_I)], _I),
+    "bk_dirk_window": ([_I, _P, _I, _D, ctypes.POINTER(_I), _P, _P, _P], _I),
+    "bk_dirk_b0": ([_P, _P, _D, _D, _I, _P, _I, _P, _P, _P, _I64], _I),
     "bk_local_hub_create": ([ctypes.POINTER(_P), _I], _I),
     "bk_local_hub_destroy": ([_P], _I),
     "bk_ctx_set_comm_local": ([_P, _P, _I], _I),
@@ -478,6 +480,50 @@ def plan_bands(row_ptr, col, max_extra: int = 96) -> dict:
     return {"nbands": g, "extra_rows": pl.extra_rows, "max_row_nnz": pl.max_row_nnz,
             "dmin": list(pl.dmin[:g]), "dmax": list(pl.dmax[:g]), "width": list(pl.width[:g]),
             "lo": list(pl.lo[:g]), "hi": list(pl.hi[:g])}
+
+
+def dirk_window(A_tab, s: int, tau: float):
+    """Window matrices of s steps of a DIRK tableau (bk_dirk_window, host only): returns
+    (A1, A2, a_elim) as numpy arrays (k x k, k x k, m'), k = s m' (m' = m - 1 when the first
+    stage is explicit and eliminated)."""
+    A = np.ascontiguousarray(np.asarray(A_tab, dtype=np.float64))
+    m = A.shape[0]
+    A1 = np.zeros((BK_MAX_K, BK_MAX_K))
+    A2 = np.zeros((BK_MAX_K, BK_MAX_K))
+    ae = np.zeros(max(m, 1))
+    k = _I()
+    st = _lib.bk_dirk_window(m, A.ctypes.data, int(s), float(tau), ctypes.byref(k), A1.ctypes.data, A2.ctypes.data,
+                             ae.ctypes.data)
+    if st:
+        raise BkError(st, "bk_dirk_window: not a DIRK tableau with at most an explicit first stage, or k > 32")
+    kk = k.value
+    mi = kk // int(s)
+    return (A1.reshape(-1)[:kk * kk].reshape(kk, kk).copy(), A2.reshape(-1)[:kk * kk].reshape(kk, kk).copy(),
+            ae[:mi].copy())
+
+
+def dirk_b0(ctx: Context, K: Matrix, mass: float, tau: float, A_tab, s: int, yn, bn, B0):
+    """B0 of the window (bk_dirk_b0): yn, bn (n-vectors or None) and B0 (n x k) host or device."""
+    A = np.ascontiguousarray(np.asarray(A_tab, dtype=np.float64))
+    keep = []
+    if _is_torch(yn):
+        py = yn.data_ptr()
+    else:
+        ya = np.ascontiguousarray(yn, dtype=np.float64)
+        keep.append(ya)
+        py = ya.ctypes.data
+    if bn is None:
+        pb = None
+    elif _is_torch(bn):
+        pb = bn.data_ptr()
+    else:
+        arr = np.ascontiguousarray(bn, dtype=np.float64)
+        keep.append(arr)
+        pb = arr.ctypes.data
+    p0, n0, k0, ld0 = _mv(B0, "B0")
+    ctx.check(_lib.bk_dirk_b0(ctx.handle, K.handle, float(mass), float(tau), A.shape[0], A.ctypes.data, int(s),
+                              _P(py), _P(pb), _P(p0), ld0), "bk_dirk_b0")
+    return B0
 
 
 class DirkReport(ctypes.Structure):

@@ -826,6 +826,36 @@ extern "C" int bk_dirk_solve(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, doub
     return dirk_entry(ctx, L, K, mass, tau, k, A1, A2, B, B0, ldb, Y, ldy, max_outer, outer_tol, inner, rep, false);
 }
 
+extern "C" int bk_dirk_b0(bk_ctx* ctx, const bk_csr* K, double mass, double tau, int m, const double* A, int s,
+                          const double* yn, const double* bn, double* B0, int64_t ldb) {
+    int r = enter(ctx);
+    if (r) return r;
+    ARG_CHECK(ctx, K && K->ctx == ctx, "bk_dirk_b0: matrix NULL or from another ctx");
+    int k = 0;
+    std::vector<double> A1((size_t)BK_MAX_K * BK_MAX_K), A2((size_t)BK_MAX_K * BK_MAX_K);
+    ARG_CHECK(ctx, A && !is_device_ptr(A) && m >= 1 && m <= BK_MAX_K && s >= 1 && s <= BK_MAX_K,
+              "bk_dirk_b0: A must be a host m x m tableau");
+    ARG_CHECK(ctx, bk_dirk_window(m, A, s, tau, &k, A1.data(), A2.data(), nullptr) == BK_OK,
+              "bk_dirk_b0: bad tableau / s / tau (see bk_dirk_window)");
+    ARG_CHECK(ctx, mass >= 0.0 && ldb >= k, "bk_dirk_b0: need mass >= 0 and ldb >= k");
+    ARG_CHECK(ctx, K->n_local == 0 || (yn && B0), "bk_dirk_b0: NULL y^n / B0");
+    BK_TRY
+    const int64_t n = K->n_local;
+    bool yh, bh = false;
+    const double* dy = stage_in(ctx, WS_STAGE_X, yn, n, 1, &yh);
+    const double* db = bn ? stage_in(ctx, WS_STAGE_C, bn, n, 1, &bh) : nullptr;
+    const bool oh = !is_device_ptr(B0);
+    double* dB0 = oh ? (double*)ws_get(ctx, WS_STAGE_Y, (size_t)std::max<int64_t>(n, 1) * ldb * sizeof(double)) : B0;
+    double* scratch = (double*)ws_get(ctx, WS_STAGE_G, (size_t)(n + 2 * BK_MAX_K) * sizeof(double));
+    r = dirk_b0_impl(ctx, K, mass, tau, m, A, s, dy, db, dB0, ldb, scratch);
+    if (r) return r;
+    if (oh && n)
+        CUDA_OK(ctx, cudaMemcpyAsync(B0, dB0, (size_t)n * ldb * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+    CUDA_OK(ctx, cudaStreamSynchronize(ctx->stream));
+    return BK_OK;
+    BK_CATCH(ctx)
+}
+
 extern "C" int bk_dirk_solve_dc(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k,
                                 const double* A1, const double* A2, const double* B, const double* B0, int64_t ldb,
                                 double* Y, int64_t ldy, int max_outer, double outer_tol, const bk_solve_opts* inner,

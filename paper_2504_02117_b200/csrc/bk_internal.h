@@ -318,6 +318,8 @@ int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::
                    const std::vector<int32_t>& colg);
 int solve_impl(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb, double* X,
                int64_t ldx, const bk_solve_opts* o, bk_solve_report* rep);
+int dirk_b0_impl(bk_ctx* ctx, const bk_csr* K, double mass, double tau, int m, const double* A, int s,
+                 const double* yn, const double* bn, double* B0, int64_t ldb, double* scratch);
 int dirk_impl(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double tau, int k, const double* A1h,
               const double* A2h, const double* B, const double* B0, int64_t ldb, double* Y, int64_t ldy,
               int max_outer, double outer_tol, const bk_solve_opts* inner, bk_dirk_report* rep, bool correction = false);

@@ -200,3 +200,80 @@ int dirk_impl(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass, double
 }
 
 }  // namespace bk
+
+// ---------------------------------------------------------------- window matrices (host only)
+// PAPER.md §2.1: s consecutive steps of a stiffly accurate DIRK tableau A (m x m) as one matrix
+// equation (window matrices P:260-288, R24); an explicit first stage (a_11 = 0) is
+// eliminated first: its row goes, its column a_{i1} couples the remaining stages to
+// y^(n,1) = y^n -- for step q >= 1 that is the last stage of step q-1 (an A2 entry at the
+// position of A1's -1/tau), for step 0 a B0 term (bk_dirk_b0).
+namespace {
+bool dirk_tableau_ok(int m, const double* A, bool* expl) {
+    if (m < 1 || !A) return false;
+    for (int i = 0; i < m; ++i)
+        for (int j = i + 1; j < m; ++j)
+            if (A[i * m + j] != 0.0) return false;   // diagonally implicit: lower triangular
+    *expl = A[0] == 0.0;
+    if (*expl && m == 1) return false;
+    for (int i = *expl ? 1 : 0; i < m; ++i)
+        if (A[i * m + i] == 0.0) return false;        // only the first stage may be explicit
+    return true;
+}
+}  // namespace
+
+extern "C" int bk_dirk_window(int m, const double* A, int s, double tau, int* k_out, double* A1, double* A2,
+                              double* a_elim) {
+    bool expl = false;
+    if (!dirk_tableau_ok(m, A, &expl) || s < 1 || !(tau > 0.0) || !k_out || !A1 || !A2) return BK_ERR_ARG;
+    const int o = expl ? 1 : 0, mi = m - o, k = s * mi;
+    if (k > BK_MAX_K) return BK_ERR_ARG;
+    std::memset(A1, 0, sizeof(double) * k * k);
+    std::memset(A2, 0, sizeof(double) * k * k);
+    for (int q = 0; q < s; ++q)
+        for (int i = 0; i < mi; ++i) {
+            const int row = q * mi + i;
+            A1[row * k + row] = 1.0 / tau;
+            for (int j = 0; j <= i; ++j) A2[row * k + q * mi + j] = A[(i + o) * m + (j + o)];
+            if (q >= 1) {
+                A1[row * k + q * mi - 1] = -1.0 / tau;
+                if (expl) A2[row * k + q * mi - 1] = A[(i + 1) * m];
+            }
+        }
+    if (a_elim)
+        for (int i = 0; i < mi; ++i) a_elim[i] = expl ? A[(i + 1) * m] : 0.0;
+    *k_out = k;
+    return BK_OK;
+}
+
+namespace bk {
+// B0 of the window (device): columns i < mi = (mass/tau) y^n + a_{i1} (b^n - K y^n) (the second
+// term only for an eliminated explicit first stage), the other columns 0.  P:282-285.
+int dirk_b0_impl(bk_ctx* ctx, const bk_csr* K, double mass, double tau, int m, const double* A, int s,
+                 const double* yn, const double* bn, double* B0, int64_t ldb, double* scratch) {
+    bool expl = false;
+    dirk_tableau_ok(m, A, &expl);
+    const int mi = expl ? m - 1 : m, k = s * mi;
+    const int64_t n = K->n_local;
+    cudaStream_t st = ctx->stream;
+    int r = cuda_check(ctx, cudaMemset2DAsync(B0, ldb * sizeof(double), 0, k * sizeof(double), n, st), "dirk b0");
+    if (r || n == 0) return r;
+    // k x k coefficient rows (device): c_y = (mass / tau, ...), c_e = (a_21, ..., a_m1)
+    std::vector<double> h(2 * mi);
+    for (int i = 0; i < mi; ++i) {
+        h[i] = mass / tau;
+        h[mi + i] = expl ? A[(i + 1) * m] : 0.0;
+    }
+    double* dc = scratch + n;   // scratch: n doubles (K y^n) + 2 mi coefficients
+    r = cuda_check(ctx, cudaMemcpyAsync(dc, h.data(), sizeof(double) * 2 * mi, cudaMemcpyHostToDevice, st), "dirk b0");
+    if (r) return r;
+    upd(ctx, n, mi, B0, ldb, 0.0, nullptr, 0, 1.0, yn, 1, 1, dc);            // (mass / tau) y^n
+    if (expl) {
+        r = spmm_dev(ctx, K, 1, yn, 1, nullptr, 1, 1.0, 0.0, scratch, 1);    // K y^n
+        if (r) return r;
+        if (bn) upd(ctx, n, mi, B0, ldb, 1.0, B0, ldb, 1.0, bn, 1, 1, dc + mi);
+        upd(ctx, n, mi, B0, ldb, 1.0, B0, ldb, -1.0, scratch, 1, 1, dc + mi);
+    }
+    return cuda_check(ctx, cudaGetLastError(), "dirk b0");
+}
+}  // namespace bk
+

@@ -89,17 +89,28 @@ __global__ void __launch_bounds__(FT) gram_flat_kernel(int64_t n, const double* 
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // last block: output o summed by the 16 lanes (o, j) over partials j, j + 16, ... in order,
-    // then a fixed xor tree over the 16 lanes
-    const int o = threadIdx.x >> 4, j = threadIdx.x & 15;
-    for (int ob = 0; ob < NO; ob += FT / 16) {
-        const int oo = ob + o;
-        double v = 0.0;
-        if (oo < NO)
-            for (int b = j; b < (int)gridDim.x; b += 16) v += __ldcg(part + (int64_t)b * NO + oo);
+    // last block: thread t sums partial rows t, t + FT, ... (every output at once: one batch of
+    // independent loads), then the same fixed shuffle / warp-order tree as above
+    double f[NO];
 #pragma unroll
-        for (int m = 8; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
-        if (oo < NO && j == 0) G[oo] = v;
+    for (int q = 0; q < NO; ++q) f[q] = 0.0;
+    for (int b = threadIdx.x; b < (int)gridDim.x; b += FT)
+#pragma unroll
+        for (int q = 0; q < NO; ++q) f[q] += __ldcg(part + (int64_t)b * NO + q);
+    __syncthreads();   // s_w reused
+#pragma unroll
+    for (int q = 0; q < NO; ++q) {
+        double v = f[q];
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) v += __shfl_xor_sync(0xffffffffu, v, m);
+        if (lane == 0) s_w[warp][q] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x < NO) {
+        double v = s_w[0][threadIdx.x];
+#pragma unroll
+        for (int w = 1; w < FT / 32; ++w) v += s_w[w][threadIdx.x];
+        G[threadIdx.x] = v;
     }
     if (threadIdx.x == 0) *ticket = 0;
 }

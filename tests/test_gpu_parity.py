@@ -688,3 +688,37 @@ def test_dirk_defect_correction_matches_sequential(ctx, bk, tab, s, method, irto
                             max_iters=500, restart=60)
     assert st == 0 and rep["last_change"] <= 1e-11, rep
     assert np.linalg.norm(Y.cpu().numpy() - Ys) / np.linalg.norm(Ys) <= 1e-8
+
+
+# ----------------------------------------------------------------------------- NEXT-1 window built by the library
+def test_dirk_window_from_library_theta_method(ctx, bk):
+    """The whole NEXT-1 pipeline from a Butcher tableau: bk_dirk_window (A1, A2 with the explicit first
+    stage eliminated), bk_dirk_b0 (B0 on the device, one apply of K, P:204-208 / P:329-333)
+    and bk_dirk_solve -- equal to s steps of the closed-form Theta scheme (oracle.theta_stepping)."""
+    import math
+    tau, theta, s, n = 0.05, 0.5, 4, 32
+    K = synth.convdiff2d(n, tau=float("inf"), gamma=1.0)
+    L = synth.convdiff2d(n, tau=tau, gamma=theta)                           # M/tau + Theta K
+    mass, N = (1.0 / n) ** 2, n * n
+    rng = np.random.default_rng(11)
+    f, g, y0 = rng.uniform(-1, 1, N), rng.uniform(-1, 1, N), rng.uniform(-1, 1, N)
+    b = np.stack([math.sin(1.0 + q * tau) * f + g for q in range(s + 1)], 1)
+    tab = [[0.0, 0.0], [1.0 - theta, theta]]
+    A1, A2, ae = bk.dirk_window(tab, s, tau)
+    MK, ML = bk.Matrix.from_csr(ctx, K), bk.Matrix.from_csr(ctx, L)
+    B0 = torch.full((N, s), float("nan"), dtype=torch.float64, device="cuda")
+    bk.dirk_b0(ctx, MK, mass, tau, tab, s, cu(torch.from_numpy(y0)), cu(torch.from_numpy(b[:, 0].copy())), B0)
+    Kd = oracle._dense(K)
+    B0r = np.zeros((N, s))
+    B0r[:, 0] = mass / tau * y0 + ae[0] * (b[:, 0] - Kd @ y0)
+    check_close(B0.cpu().numpy(), B0r, mass / tau * np.abs(y0)[:, None] + ae[0] * (np.abs(b[:, :1]) +
+                np.abs(Kd) @ np.abs(y0)[:, None]), what="dirk b0")
+    B0h = np.zeros((N, s))                                                   # host buffers, b^n = NULL
+    bk.dirk_b0(ctx, MK, mass, tau, tab, s, y0, None, B0h)
+    assert np.allclose(B0h[:, 0], mass / tau * y0 - ae[0] * (Kd @ y0), rtol=0, atol=1e-12 * np.abs(B0r).max())
+    Y = torch.zeros(N, s, dtype=torch.float64, device="cuda")
+    st, rep = bk.dirk_solve(ctx, ML, MK, mass, tau, A1, A2, cu(torch.from_numpy(b[:, 1:].copy())), B0, Y,
+                            method="gmres", rtol=1e-12, restart=100, max_iters=3000)
+    assert st == 0, rep
+    Yt = oracle.theta_stepping(K, mass, theta, b, y0, tau, s)
+    assert np.linalg.norm(Y.cpu().numpy() - Yt) / np.linalg.norm(Yt) <= 1e-8

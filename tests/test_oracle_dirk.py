@@ -66,6 +66,9 @@ def test_theta_window_equals_closed_form_theta_scheme():
         y = np.linalg.solve(mass / tau * np.eye(N) + theta * Kd,
                             theta * b[q + 1] + mass / tau * y + (1.0 - theta) * (b[q] - Kd @ y))
         assert np.abs(Ya[:, q] - y).max() <= 1e-12 * np.abs(y).max()
+    # oracle.theta_stepping is that recurrence (used by the library window tests)
+    Yt = oracle.theta_stepping(K, mass, theta, np.stack(b, 1), y0, tau, s)
+    assert np.abs(Ya - Yt).max() <= 1e-12 * np.abs(Yt).max()
 
 
 @pytest.mark.parametrize("tab,s", [("sdirk2", 2), ("sdirk3", 2)])
