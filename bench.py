@@ -412,6 +412,12 @@ def run_ours(args):
             solve_report[name + "_iterations"] = rep["iterations"]
             solve_report[name + "_max_true_relres"] = float(max(rep["true_relres"]))
 
+    if world == 1 and not args.no_sweep and not args.no_solves and solve_report is not None:
+        try:
+            solve_report.update(solve_benchmarks(bk, ctx, dev))
+        except Exception as e:   # never fail the bench line on the side measurement
+            solve_report["error"] = str(e)[:400]
+
     # ---- e2e: same step through the C ABI with pinned HOST buffers (H2D/D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -497,6 +503,68 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+# ------------------------------------------------------------------ full solves (the metric's "block-Krylov solve time")
+BCG_RHS = 128
+BCG_KS = (1, 2, 4, 8, 16, 32)
+
+
+def solve_benchmarks(bk, ctx, dev, bcg_grid=128):
+    """BASELINE.json's solve-time half of the metric, outside the timed region:
+    * c3 (BJ configs[2]): block GMRES(64), k = 12, rtol 1e-10, X0 = 0 -- time, block iterations,
+      recomputed true residual;
+    * the analog of the paper's Block-CG benchmark (Fig. bcgbenchmark): 128
+      right-hand sides solved k at a time (k = 1, 2, 4, 8, 16, 32) to a defect reduction of 1e-8 for
+      all of them, on the Richards-type stiffness matrix (the c4 recipe, R20/R21) at bcg_grid^3, block
+      CG preconditioned by the Chebyshev polynomial (R28; the paper uses AMG, out of scope): total time
+      and block iterations per chunk."""
+    import torch
+    import synth
+    out = {}
+    A = synth.make_matrix("c3", device=dev)
+    M = bk.Matrix.from_csr(ctx, A)
+    k = 12
+    B = synth.multivector(A.n_rows, k, synth.SEEDS["B"], device=dev)
+    X = torch.zeros_like(B)
+    bk.block_krylov_solve(ctx, M, B, X, method="gmres", restart=64, rtol=1e-10, max_iters=2, x0_is_zero=True)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    st, rep = bk.block_krylov_solve(ctx, M, B, X, method="gmres", restart=64, rtol=1e-10, max_iters=2000,
+                                    x0_is_zero=True, check_every=4)
+    b.record()
+    torch.cuda.synchronize()
+    out["c3_gmres64_k12"] = {"ms": a.elapsed_time(b), "block_iterations": rep["iterations"],
+                             "converged": rep["converged"], "max_true_relres": float(max(rep["true_relres"])),
+                             "rtol": 1e-10}
+    del M, A, B, X
+    torch.cuda.empty_cache()
+    n3 = bcg_grid
+    A = synth.richards3d(n3, n3, n3, device=dev)
+    M = bk.Matrix.from_csr(ctx, A)
+    Ball = synth.multivector(A.n_rows, BCG_RHS, synth.SEEDS["B"], device=dev)
+    rows = {}
+    for k in BCG_KS:
+        Bk = [Ball[:, c:c + k].contiguous() for c in range(0, BCG_RHS, k)]
+        Xk = torch.zeros_like(Bk[0])
+        bk.block_krylov_solve(ctx, M, Bk[0], Xk, method="cg", precond="chebyshev", cheb_steps=4, rtol=1e-8,
+                              max_iters=2, x0_is_zero=True)
+        its, worst = [], 0.0
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for Bc in Bk:
+            st, rep = bk.block_krylov_solve(ctx, M, Bc, Xk, method="cg", precond="chebyshev", cheb_steps=4,
+                                            rtol=1e-8, max_iters=5000, x0_is_zero=True, check_every=8)
+            its.append(rep["iterations"])
+            worst = max(worst, float(max(rep["true_relres"])))
+        b.record()
+        torch.cuda.synchronize()
+        rows[k] = {"ms": a.elapsed_time(b), "chunks": len(Bk), "iterations_per_chunk": sorted(set(its)),
+                   "max_true_relres": worst}
+    out["bcg128_richards"] = {"grid": f"{n3}^3", "rows": A.n_rows, "rhs": BCG_RHS, "rtol": 1e-8,
+                              "precond": "chebyshev(4 steps, Gershgorin interval)", "by_k": rows,
+                              "fastest_k": min(rows, key=lambda kk: rows[kk]["ms"])}
+    return out
 
 
 # ------------------------------------------------------------------ strong scaling on c5 (north star E(N))
@@ -759,6 +827,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-reps", type=int, default=1)
     ap.add_argument("--no-strong", action="store_true", help="N > 1: skip the c5 strong-scaling section")
+    ap.add_argument("--no-solves", action="store_true", help="skip the full-solve benchmarks (c3 GMRES, 128-RHS CG)")
     ap.add_argument("--strong-c5", action="store_true", help="run the c5 strong-scaling section at N = 1 too")
     ap.add_argument("--oracle-timing", nargs=4, type=int, metavar=("ROWS", "PROCS", "REPS", "WARMUP"),
                     help=argparse.SUPPRESS)

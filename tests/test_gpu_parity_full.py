@@ -263,3 +263,21 @@ def test_flat_update_narrow(ctx, bk, kp, k):
         X = X0.cuda()
         bk.block_update(ctx, X, P.cuda(), C.cuda(), a=a, s=s)
         assert np.array_equal(X.cpu().numpy(), oracle.update(X0, P, C, a, s)), (kp, k, a, s)
+
+
+def test_gmres64_full_solve_c3_recipe(ctx, bk):
+    """c3's solver (BJ configs[2]: block GMRES, k = 12) run to rtol 1e-10 with restart 64 on the c3
+    operator recipe at 24^3 (R16; the oracle's long-double Grams make the 128^3 solve too slow for a
+    test): solution within 1e-8 of the oracle O5, block iterations within 1 (R18)."""
+    A = synth.diffreact3d(24)
+    k = 12
+    B = synth.multivector(A.n_rows, k, synth.SEEDS["B"])
+    M = bk.Matrix.from_csr(ctx, A)
+    X = torch.zeros(A.n_rows, k, dtype=torch.float64, device="cuda")
+    st, rep = bk.block_krylov_solve(ctx, M, B.cuda(), X, method="gmres", restart=64, rtol=1e-10, max_iters=2000,
+                                    x0_is_zero=True)
+    Xr, rr = oracle.block_gmres(A, B, rtol=1e-10, max_iters=2000, restart=64)
+    assert st == 0 and rr.converged
+    assert abs(rep["iterations"] - rr.iterations) <= 1, (rep["iterations"], rr.iterations)
+    assert np.linalg.norm(X.cpu().numpy() - Xr) / np.linalg.norm(Xr) <= 1e-8
+    assert np.all(rep["true_relres"] <= 1e-9)
