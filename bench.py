@@ -510,7 +510,7 @@ BCG_RHS = 128
 BCG_KS = (1, 2, 4, 8, 16, 32)
 
 
-def solve_benchmarks(bk, ctx, dev, bcg_grid=128):
+def solve_benchmarks(bk, ctx, dev, bcg_grid=96):
     """BASELINE.json's solve-time half of the metric, outside the timed region:
     * c3 (BJ configs[2]): block GMRES(64), k = 12, rtol 1e-10, X0 = 0 -- time, block iterations,
       recomputed true residual;

@@ -702,7 +702,8 @@ def test_dirk_window_from_library_theta_method(ctx, bk):
     mass, N = (1.0 / n) ** 2, n * n
     rng = np.random.default_rng(11)
     f, g, y0 = rng.uniform(-1, 1, N), rng.uniform(-1, 1, N), rng.uniform(-1, 1, N)
-    b = np.stack([math.sin(1.0 + q * tau) * f + g for q in range(s + 1)], 1)
+    e = rng.uniform(-0.5, 0.5, (N, s + 1))                                   # R26: a full-rank block RHS
+    b = np.stack([math.sin(1.0 + q * tau) * f + g + e[:, q] for q in range(s + 1)], 1)
     tab = [[0.0, 0.0], [1.0 - theta, theta]]
     A1, A2, ae = bk.dirk_window(tab, s, tau)
     MK, ML = bk.Matrix.from_csr(ctx, K), bk.Matrix.from_csr(ctx, L)
