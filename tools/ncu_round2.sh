@@ -7,18 +7,26 @@
 # Each profiled command first exits 0 without ncu (the recipe in B200_PROFILING.md).
 set -u
 O=gpurun_out
+# reports are exported to CSV and deleted (gpurun brings back <= 64 MiB)
+export_rep() {
+    ncu -i $O/$1.ncu-rep --page raw --csv > $O/$1.raw.csv 2>/dev/null
+    ncu -i $O/$1.ncu-rep --page details --csv > $O/$1.details.csv 2>/dev/null
+    rm -f $O/$1.ncu-rep
+}
 STEP="python bench.py --profile-step --no-sweep --no-e2e --no-cpu-baseline --no-configs --steps 1 --warmup 3"
 $STEP > $O/r2_step_plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start off --csv \
     --log-file $O/r2_launches.csv $STEP > $O/r2_launches.log 2>&1
 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:bcg_tail -c 1 \
     -o $O/r2_bcg_tail $STEP > $O/r2_bcg_tail.log 2>&1
+export_rep r2_bcg_tail
 for cfg in "c2 16" "c2 32" "c3 12" "c5 16" "c5 32"; do
     set -- $cfg
     tag=r2_apply_$1_k$2
     python tools/one_apply.py --cfg $1 --k $2 --reps 2 > $O/$tag.plain.log 2>&1 && \
     ncu --set full --clock-control none --import-source on -k regex:bspmm -s 1 -c 1 -o $O/$tag \
         python tools/one_apply.py --cfg $1 --k $2 --reps 2 > $O/$tag.log 2>&1
+    export_rep $tag
 done
 SW="python tools/sweep.py --cfg c2 --ks 1,2,3,4 --ops gram,update --reps 2"
 $SW > $O/r2_small_plain.log 2>&1 && \
