@@ -442,6 +442,36 @@ extern "C" int bk_csr_get_info(const bk_csr* A, bk_csr_info* info) {
 
 // ------------------------------------------------------------------ a1 apply
 namespace bk {
+// 3-D lattices: y-slab tile order for the gather kernel (sets a.sl_*; no-op otherwise)
+static void slab_order(SpmmArgs& a, const BandPlan& bp_, int k) {
+    // 3-D lattice whose z-neighbour planes do not stay in L2 across two planes of streaming
+    // (c4 / c5: 256^2 / 512^2 planes): y-slab tile order.  S = the smallest power of two with
+    // 2 (ny / S) nx (16 k + 88) B <= 28 MB.  Round 1 (56 MB, 12 <= k <= 16 only): ncu c5 k = 16
+    // DRAM reads 20.3 -> 16.5 GB (14.5 algorithmic).  Round 2 (28 MB, every k):
+    // c5 k = 8 / 16 / 32 0.83 / 0.64 / 0.57 -> 0.84 / 0.76 / 0.66 of HBM, c4 0.86 / 0.71 / 0.64
+    // -> 0.87 / 0.75 / 0.68; ncu c5 k = 32 without it read X 1.9 times from DRAM.  BK_SLAB=0: off
+    static const int slab = env_int("BK_SLAB", 1);
+    const BandPlan& bp = bp_;
+    const bool slab_k = slab != 0;
+    if (slab_k && bp.nbands == 5 && bp.dmin[0] == bp.dmax[0] && bp.dmin[1] == bp.dmax[1] && bp.dmin[1] < 0 &&
+        bp.dmin[0] < bp.dmin[1] && a.row0 == bp.row0 && a.nrows == bp.nrows) {
+        const int64_t nx = -(int64_t)bp.dmin[1], plane = -(int64_t)bp.dmin[0];
+        if (plane % nx == 0 && a.nrows % plane == 0) {
+            const int64_t ny = plane / nx, nz = a.nrows / plane;
+            const double row_bytes = 16.0 * k + 88.0;
+            const double budget = 28.0 * 1024 * 1024;   // of the 126 MB L2 (two 63 MB partitions)
+            int S = 1;
+            while (2.0 * (double)(ny / S) * nx * row_bytes > budget && ny % (2 * S) == 0 && ny / (2 * S) >= 8)
+                S *= 2;
+            if (S > 1 && ny < (1 << 30) && nz < (1 << 30) && nx < (1 << 30)) {
+                a.sl_S = S; a.sl_tpl = (int)nx; a.sl_ny = (int)ny; a.sl_nz = (int)nz;
+            }
+        }
+    }
+}
+}  // namespace bk
+
+namespace bk {
 int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, const double* C, int kout,
              double alpha, double beta, double* Y, int64_t ldy) {
     SpmmArgs a{};
@@ -461,29 +491,7 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
     if (ctx->nranks == 1 || A->n_ghost == 0) {
         a.row0 = 0;
         a.nrows = A->n_local;
-        // 3-D lattice whose z-neighbour planes do not stay in L2 across two planes of streaming
-        // (c5: 512 x 512 planes): y-slab tile order.  ncu c5 k = 16: DRAM reads 20.3 -> 16.5 GB
-        // (14.5 GB algorithmic); three repeated sweeps: k = 16 0.665-0.675 -> 0.693-0.717 of
-        // HBM, k = 8 0.818 -> 0.812, k = 32 no gain.  Default 12 <= k <= 16 (BK_SLAB=0 off,
-        // 1 every k <= 16, 2 every k)
-        static const int slab = env_int("BK_SLAB", -1);
-        const BandPlan& bp = A->band;
-        const bool slab_k = slab == 2 || (slab == 1 && k <= 16) || (slab < 0 && k >= 12 && k <= 16);
-        if (slab_k && bp.nbands == 5 && bp.dmin[0] == bp.dmax[0] && bp.dmin[1] == bp.dmax[1] && bp.dmin[1] < 0 &&
-            bp.dmin[0] < bp.dmin[1] && a.row0 == bp.row0 && a.nrows == bp.nrows) {
-            const int64_t nx = -(int64_t)bp.dmin[1], plane = -(int64_t)bp.dmin[0];
-            if (plane % nx == 0 && a.nrows % plane == 0) {
-                const int64_t ny = plane / nx, nz = a.nrows / plane;
-                const double row_bytes = 16.0 * k + 88.0;
-                const double budget = 56.0 * 1024 * 1024;   // of the 126 MB L2
-                int S = 1;
-                while (2.0 * (double)(ny / S) * nx * row_bytes > budget && ny % (2 * S) == 0 && ny / (2 * S) >= 8)
-                    S *= 2;
-                if (S > 1 && ny < (1 << 30) && nz < (1 << 30) && nx < (1 << 30)) {
-                    a.sl_S = S; a.sl_tpl = (int)nx; a.sl_ny = (int)ny; a.sl_nz = (int)nz;
-                }
-            }
-        }
+        slab_order(a, A->band, k);
         if (!launch_bspmm_win(a, A->band, ctx->stream)) launch_bspmm(a, ctx->stream);
         return post_launch(ctx, "bspmm_apply");
     }
@@ -502,7 +510,9 @@ int spmm_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, int64_t ldx, 
         a.rows = A->d_interior_rows;
         a.nrows = A->n_interior;
     }
+    if (!a.rows) slab_order(a, A->band, k);
     if (!launch_bspmm_win(a, A->band, ctx->stream)) launch_bspmm(a, ctx->stream);
+    a.sl_S = 0;
     cudaStreamWaitEvent(ctx->stream, ctx->ev_b, 0);
     a.grid_sms = 0;
     a.rows = A->d_boundary_rows;

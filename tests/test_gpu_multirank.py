@@ -200,3 +200,26 @@ def test_partitioned_apply_empty_halo_and_host_buffers(bk):
     res = run_ranks(bk, P, fn)
     assert np.array_equal(np.concatenate([o[0] for o in res]), oracle.spmm(A, X))
     assert all(o[1]["n_ghost"] == 0 for o in res)
+
+
+@pytest.mark.parametrize("k", [12, 16])
+def test_partitioned_apply_slab_order_interior(bk, k):
+    """512 x 512 planes split into z-slabs: each rank's interior planes take the y-slab tile order
+    (abi.cpp slab_order, also on the p > 1 interior range) -- the union stays bitwise equal to the
+    oracle on integer data."""
+    A = synth.richards3d(512, 512, 6, integer=True)
+    P = 2
+    rb = bounds(A.n_rows, P, 512 * 512)
+    X = synth.multivector(A.n_rows, k, 3, integer=True)
+
+    def fn(r, ctx):
+        r0, r1 = rb[r], rb[r + 1]
+        S = A.rows(r0, r1)
+        M = bk.Matrix(ctx, S.row_ptr, S.col, S.val, n_global=A.n_rows, row_begin=r0, n_local=r1 - r0)
+        Y = torch.full((r1 - r0, k), float("nan"), dtype=torch.float64, device="cuda")
+        bk.bspmm_apply(ctx, M, X[r0:r1].cuda(), Y)
+        M.close()
+        return Y.cpu().numpy()
+
+    res = run_ranks(bk, P, fn)
+    assert np.array_equal(np.concatenate(res), oracle.spmm(A, X))

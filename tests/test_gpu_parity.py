@@ -645,8 +645,8 @@ def test_fused_cg_matches_unfused_iterates(ctx, bk, k):
 def _slab_case(k):
     import paper_2504_02117_b200 as m
     ctx = m.Context(0)
-    # 512 x 512 planes: 2 (512/S) 512 (16k + 88) B <= 56 MB needs S = 4 at k = 12 / 16 -- the
-    # default dispatch takes the y-slab order with the same S as c5 (abi.cpp)
+    # 512 x 512 planes: 2 (512/S) 512 (16k + 88) B <= 28 MB needs S = 8 / 16 / 32 at k = 12 / 16 / 32 --
+    # the default dispatch takes the y-slab order with the same S as c5 (abi.cpp slab_order)
     A = synth.richards3d(512, 512, 2, integer=True)
     X = synth.multivector(A.n_rows, k, 3, integer=True)
     M = m.Matrix.from_csr(ctx, A)
@@ -657,15 +657,15 @@ def _slab_case(k):
 
 @pytest.mark.parametrize("k", [12, 16, 32])
 def test_spmm_slab_order_bitwise(k):
-    """Large 3-D planes with the y-slab tile order of the gather kernel (default for
-    12 <= k <= 16 with S = 4 on these planes; BK_SLAB=2 forces it for every k):
-    a permutation of the tiles, so the apply stays bitwise equal to the oracle on integer data
-    (subprocess: the knob is read once)."""
+    """Large 3-D planes with the y-slab tile order of the gather kernel (the default for every k;
+    BK_SLAB=0 switches it off): a permutation of the tiles, so the apply stays
+    bitwise equal to the oracle on integer data, with and without it (subprocess: the knob is
+    read once)."""
     import subprocess
     import sys
     code = f"import sys; sys.path.insert(0, {ROOT!r}); sys.path.insert(0, {os.path.join(ROOT, 'tests')!r}); " \
            f"import test_gpu_parity as t; t._slab_case({k})"
-    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BK_SLAB="2"), capture_output=True,
+    r = subprocess.run([sys.executable, "-c", code], env=dict(os.environ, BK_SLAB="0"), capture_output=True,
                        text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     _slab_case(k)                                                      # and the default choice
