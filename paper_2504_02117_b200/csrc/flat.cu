@@ -17,7 +17,7 @@
 namespace bk {
 namespace {
 
-constexpr int FT = 256;       // threads per block
+constexpr int FT = 512;       // threads per block
 constexpr int FU = 4;         // rows per thread per loop trip (independent loads in flight)
 
 template <int W>
@@ -168,15 +168,17 @@ __global__ void __launch_bounds__(FT) upd_flat_kernel(const UpdArgs u) {
     }
 }
 
+// grid: at most 2 blocks of 512 per SM (4 rows per thread per trip keep >= 40 MB of loads in
+// flight); few blocks keep the serial tail short -- one partial row per thread of the last block
 int flat_grid(int64_t n, int num_sms) {
     const int64_t want = (n + (int64_t)FT * FU - 1) / ((int64_t)FT * FU);
-    const int64_t cap = (int64_t)8 * num_sms;
+    const int64_t cap = (int64_t)2 * num_sms;
     return (int)(want < 1 ? 1 : (want < cap ? want : cap));
 }
 
 }  // namespace
 
-size_t flat_part_doubles(int num_sms) { return (size_t)8 * num_sms * 16; }
+size_t flat_part_doubles(int num_sms) { return (size_t)2 * num_sms * 16; }
 
 bool launch_gram_flat(int64_t n, int ka, int kb, const double* X, int64_t ldx, const double* Y, int64_t ldy,
                       double* G, double* part, int* ticket, int num_sms, cudaStream_t st) {
