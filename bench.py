@@ -57,7 +57,7 @@ def peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def step_bytes(pm, n, nnz, ks=KS, solve_k=SOLVE_K, solve_iters=SOLVE_ITERS, n_ghost_rows=0):
+def step_bytes(pm, n, nnz, ks=KS, solve_k=SOLVE_K, solve_iters=SOLVE_ITERS, n_ghost_rows=0, fused_apply=True):
     """Algorithmic bytes / flops of one step (perfmodel.py)."""
     b = f = 0
     parts = {}
@@ -72,7 +72,7 @@ def step_bytes(pm, n, nnz, ks=KS, solve_k=SOLVE_K, solve_iters=SOLVE_ITERS, n_gh
     # solve: x0 = 0 -> R = B (copy), ||R||, Rt aliases B (no copy), P = R, iterations, final
     # true residual -- only the passes solve.cpp enqueues (the library reports the same count as
     # bk_solve_report.alg_bytes; run_ours checks the two agree)
-    sb = pm.bicgstab_solve_bytes(n, nnz, solve_k, solve_iters)
+    sb = pm.bicgstab_solve_bytes(n, nnz, solve_k, solve_iters, fused_apply=fused_apply)
     parts["solve"] = dict(bytes=sb)
     b += sb
     return b, f, parts
@@ -270,7 +270,8 @@ def run_ours(args):
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     n_ghost = info["n_ghost"]
-    bytes_rank, flops_rank, parts = step_bytes(pm, n, nnz, n_ghost_rows=n_ghost)
+    # one rank: the fused BiCGStab takes its reductions in the applies' epilogues (2-D band plan)
+    bytes_rank, flops_rank, parts = step_bytes(pm, n, nnz, n_ghost_rows=n_ghost, fused_apply=(world == 1))
     if solve_bytes_lib is not None and solve_bytes_lib != parts["solve"]["bytes"]:
         raise RuntimeError(f"byte model of the solve ({parts['solve']['bytes']}) != the solver's own count "
                            f"({solve_bytes_lib})")
@@ -297,12 +298,16 @@ def run_ours(args):
     v16 = 8 * n * SOLVE_K
     cls_ms = {c: sum(t[c] for t, _ in solve_cls) / len(solve_cls) for c in solve_cls[0][0]}
     cls_n = {c: sum(m[c] for _, m in solve_cls) / len(solve_cls) for c in solve_cls[0][1]}
+    sb16 = pm.spmm_bytes(n, nnz, SOLVE_K, n_ghost=info["n_ghost"])
     kern = {
         "bcg_tail_k16": dict(ms=cls_ms["fused_tail"], n=cls_n["fused_tail"], bytes=8 * v16),
         "fused_gram_k16": dict(ms=cls_ms["fused_gram"], n=cls_n["fused_gram"], bytes=3 * v16),
         "fused_dots_k16": dict(ms=cls_ms["fused_dots"], n=cls_n["fused_dots"], bytes=3 * v16),
-        "spmm_k16": dict(ms=cls_ms["spmm"] + per["spmm_k16"]["ms"], n=cls_n["spmm"] + 1,
-                         bytes=pm.spmm_bytes(n, nnz, SOLVE_K, n_ghost=info["n_ghost"])),
+        "spmm_k16": dict(ms=cls_ms["spmm"] + per["spmm_k16"]["ms"], n=cls_n["spmm"] + 1, bytes=sb16),
+        # the applies with a reduction in their epilogue: (V = A P, + Rt, R) and (T = A S, + Rt),
+        # 1.5 extra operands per launch on average
+        "fused_apply_k16": dict(ms=cls_ms.get("fused_apply", 0.0), n=cls_n.get("fused_apply", 0),
+                                bytes=sb16 + 3 * v16 // 2),
     }
     for kk, v in per.items():
         if not kk.startswith("solve") and kk not in kern:

@@ -45,7 +45,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         common += ["-I", inc]
     else:
         common += ["-DBK_NO_NCCL"]
-    headers = [os.path.join(CSRC, "bk_internal.h"), os.path.join(CSRC, "ptx.cuh"), os.path.join(CSRC, "dense_dev.cuh"), os.path.join(ROOT, "include", "bk.h")]
+    headers = [os.path.join(CSRC, "bk_internal.h"), os.path.join(CSRC, "ptx.cuh"), os.path.join(CSRC, "dense_dev.cuh"), os.path.join(CSRC, "reduce.cuh"), os.path.join(ROOT, "include", "bk.h")]
     hdr_mtime = max(os.path.getmtime(h) for h in headers)
     nvcc = _nvcc()
 

@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "bk_internal.h"
+#include "reduce.cuh"
 
 using namespace bk;
 
@@ -559,6 +560,36 @@ extern "C" int bspmm_apply(bk_ctx* ctx, const bk_csr* A, int k, const double* X,
     return BK_OK;
     BK_CATCH(ctx)
 }
+
+namespace bk {
+bool spmm_red_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, double* Y, int red, const double* e0,
+                  const double* e1, double* blk0, double* blk1, double* dot0, double* dot1, const SmallEpi* epi) {
+    if (ctx->nranks > 1 || A->n_local <= 0 || !use_stream_kernels()) return false;
+    SpmmArgs a{};
+    a.rp = A->d_rp;
+    a.col = A->d_col;
+    a.val = A->d_val;
+    a.X = X;
+    a.ldx = k;
+    a.k = k;
+    a.kout = k;
+    a.alpha = 1.0;
+    a.beta = 0.0;
+    a.Y = Y;
+    a.ldy = k;
+    a.ncol_local = (int32_t)A->n_local;
+    a.row0 = 0;
+    a.nrows = A->n_local;
+    RedOut ro;
+    ro.part = (double*)ws_get(ctx, WS_GRAM_PART + 32, stream_part_doubles(ctx->num_sms) * sizeof(double));
+    ro.ticket = ctx->d_tickets;
+    ro.blk[0][0] = blk0;
+    ro.blk[0][1] = blk1;
+    ro.dots[0] = dot0;
+    ro.dots[1] = dot1;
+    return launch_bspmm_win_red(a, A->band, ctx->stream, red, e0, e1, ro, epi);
+}
+}  // namespace bk
 
 // ------------------------------------------------------------------ a3 gram
 namespace bk {

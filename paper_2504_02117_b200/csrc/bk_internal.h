@@ -98,6 +98,15 @@ struct BandPlan {
     int64_t row0 = 0, nrows = 0;     // planned contiguous row range
 };
 bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& b, cudaStream_t st);
+// The windowed apply with a fused reduction epilogue (the fused block-BiCGStab passes,
+// DESIGN.md §4.4; 2-D band plans, k = 8 / 12 / 16, alpha 1, beta 0); false = not applicable:
+//   red 1: ro.blk[0][0] = e0^T Y, ro.blk[0][1] = e0^T e1
+//   red 2: ro.blk[0][0] = e0^T Y, ro.dots[0] = <Y_c, X_c>, ro.dots[1] = <Y_c, Y_c>
+// reduced over the grid in a fixed order; the final CTA runs the k x k epilogue epi (may be null).
+struct RedOut;
+struct SmallEpi;
+bool launch_bspmm_win_red(const SpmmArgs& a, const BandPlan& b, cudaStream_t st, int red, const double* e0,
+                          const double* e1, const RedOut& ro, const SmallEpi* epi);
 void launch_update(const UpdArgs& a, cudaStream_t st);
 // G (ka x kb, row-major, device) = X^T Y; `partials` workspace of gram_ws_doubles().
 size_t gram_ws_doubles(int64_t n, int ka, int kb, int num_sms);
@@ -316,6 +325,10 @@ int allreduce_sum(bk_ctx* ctx, double* d, int64_t n);
 // collective (nranks > 1): halo plan, renumbering, neighbour lists (comm.cpp)
 int csr_setup_comm(bk_ctx* ctx, bk_csr* A, const std::vector<int32_t>& rp, std::vector<int32_t>& col_local,
                    const std::vector<int32_t>& colg);
+// Y = A X with the fused reduction epilogue (launch_bspmm_win_red) on a single-rank matrix whose
+// band plan allows it; false = not applicable (the caller runs the separate passes)
+bool spmm_red_dev(bk_ctx* ctx, const bk_csr* A, int k, const double* X, double* Y, int red, const double* e0,
+                  const double* e1, double* blk0, double* blk1, double* dot0, double* dot1, const SmallEpi* epi);
 int solve_impl(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb, double* X,
                int64_t ldx, const bk_solve_opts* o, bk_solve_report* rep);
 int dirk_b0_impl(bk_ctx* ctx, const bk_csr* K, double mass, double tau, int m, const double* A, int s,

@@ -322,6 +322,19 @@ struct Solver {
         for (int q = 0; q < ndot; ++q) outs.push_back({dots[q], k});
         return reduce_outputs(outs);
     }
+    // Y = A X with a reduction in the apply's epilogue (spmm_red_dev; false = not applicable,
+    // nothing enqueued): red 1 blk0 = e0^T Y, blk1 = e0^T e1; red 2 blk0 = e0^T Y, dots <Y,X>, <Y,Y>
+    bool spmm_red(const double* X, double* Y, int red, const double* e0, const double* e1, double* blk0,
+                  double* blk1, double* dot0, double* dot1, const SmallEpi* epi, int* err) {
+        tb();
+        if (!spmm_red_dev(ctx, A, k, X, Y, red, e0, e1, blk0, blk1, dot0, dot1, epi)) return false;
+        te(BK_K_FUSED_APPLY);
+        rep->n_spmm++;
+        rep->n_gram++;
+        ab(spmm_b(false) + (red == 1 ? 2 : 1) * vb());
+        *err = launched("fused apply");
+        return true;
+    }
     // out = a Xin + s P C (+ w W), optionally halted
     int upd(double* out, int64_t ldo, double a, const double* Xin, int64_t ldxin, double s, const double* P,
             int64_t ldp, int kp, const double* C, const double* W = nullptr, int64_t ldw = 0, double w_host = 0.0,
@@ -557,7 +570,39 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     e_be.kind = 2; e_be.k = k; e_be.st = S.ds; e_be.ts = ts; e_be.tt = tt; e_be.Rhs = RtT; e_be.Out = be;
     e_be.sign = -1.0; e_be.LU = LUf; e_be.piv = piv;
     e_cv.kind = 3; e_cv.k = k; e_cv.st = S.ds; e_cv.g = nr; e_cv.rtol = S.o->rtol; e_cv.conv_mode = S.o->conv_mode;
+    // one rank, 2-D band plan: the Rt^T [V R] and Rt^T T, <T,S>, <T,T> passes ride in the
+    // epilogues of the applies that produce V and T (BK_FUSED_APPLY=0: separate)
+    static const int fa_env = env_int("BK_FUSED_APPLY", 1);
+    const bool fapply = fused && epi && fa_env != 0;
     auto iteration = [&]() -> int {
+        int ferr = 0;
+        if (fapply && S.spmm_red(P, V, 1, Rt, R, M1, RR, nullptr, nullptr, &e_al, &ferr)) {
+            TRY(ferr);
+            TRY(S.upd(Sv, k, 1.0, R, k, -1.0, V, k, k, al));
+            if (S.spmm_red(Sv, T, 2, Rt, nullptr, RtT, nullptr, ts, tt, &e_be, &ferr)) {
+                TRY(ferr);
+            } else {
+                TRY(S.spmm(Sv, k, T, k));
+                const double* arr[3] = {Rt, Sv, T};
+                const int xs[1] = {0}, ys[1] = {2};
+                double* const blk[3][2] = {{RtT, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+                const int dp[2][2] = {{2, 1}, {2, 2}};
+                double* const dots[2] = {ts, tt};
+                if (!dots_fused) TRY(S.coldot(T, k, Sv, k, T, k, ts, tt));
+                TRY(S.gram_multi(1, xs, 1, ys, 3, arr, blk, dots_fused ? 2 : 0, dp, dots, &e_be, BK_K_FUSED_DOTS));
+            }
+            S.rep->n_update += 3;
+            double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
+            S.ab(8 * S.vb());   // X, P, S, T, V read; X, R, P written
+            S.tb();
+            if (!launch_bcg_tail_stream(S.n, k, X, R, P, Sv, T, V, al, be, om, nr, &S.ds->halt, spart,
+                                        S.ctx->d_tickets, S.ctx->num_sms, S.st, &e_cv))
+                return set_error(S.ctx, BK_ERR_UNSUPPORTED, "fused BiCGStab tail not applicable");
+            S.te(BK_K_FUSED_TAIL);
+            TRY(S.launched("bcg_tail"));
+            S.rep->n_small += 4;
+            return 0;
+        }
         TRY(S.spmm(P, k, V, k));
         if (fused) {
             const double* arr[3] = {Rt, V, R};

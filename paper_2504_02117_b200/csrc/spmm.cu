@@ -25,7 +25,9 @@
 #include <cstring>
 
 #include "bk_internal.h"
+#include "dense_dev.cuh"
 #include "ptx.cuh"
+#include "reduce.cuh"
 
 namespace bk {
 namespace {
@@ -510,6 +512,16 @@ struct BandArgs {
     int stage_bytes, off_col, off_val, off_rp;
     int ntiles;
     int64_t ncols;      // rows of X
+    // fused reduction epilogue (RED > 0; the fused block-BiCGStab passes): the
+    // rows [r0, r0 + nr) of e[0] (= Rt) and e[1] (= R) are staged with the tile, and
+    //   RED 1:  ro.blk[0][0] = e0^T Y, ro.blk[0][1] = e0^T e1         (Y = A X, e.g. V = A P)
+    //   RED 2:  ro.blk[0][0] = e0^T Y, dots[0] = <Y_c, X_c>, dots[1] = <Y_c, Y_c>   (T = A S)
+    // are accumulated on the FP64 tensor cores / in FMA registers and reduced over the grid in
+    // a fixed order (reduce.cuh); the CTA that writes the result runs the k x k epilogue `epi`.
+    const double* e[2];
+    int off_e[2];
+    RedOut ro;
+    SmallEpi epi;
 };
 constexpr int kMetaDepth = 8;   // tiles whose row-pointer bounds are in flight
 
@@ -593,9 +605,10 @@ __device__ __forceinline__ void store_split(const SpmmArgs& a, int64_t row, int 
     }
 }
 
-template <int KP, int VEC, bool HAS_C, int NC, int NB, int MR, bool KEXACT>
-__global__ void __launch_bounds__(NC + 32, 1)
+template <int KP, int VEC, bool HAS_C, int NC, int NB, int MR, bool KEXACT, int RED = 0>
+__global__ void __launch_bounds__(NC + 32, RED ? 2 : 1)   // (fused reduction: keep 2 CTAs per SM)
 bspmm_win_kernel(const BandArgs w) {
+    static_assert(RED == 0 || (!HAS_C && VEC == 4 && (KP == 8 || KP == 16)), "fused reduction: plain apply, k 8..16");
     const SpmmArgs& a = w.a;
     constexpr int LANES = KP / VEC;
     constexpr int RPP = NC / LANES;
@@ -699,6 +712,7 @@ bspmm_win_kernel(const BandArgs w) {
                     }
                 }
             }
+            if constexpr (RED > 0) bytes += (RED == 1 ? 2u : 1u) * (uint32_t)nr * kb;
             mbar_expect_tx(&full[s], bytes);
             bulk_g2s(st + w.off_rp, a.rp + ra, rp_bytes, &full[s], pol_once);
             if (col_bytes) {
@@ -711,6 +725,11 @@ bspmm_win_kernel(const BandArgs w) {
                     const int64_t lo = r0 + w.lo[g];
                     bulk_g2s(s_win + (int64_t)(w.wb[g] + (sa[g] - lo)) * k, a.X + sa[g] * k, sb[g], &full[s], pol_x);
                 }
+            }
+            if constexpr (RED > 0) {   // the tile's rows of Rt (and R): read once
+#pragma unroll
+                for (int j = 0; j < (RED == 1 ? 2 : 1); ++j)
+                    bulk_g2s(st + w.off_e[j], w.e[j] + r0 * k, (uint32_t)nr * kb, &full[s], pol_once);
             }
             if (++s == w.ns) {
                 s = 0;
@@ -735,6 +754,22 @@ bspmm_win_kernel(const BandArgs w) {
     constexpr int PP = (TCE && WR < 8) ? 8 / WR : 1;
     // (C's fragments stay in shared memory here: register-resident fragments raised the k = 16
     // kernel to 106 registers and measured 0.66 -> 0.49 of HBM; the gather kernel keeps them)
+    // fused reduction (RED): Gram fragments (m8n8k4 accumulators) and per-lane column dots
+    constexpr int RNA = KP / 8;
+    double g0[RED ? RNA : 1][RED ? RNA : 1][2], g1[RED == 1 ? RNA : 1][RED == 1 ? RNA : 1][2];
+    double dd0[RED == 2 ? 4 : 1], dd1[RED == 2 ? 4 : 1];
+    if constexpr (RED > 0) {
+#pragma unroll
+        for (int i = 0; i < RNA; ++i)
+#pragma unroll
+            for (int j = 0; j < RNA; ++j) {
+                g0[i][j][0] = g0[i][j][1] = 0.0;
+                if constexpr (RED == 1) g1[i][j][0] = g1[i][j][1] = 0.0;
+            }
+        if constexpr (RED == 2)
+#pragma unroll
+            for (int t = 0; t < 4; ++t) dd0[t] = dd1[t] = 0.0;
+    }
     int s = 0;
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < w.ntiles; tile += gridDim.x) {
@@ -788,6 +823,61 @@ bspmm_win_kernel(const BandArgs w) {
                 } else {
                     row_epilogue<KP, VEC, HAS_C>(a, s_C, t_row, c0, active, r0 + r, acc);
                 }
+                if constexpr (RED > 0) {
+                    // the warp's WR rows of Y -> its scratch (columns >= k and inactive rows zero)
+                    double* w_scr = s_C + warp * WR * TS;
+                    double* tp = w_scr + (lane32 / LANES) * TS + c0;
+                    const bool keep = active && c0 < k;
+                    reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
+                    reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+                    if constexpr (RED == 2) {   // <Y_c, X_c>, <Y_c, Y_c>: X row r from the staged window
+                        if (keep) {
+                            const int c = (int)(r0 + r);
+                            int f = fo[0];
+#pragma unroll
+                            for (int g = 1; g < NB; ++g) f = (c >= thr[g]) ? fo[g] : f;
+                            const double* xr = s_win + (int64_t)(c + f) * kk + c0;
+                            const double2 xa = reinterpret_cast<const double2*>(xr)[0];
+                            const double2 xb = reinterpret_cast<const double2*>(xr)[1];
+                            const double xv[4] = {xa.x, xa.y, xb.x, xb.y};
+#pragma unroll
+                            for (int t = 0; t < 4; ++t) {
+                                dd0[t] = fma(acc[t], xv[t], dd0[t]);
+                                dd1[t] = fma(acc[t], acc[t], dd1[t]);
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    // e0^T Y (and e0^T e1) over the warp's rows: blocks of 8 rows, two k-steps of 4
+                    const int mg = lane32 >> 2, kq = lane32 & 3;
+                    const double* E0 = reinterpret_cast<const double*>(st + w.off_e[0]);
+                    const double* E1 = reinterpret_cast<const double*>(st + w.off_e[RED == 1 ? 1 : 0]);
+#pragma unroll
+                    for (int b = 0; b < WR / 8; ++b)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int lr = 8 * b + 4 * h + kq;               // scratch row (k index)
+                            const int tr = pass * RPP + warp * WR + lr;      // tile row
+                            const bool rin = pass < passes && tr < nr;
+                            double af[RNA], bf[RNA], cf[RED == 1 ? RNA : 1];
+#pragma unroll
+                            for (int i = 0; i < RNA; ++i) {
+                                const int col = 8 * i + mg;
+                                const bool ok = rin && col < k;
+                                af[i] = ok ? E0[(int64_t)tr * k + col] : 0.0;
+                                bf[i] = ok ? w_scr[lr * TS + col] : 0.0;
+                                if constexpr (RED == 1) cf[i] = ok ? E1[(int64_t)tr * k + col] : 0.0;
+                            }
+#pragma unroll
+                            for (int i = 0; i < RNA; ++i)
+#pragma unroll
+                                for (int j = 0; j < RNA; ++j) {
+                                    dmma(g0[i][j][0], g0[i][j][1], af[i], bf[j]);
+                                    if constexpr (RED == 1) dmma(g1[i][j][0], g1[i][j][1], af[i], cf[j]);
+                                }
+                        }
+                    __syncwarp();
+                }
             }
             if constexpr (TCE) {
                 // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA by the warp itself: no CTA
@@ -833,17 +923,71 @@ bspmm_win_kernel(const BandArgs w) {
             ph ^= 1u;
         }
     }
+    if constexpr (RED > 0) {
+        // every issued copy was waited on: once all consumers are here the ring holds the combine
+        constexpr int KBP = (RED == 1 ? 2 : 1) * KP, NOUT = KP * KBP + 64;
+        asm volatile("bar.sync 1, %0;" ::"r"(NC));
+        double* s_red = reinterpret_cast<double*>(smem);
+        const int mg = lane32 >> 2, kq = lane32 & 3;
+#pragma unroll
+        for (int i = 0; i < RNA; ++i)
+#pragma unroll
+            for (int j = 0; j < RNA; ++j) {
+                double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + 8 * j + 2 * kq;
+                d[0] = g0[i][j][0];
+                d[1] = g0[i][j][1];
+                if constexpr (RED == 1) {
+                    d[KP] = g1[i][j][0];
+                    d[KP + 1] = g1[i][j][1];
+                }
+            }
+        if constexpr (RED == 2) {
+            // lanes holding the same columns (equal lane % LANES): fixed xor tree
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int m = LANES; m < 32; m <<= 1) {
+                    dd0[t] += __shfl_xor_sync(0xffffffffu, dd0[t], m);
+                    dd1[t] += __shfl_xor_sync(0xffffffffu, dd1[t], m);
+                }
+            if (lane32 < LANES)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    s_red[warp * NOUT + NOUT - 64 + c0 + t] = dd0[t];
+                    s_red[warp * NOUT + NOUT - 32 + c0 + t] = dd1[t];
+                }
+        }
+        const int kb_real = (RED == 1 ? 2 : 1) * k;
+        if (grid_reduce<NC, NOUT>(w.ro, s_red, k * kb_real + (RED == 2 ? 2 * k : 0), kb_real, KBP, false) &&
+            w.epi.kind && warp == 0)
+            dd::run_small_epi(w.epi, reinterpret_cast<double*>(smem));
+    }
 }
 
 
-template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT, int NC>
-bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int ctas, bool big_tiles = true) {
+// the fused reduction of one launch (RED > 0): extra operands, outputs, k x k epilogue
+struct RedArgs {
+    const double* e0;
+    const double* e1;
+    RedOut ro;
+    const SmallEpi* epi;
+};
+
+template <int KP, int VEC, bool HAS_C, int NB, int MR, bool KEXACT, int NC, int RED = 0>
+bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int ctas, bool big_tiles = true,
+                  const RedArgs* ra = nullptr) {
     constexpr int LANES = KP / VEC;
     constexpr int RPP = NC / LANES;
     static const int tr_env = env_int("BK_WIN_TR", 0);
     BandArgs w{};
     w.a = a;
     w.G = p.nbands;
+    if constexpr (RED > 0) {
+        w.e[0] = ra->e0;
+        w.e[1] = ra->e1;
+        w.ro = ra->ro;
+        if (ra->epi) w.epi = *ra->epi;
+    }
     auto r16 = [](int64_t x) { return (x + 15) & ~(int64_t)15; };
     auto layout = [&](int TR) {
         w.TR = TR;
@@ -859,7 +1003,12 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
         w.off_col = (int)r16(win);
         w.off_val = w.off_col + (int)r16((int64_t)(w.cap + 4) * 4);
         w.off_rp = w.off_val + (int)r16((int64_t)(w.cap + 2) * 8);
-        w.stage_bytes = (int)((w.off_rp + r16((TR + 8) * 4) + 127) & ~(int64_t)127);
+        int end = w.off_rp + (int)r16((TR + 8) * 4);
+        for (int j = 0; j < (RED == 0 ? 0 : (RED == 1 ? 2 : 1)); ++j) {   // staged rows of Rt (, R)
+            w.off_e[j] = end;
+            end += (int)r16((int64_t)TR * a.k * 8);
+        }
+        w.stage_bytes = (int)((end + 127) & ~(int64_t)127);
     };
     // barriers + row-pointer ring + (C, coupled-apply scratch): with the tensor-core epilogue
     // (TCE) C fragments and the per-warp (A X) rows (RPP rows of KP + 2), else C and one
@@ -870,7 +1019,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
         constexpr int scr_rows = (NC / 32) * ((32 / LANES) < 8 ? 8 : (32 / LANES));
         (void)tr;
         const int cb = TCE ? ((KP / 4) * (KP / 8) * 32 + scr_rows * (KP + 2)) * 8
-                           : (KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
+                           : (RED ? RPP * (KP + 2) : KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
         return 16 * 8 + kMetaDepth * 8 + cb;
     };
     // (coupled k > 16 pairs PP passes per DMMA block: a tile holds at least PP passes)
@@ -900,6 +1049,10 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     if (ns > 8) ns = 8;
     if (ns < 2) return false;
     w.ns = ns;
+    if constexpr (RED > 0) {   // the combine buffer (warps x NOUT doubles) reuses the drained ring
+        constexpr int KBP = (RED == 1 ? 2 : 1) * KP;
+        if ((size_t)(NC / 32) * (KP * KBP + 64) * 8 > (size_t)ns * w.stage_bytes) return false;
+    }
     const int64_t ntiles = (a.nrows + w.TR - 1) / w.TR;
     if (ntiles >= (1ll << 31)) return false;
     w.ntiles = (int)ntiles;
@@ -907,7 +1060,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     const int smem = ns * w.stage_bytes + fixed;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT>,
+        cudaFuncSetAttribute(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT, RED>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize,
                              227 * 1024);
         attr = true;
@@ -915,7 +1068,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     const int nsm = num_sms_cached();
     const int64_t cap = (int64_t)ctas * (a.grid_sms > 0 && a.grid_sms < nsm ? a.grid_sms : nsm);
     const int64_t grid = ntiles < cap ? ntiles : cap;
-    BK_KERNEL(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT><<<(unsigned)grid, NC + 32, smem, st>>>(w));
+    BK_KERNEL(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT, RED><<<(unsigned)grid, NC + 32, smem, st>>>(w));
     return true;
 }
 
@@ -995,6 +1148,31 @@ void launch_bspmm(const SpmmArgs& a, cudaStream_t st) {
     else if (kmax <= 8) launch_k<8>(a, st, vec2);
     else if (kmax <= 16) launch_k<16>(a, st, vec2);
     else launch_k<32>(a, st, vec2);
+}
+
+bool launch_bspmm_win_red(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int red, const double* e0,
+                          const double* e1, const RedOut& ro, const SmallEpi* epi) {
+    if (!win_enabled() || red < 1 || red > 2) return false;
+    // 2-D 5-point lattices (3 bands), plain apply, k = 8, 12, 16, packed and 16-byte aligned operands
+    if (p.nbands != 3 || p.max_row_nnz > 5 || a.C || a.rows || a.Xg || a.alpha != 1.0 || a.beta != 0.0) return false;
+    if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
+    const int k = a.k;
+    if (!(k == 8 || k == 12 || k == 16) || a.kout != k || a.ldx != k || a.ldy != k) return false;
+    auto al16 = [](const void* q) { return q && ((uintptr_t)q & 15) == 0; };
+    if (!al16(a.X) || !al16(a.Y) || !al16(e0) || (red == 1 && !al16(e1))) return false;
+    RedArgs ra{e0, e1, ro, epi};
+    ra.ro.mode = 2;
+    ra.ro.ka = k;
+    ra.ro.kb = (red == 1 ? 2 : 1) * k;
+    ra.ro.kw = k;
+    if (k == 8)
+        return red == 1 ? launch_win_t<8, 4, false, 3, 5, true, 256, 1>(a, p, st, 2, true, &ra)
+                        : launch_win_t<8, 4, false, 3, 5, true, 256, 2>(a, p, st, 2, true, &ra);
+    if (k == 16)
+        return red == 1 ? launch_win_t<16, 4, false, 3, 5, true, 256, 1>(a, p, st, 2, true, &ra)
+                        : launch_win_t<16, 4, false, 3, 5, true, 256, 2>(a, p, st, 2, true, &ra);
+    return red == 1 ? launch_win_t<16, 4, false, 3, 5, false, 256, 1>(a, p, st, 2, true, &ra)
+                    : launch_win_t<16, 4, false, 3, 5, false, 256, 2>(a, p, st, 2, true, &ra);
 }
 
 bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {

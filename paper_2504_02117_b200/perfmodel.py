@@ -78,7 +78,7 @@ def bicgstab_fused(k: int) -> bool:
     return k % 4 == 0 and k <= 16
 
 
-def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> int:
+def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None, fused_apply: bool = False) -> int:
     """One block BiCGStab iteration as enqueued by solve.cpp (DESIGN.md §3 O6, §4.4).
 
     Fused (default where solve.cpp fuses): 2 applies + [Rt V R] Gram pass (3 N x k reads)
@@ -87,6 +87,12 @@ def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> 
     for the separate <T,S>, <T,T> pass when k does not divide 32)."""
     if fused is None:
         fused = bicgstab_fused(k)
+    if fused and fused_apply:
+        # one rank, 2-D band plan, k = 8 / 12 / 16 (solve.cpp fapply): Rt^T [V R] rides in the V = A P
+        # apply (+ Rt, R read), Rt^T T, <T,S>, <T,T> in the T = A S apply (+ Rt read; S, T are the
+        # apply's own operands): 2 applies + 14 N x k passes
+        v = 8 * n * k
+        return 2 * spmm_bytes(n, nnz, k) + 2 * v + v + update_bytes(n, k, k) + 8 * v
     if fused:
         v = 8 * n * k
         dots = 0 if 32 % k == 0 else coldot_bytes(n, k, 1)   # <T,S>, <T,T> in their own pass (T, S read)
@@ -124,7 +130,7 @@ def gmres_step_bytes(n: int, nnz: int, k: int, j: int) -> int:
 
 
 def bicgstab_solve_bytes(n: int, nnz: int, k: int, iters: int, x0_is_zero: bool = True, rt_is_b: bool = True,
-                         fused: bool | None = None) -> int:
+                         fused: bool | None = None, fused_apply: bool = False) -> int:
     """A whole block_krylov_solve(method=bicgstab) call as solve.cpp enqueues it (no convergence
     before `iters`): R = B (copy; + an apply when X0 != 0), ||R_c|| (one same-operand column-dot
     pass), Rt = R0 (no copy when X0 = 0: Rt aliases B), P = R (copy), `iters` iterations, and the
@@ -133,6 +139,6 @@ def bicgstab_solve_bytes(n: int, nnz: int, k: int, iters: int, x0_is_zero: bool 
     b = 2 * v + (0 if x0_is_zero else spmm_bytes(n, nnz, k, beta_nonzero=True))
     b += coldot_bytes(n, k, 0)
     b += (0 if (x0_is_zero and rt_is_b) else 2 * v) + 2 * v
-    b += iters * bicgstab_iter_bytes(n, nnz, k, fused)
+    b += iters * bicgstab_iter_bytes(n, nnz, k, fused, fused_apply)
     b += 2 * v + spmm_bytes(n, nnz, k, beta_nonzero=True) + coldot_bytes(n, k, 0)
     return b

@@ -61,3 +61,14 @@ def test_bicgstab_solve_bytes_counts_only_enqueued_passes():
     assert pm.bicgstab_solve_bytes(n, nnz, k, 5) == (2 * v + v + 2 * v + 5 * it + 2 * v
                                                      + pm.spmm_bytes(n, nnz, k, beta_nonzero=True) + v)
     assert pm.bicgstab_solve_bytes(n, nnz, k, 5, rt_is_b=False) == pm.bicgstab_solve_bytes(n, nnz, k, 5) + 2 * v
+
+
+def test_bicgstab_fused_apply_bytes():
+    """One rank, 2-D band plan (solve.cpp fapply): the two reduction passes ride in the applies --
+    2 applies + 14 N x k passes per iteration (3 fewer than the fused-pass structure)."""
+    n, nnz = 1000, 5000
+    for k in (8, 12, 16):
+        v = 8 * n * k
+        assert pm.bicgstab_iter_bytes(n, nnz, k, fused_apply=True) == 2 * pm.spmm_bytes(n, nnz, k) + 14 * v
+        assert pm.bicgstab_iter_bytes(n, nnz, k) - pm.bicgstab_iter_bytes(n, nnz, k, fused_apply=True) == \
+            (3 if 32 % k == 0 else 5) * v
