@@ -929,16 +929,20 @@ bspmm_win_kernel(const BandArgs w) {
         asm volatile("bar.sync 1, %0;" ::"r"(NC));
         double* s_red = reinterpret_cast<double*>(smem);
         const int mg = lane32 >> 2, kq = lane32 & 3;
+        // grid_reduce reads output (a, b) at a * KBP + b with the Y blocks packed k apart
+        // (b = block * k + c): columns >= k of a block are padding and are not written
 #pragma unroll
         for (int i = 0; i < RNA; ++i)
 #pragma unroll
             for (int j = 0; j < RNA; ++j) {
-                double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + 8 * j + 2 * kq;
+                const int c = 8 * j + 2 * kq;
+                if (c >= k) continue;
+                double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + c;
                 d[0] = g0[i][j][0];
                 d[1] = g0[i][j][1];
                 if constexpr (RED == 1) {
-                    d[KP] = g1[i][j][0];
-                    d[KP + 1] = g1[i][j][1];
+                    d[k] = g1[i][j][0];
+                    d[k + 1] = g1[i][j][1];
                 }
             }
         if constexpr (RED == 2) {
@@ -1022,6 +1026,9 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
                            : (RED ? RPP * (KP + 2) : KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
         return 16 * 8 + kMetaDepth * 8 + cb;
     };
+    // two CTAs per SM: half the shared memory each (the fused-reduction kernels also hold a few
+    // bytes of static shared memory: 1 KB less)
+    constexpr int kHalf = (RED ? 112 : 113) * 1024;
     // (coupled k > 16 pairs PP passes per DMMA block: a tile holds at least PP passes)
     constexpr int PPm = (TCE && (32 / LANES) < 8) ? 8 / (32 / LANES) : 1;
     int TR = std::max(64, PPm * RPP);
@@ -1030,7 +1037,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     } else if (ctas == 2 && big_tiles) {   // the largest multiple of 16 rows with two stages per CTA
         for (int t = std::min(1024, 8 * RPP) & ~15; t >= 64; t -= 16) {
             layout(t);
-            if (2 * w.stage_bytes + fixed_for(t) <= 113 * 1024) {
+            if (2 * w.stage_bytes + fixed_for(t) <= kHalf) {
                 TR = t;
                 break;
             }
@@ -1038,12 +1045,12 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     }
     layout(TR);
     int fixed = fixed_for(TR);
-    int budget = (ctas == 1 ? 227 * 1024 : 113 * 1024) - fixed;
+    int budget = (ctas == 1 ? 227 * 1024 : kHalf) - fixed;
     while (budget / w.stage_bytes < 2 && TR > 2 * 2) {   // huge windows: smaller tiles
         TR = (TR / 2) & ~1;
         layout(TR);
         fixed = fixed_for(TR);
-        budget = (ctas == 1 ? 227 * 1024 : 113 * 1024) - fixed;
+        budget = (ctas == 1 ? 227 * 1024 : kHalf) - fixed;
     }
     int ns = budget / w.stage_bytes;
     if (ns > 8) ns = 8;
@@ -1058,12 +1065,13 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     w.ntiles = (int)ntiles;
     w.ncols = a.ncol_local;
     const int smem = ns * w.stage_bytes + fixed;
-    static bool attr = false;
-    if (!attr) {
+    // the exact dynamic size (the fused-reduction instantiations also hold static shared memory,
+    // so "227 KB dynamic" would be refused); raised when a later launch needs more
+    static int attr_bytes = 0;
+    if (smem > attr_bytes) {
         cudaFuncSetAttribute(bspmm_win_kernel<KP, VEC, HAS_C, NC, NB, MR, KEXACT, RED>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             227 * 1024);
-        attr = true;
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_bytes = smem;
     }
     const int nsm = num_sms_cached();
     const int64_t cap = (int64_t)ctas * (a.grid_sms > 0 && a.grid_sms < nsm ? a.grid_sms : nsm);
