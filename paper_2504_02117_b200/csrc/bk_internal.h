@@ -102,6 +102,7 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& b, cudaStream_t st);
 // DESIGN.md §4.4; 2-D band plans, k = 8 / 12 / 16, alpha 1, beta 0); false = not applicable:
 //   red 1: ro.blk[0][0] = e0^T Y, ro.blk[0][1] = e0^T e1
 //   red 2: ro.blk[0][0] = e0^T Y, ro.dots[0] = <Y_c, X_c>, ro.dots[1] = <Y_c, Y_c>
+//   red 3: ro.blk[0][0] = X^T Y (no extra operand)
 // reduced over the grid in a fixed order; the final CTA runs the k x k epilogue epi (may be null).
 struct RedOut;
 struct SmallEpi;

@@ -331,7 +331,7 @@ struct Solver {
         te(BK_K_FUSED_APPLY);
         rep->n_spmm++;
         rep->n_gram++;
-        ab(spmm_b(false) + (red == 1 ? 2 : 1) * vb());
+        ab(spmm_b(false) + (red == 1 ? 2 : (red == 2 ? 1 : 0)) * vb());
         *err = launched("fused apply");
         return true;
     }
@@ -454,19 +454,26 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     // (BK_EPI=0: separate one-warp kernels instead of the epilogues -- A/B timing)
     static const int epi_env = env_int("BK_EPI", 1);
     const bool epi = fused && !S.allred && epi_env != 0;
+    static const int fa_env = env_int("BK_FUSED_APPLY", 1);
+    const bool fapply = epi && fa_env != 0;   // 2-D band plans: P^T Q in the Q = A P apply
     SmallEpi e_al, e_be;
     e_al.kind = 4; e_al.k = k; e_al.st = S.ds; e_al.G = PQ; e_al.Rhs = RZ; e_al.Out = al; e_al.tol = tol;
     e_be.kind = 5; e_be.k = k; e_be.st = S.ds; e_be.g = RZn; e_be.Rhs = RZ; e_be.Out = be; e_be.tol = tol;
     e_be.rtol = S.o->rtol; e_be.conv_mode = S.o->conv_mode;
     auto cg_fused = [&]() -> int {
-        TRY(S.spmm(P, k, Q, k));
-        const double* arr[2] = {P, Q};
-        const int xs[1] = {0}, ys[1] = {1};
-        double* const blk[3][2] = {{PQ, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
-        TRY(S.gram_multi(1, xs, 1, ys, 2, arr, blk, 0, nullptr, nullptr, epi ? &e_al : nullptr));
-        if (!epi) sd_chol_solve(PQ, RZ, al, k, k, tol, S.ds, S.st);
+        int ferr = 0;
+        if (fapply && S.spmm_red(P, Q, 3, nullptr, nullptr, PQ, nullptr, nullptr, nullptr, &e_al, &ferr)) {
+            TRY(ferr);   // P^T Q in the epilogue of the apply that produces Q
+        } else {
+            TRY(S.spmm(P, k, Q, k));
+            const double* arr[2] = {P, Q};
+            const int xs[1] = {0}, ys[1] = {1};
+            double* const blk[3][2] = {{PQ, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+            TRY(S.gram_multi(1, xs, 1, ys, 2, arr, blk, 0, nullptr, nullptr, epi ? &e_al : nullptr));
+            if (!epi) sd_chol_solve(PQ, RZ, al, k, k, tol, S.ds, S.st);
+        }
         S.rep->n_update += 2;
-        S.rep->n_gram++;
+        S.rep->n_gram++;   // the tail's R^T R
         double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
         S.ab(6 * S.vb());   // X, P, R, Q read; X, R written
         S.tb();

@@ -516,6 +516,7 @@ struct BandArgs {
     // rows [r0, r0 + nr) of e[0] (= Rt) and e[1] (= R) are staged with the tile, and
     //   RED 1:  ro.blk[0][0] = e0^T Y, ro.blk[0][1] = e0^T e1         (Y = A X, e.g. V = A P)
     //   RED 2:  ro.blk[0][0] = e0^T Y, dots[0] = <Y_c, X_c>, dots[1] = <Y_c, Y_c>   (T = A S)
+    //   RED 3:  ro.blk[0][0] = X^T Y (X from the staged window; no extra operand)   (Q = A P)
     // are accumulated on the FP64 tensor cores / in FMA registers and reduced over the grid in
     // a fixed order (reduce.cuh); the CTA that writes the result runs the k x k epilogue `epi`.
     const double* e[2];
@@ -609,6 +610,7 @@ template <int KP, int VEC, bool HAS_C, int NC, int NB, int MR, bool KEXACT, int 
 __global__ void __launch_bounds__(NC + 32, RED ? 2 : 1)   // (fused reduction: keep 2 CTAs per SM)
 bspmm_win_kernel(const BandArgs w) {
     static_assert(RED == 0 || (!HAS_C && VEC == 4 && (KP == 8 || KP == 16)), "fused reduction: plain apply, k 8..16");
+    constexpr int NE = RED == 1 ? 2 : (RED == 2 ? 1 : 0);   // streamed extra operands
     const SpmmArgs& a = w.a;
     constexpr int LANES = KP / VEC;
     constexpr int RPP = NC / LANES;
@@ -712,7 +714,7 @@ bspmm_win_kernel(const BandArgs w) {
                     }
                 }
             }
-            if constexpr (RED > 0) bytes += (RED == 1 ? 2u : 1u) * (uint32_t)nr * kb;
+            if constexpr (NE > 0) bytes += (uint32_t)NE * (uint32_t)nr * kb;
             mbar_expect_tx(&full[s], bytes);
             bulk_g2s(st + w.off_rp, a.rp + ra, rp_bytes, &full[s], pol_once);
             if (col_bytes) {
@@ -726,9 +728,9 @@ bspmm_win_kernel(const BandArgs w) {
                     bulk_g2s(s_win + (int64_t)(w.wb[g] + (sa[g] - lo)) * k, a.X + sa[g] * k, sb[g], &full[s], pol_x);
                 }
             }
-            if constexpr (RED > 0) {   // the tile's rows of Rt (and R): read once
+            if constexpr (NE > 0) {   // the tile's rows of Rt (and R): read once
 #pragma unroll
-                for (int j = 0; j < (RED == 1 ? 2 : 1); ++j)
+                for (int j = 0; j < NE; ++j)
                     bulk_g2s(st + w.off_e[j], w.e[j] + r0 * k, (uint32_t)nr * kb, &full[s], pol_once);
             }
             if (++s == w.ns) {
@@ -852,6 +854,8 @@ bspmm_win_kernel(const BandArgs w) {
                     const int mg = lane32 >> 2, kq = lane32 & 3;
                     const double* E0 = reinterpret_cast<const double*>(st + w.off_e[0]);
                     const double* E1 = reinterpret_cast<const double*>(st + w.off_e[RED == 1 ? 1 : 0]);
+                    // RED 3 (X^T Y, e.g. P^T Q of block CG): the left operand is the apply's own
+                    // input, read from the staged window (centre row of each tile row)
 #pragma unroll
                     for (int b = 0; b < WR / 8; ++b)
 #pragma unroll
@@ -860,11 +864,19 @@ bspmm_win_kernel(const BandArgs w) {
                             const int tr = pass * RPP + warp * WR + lr;      // tile row
                             const bool rin = pass < passes && tr < nr;
                             double af[RNA], bf[RNA], cf[RED == 1 ? RNA : 1];
+                            const double* erow = E0 + (int64_t)tr * k;
+                            if constexpr (RED == 3) {
+                                const int c = (int)(r0 + tr);
+                                int f = fo[0];
+#pragma unroll
+                                for (int g = 1; g < NB; ++g) f = (c >= thr[g]) ? fo[g] : f;
+                                erow = s_win + (int64_t)(c + f) * kk;
+                            }
 #pragma unroll
                             for (int i = 0; i < RNA; ++i) {
                                 const int col = 8 * i + mg;
                                 const bool ok = rin && col < k;
-                                af[i] = ok ? E0[(int64_t)tr * k + col] : 0.0;
+                                af[i] = ok ? erow[col] : 0.0;
                                 bf[i] = ok ? w_scr[lr * TS + col] : 0.0;
                                 if constexpr (RED == 1) cf[i] = ok ? E1[(int64_t)tr * k + col] : 0.0;
                             }
@@ -1008,7 +1020,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
         w.off_val = w.off_col + (int)r16((int64_t)(w.cap + 4) * 4);
         w.off_rp = w.off_val + (int)r16((int64_t)(w.cap + 2) * 8);
         int end = w.off_rp + (int)r16((TR + 8) * 4);
-        for (int j = 0; j < (RED == 0 ? 0 : (RED == 1 ? 2 : 1)); ++j) {   // staged rows of Rt (, R)
+        for (int j = 0; j < (RED == 1 ? 2 : (RED == 2 ? 1 : 0)); ++j) {   // staged rows of Rt (, R)
             w.off_e[j] = end;
             end += (int)r16((int64_t)TR * a.k * 8);
         }
@@ -1160,27 +1172,29 @@ void launch_bspmm(const SpmmArgs& a, cudaStream_t st) {
 
 bool launch_bspmm_win_red(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int red, const double* e0,
                           const double* e1, const RedOut& ro, const SmallEpi* epi) {
-    if (!win_enabled() || red < 1 || red > 2) return false;
+    if (!win_enabled() || red < 1 || red > 3) return false;
     // 2-D 5-point lattices (3 bands), plain apply, k = 8, 12, 16, packed and 16-byte aligned operands
     if (p.nbands != 3 || p.max_row_nnz > 5 || a.C || a.rows || a.Xg || a.alpha != 1.0 || a.beta != 0.0) return false;
     if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
     const int k = a.k;
     if (!(k == 8 || k == 12 || k == 16) || a.kout != k || a.ldx != k || a.ldy != k) return false;
     auto al16 = [](const void* q) { return q && ((uintptr_t)q & 15) == 0; };
-    if (!al16(a.X) || !al16(a.Y) || !al16(e0) || (red == 1 && !al16(e1))) return false;
+    if (!al16(a.X) || !al16(a.Y) || (red != 3 && !al16(e0)) || (red == 1 && !al16(e1))) return false;
     RedArgs ra{e0, e1, ro, epi};
     ra.ro.mode = 2;
     ra.ro.ka = k;
     ra.ro.kb = (red == 1 ? 2 : 1) * k;
     ra.ro.kw = k;
-    if (k == 8)
-        return red == 1 ? launch_win_t<8, 4, false, 3, 5, true, 256, 1>(a, p, st, 2, true, &ra)
-                        : launch_win_t<8, 4, false, 3, 5, true, 256, 2>(a, p, st, 2, true, &ra);
-    if (k == 16)
-        return red == 1 ? launch_win_t<16, 4, false, 3, 5, true, 256, 1>(a, p, st, 2, true, &ra)
-                        : launch_win_t<16, 4, false, 3, 5, true, 256, 2>(a, p, st, 2, true, &ra);
-    return red == 1 ? launch_win_t<16, 4, false, 3, 5, false, 256, 1>(a, p, st, 2, true, &ra)
-                    : launch_win_t<16, 4, false, 3, 5, false, 256, 2>(a, p, st, 2, true, &ra);
+#define BK_RED(KP_, KX)                                                                              \
+    switch (red) {                                                                               \
+        case 1: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 1>(a, p, st, 2, true, &ra);   \
+        case 2: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 2>(a, p, st, 2, true, &ra);   \
+        default: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 3>(a, p, st, 2, true, &ra);  \
+    }
+    if (k == 8) { BK_RED(8, true) }
+    if (k == 16) { BK_RED(16, true) }
+    BK_RED(16, false)
+#undef BK_RED
 }
 
 bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {

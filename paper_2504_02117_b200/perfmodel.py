@@ -108,11 +108,15 @@ def bicgstab_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None, fus
     return b
 
 
-def cg_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None) -> int:
+def cg_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None, fused_apply: bool = False) -> int:
     """One block CG iteration (unpreconditioned) as enqueued by solve.cpp (O4).  Fused (k % 4 == 0, <= 16):
-    apply + P^T Q (2 reads) + tail X, P, R, Q -> X, R with R^T R (4 reads, 2 writes) + P update."""
+    apply + P^T Q (2 reads) + tail X, P, R, Q -> X, R with R^T R (4 reads, 2 writes) + P update.
+    fused_apply (one rank, 2-D band plan, k = 8 / 12 / 16): P^T Q rides in the apply's epilogue."""
     if fused is None:
         fused = k % 4 == 0 and k <= 16
+    if fused and fused_apply:
+        v = 8 * n * k
+        return spmm_bytes(n, nnz, k) + 6 * v + update_bytes(n, k, k)
     if fused:
         v = 8 * n * k
         return spmm_bytes(n, nnz, k) + 2 * v + 6 * v + update_bytes(n, k, k)
