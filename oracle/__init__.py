@@ -13,7 +13,7 @@ module both sides use is ``synth`` (seeded inputs, no method arithmetic).
   O7 (dense reference solve) and O8 (the DIRK window of SURVEY.md §8(f) NEXT-1:
   sequential SDIRK stepping, the all-at-once Kronecker solve, the splitting
   fixed point), O9 (the Chebyshev polynomial preconditioner and
-  its Gershgorin interval).  SURVEY.md §8(c) and DESIGN.md §3 give the
+  its Gershgorin interval), O11 (single-reduction block CG).  SURVEY.md §8(c) and DESIGN.md §3 give the
   readings.  Pins live in tests/test_oracle_*.py.
 
 Parity status: every function here is pinned (see DESIGN.md §3 table).
@@ -326,6 +326,70 @@ def block_cg(A, B, X0=None, *, rtol=1e-10, max_iters=1000, precond="none",
     return _finish(A, B, X, r0, it, rep)
 
 
+def block_cg1(A, B, X0=None, *, rtol=1e-10, max_iters=1000, breakdown_tol=1e-13, conv_mode="all"):
+    """O11: single-reduction block CG -- O'Leary's block CG (O4) in the one-synchronisation
+    form of Chronopoulos & Gear (the communication-avoiding block
+    Krylov the paper motivates with, "rediscovered to mitigate the communication
+    overhead"; R32).  Every k x k quantity of an iteration comes from ONE reduction
+    pass over [R, W = A R]:
+
+        R = B - A X;  W = A R;  G = R^T R;  D = R^T W;  S = D;  S alpha = G (Cholesky);
+        P = R;  Q = W.
+        Loop:  X += P alpha;  R -= Q alpha;
+               W = A R;  Gn = R^T R;  D = R^T W                        (the one reduction)
+               stop when every column sqrt(Gn_cc) <= rtol ||R0_c||     (R5)
+               G beta = Gn (Cholesky);  S = D - beta^T S beta;  S alpha = Gn (Cholesky);
+               P = R + P beta;  Q = W + Q beta;  G = Gn.
+
+    S = P^T A P follows from block-CG orthogonality (R_new^T R_old = 0, Q = A P): with
+    P_new = R + P beta, P^T A R = -S beta, so P_new^T A P_new = D - beta^T S beta.  In exact
+    arithmetic the iterates are those of O4 (pinned against O4, scalar CG and dense LU in
+    tests/test_oracle_pins.py); Q = A P is carried by the recurrence instead of an apply.
+    Unpreconditioned.
+    """
+    A = CsrNp.of(A)
+    B = _np(B, np.float64)
+    X = np.zeros_like(B) if X0 is None else _np(X0, np.float64).copy()
+    rep = Report()
+    R = B - spmm(A, X)
+    W = spmm(A, R)
+    G = gram(R, R)
+    D = gram(R, W)
+    r0 = np.sqrt(np.maximum(np.diag(G), 0.0))
+    S = D
+    it = 0
+    try:
+        alpha = spd_solve(S, G, breakdown_tol)
+    except Breakdown as e:
+        rep.status, rep.breakdown_column = "breakdown", e.column
+        return _finish(A, B, X, r0, it, rep)
+    P = R.copy()
+    Q = W.copy()
+    while it < max_iters:
+        X = update(X, P, alpha, 1.0, 1.0)
+        R = update(R, Q, alpha, 1.0, -1.0)
+        it += 1
+        W = spmm(A, R)
+        Gn = gram(R, R)
+        D = gram(R, W)
+        rel = np.sqrt(np.maximum(np.diag(Gn), 0.0)) / np.where(r0 > 0, r0, 1.0)
+        rep.history.append(rel)
+        if _converged(rel, conv_mode, rtol):
+            rep.converged = True
+            break
+        try:
+            beta = spd_solve(G, Gn, breakdown_tol)
+            S = D - beta.T @ S @ beta
+            alpha = spd_solve(S, Gn, breakdown_tol)
+        except Breakdown as e:
+            rep.status, rep.breakdown_column = "breakdown", e.column
+            break
+        P = update(R, P, beta, 1.0, 1.0)
+        Q = update(W, Q, beta, 1.0, 1.0)
+        G = Gn
+    return _finish(A, B, X, r0, it, rep)
+
+
 def _converged(rel, mode, rtol):
     if mode == "first":
         return rel[0] <= rtol
@@ -482,7 +546,7 @@ def dense_solve(A, B):
     return np.linalg.solve(D, _np(B, np.float64))
 
 
-SOLVERS = {"cg": block_cg, "gmres": block_gmres, "bicgstab": block_bicgstab}
+SOLVERS = {"cg": block_cg, "gmres": block_gmres, "bicgstab": block_bicgstab, "cg1": block_cg1}
 
 
 # ---------------------------------------------------------------------------

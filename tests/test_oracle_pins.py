@@ -372,3 +372,63 @@ def test_bicgstab_count_is_rounding_sensitive():
         noise = np.random.default_rng(sd).uniform(-1, 1, B.shape) * 2.2e-16 if sd else 0.0
         cg.append(oracle.block_cg(As, B * (1 + noise), rtol=1e-10, max_iters=2000)[1].iterations)
     assert max(cg) - min(cg) <= 1, cg
+
+
+# ----------------------------------------------------------------------------- O11 single-reduction CG
+def test_cg1_iterates_equal_block_cg():
+    """O11 is O4 rearranged (exact arithmetic): the iterates after j iterations agree with the
+    independently pinned O4 to rounding, at every j (c1s, k = 4)."""
+    A = synth.make_matrix("c1s")
+    B = synth.multivector(A.n_rows, 4, 2).numpy()
+    for j in (1, 2, 5, 10, 20):
+        X1, _ = oracle.block_cg1(A, B, rtol=1e-30, max_iters=j)
+        X4, _ = oracle.block_cg(A, B, rtol=1e-30, max_iters=j)
+        assert np.linalg.norm(X1 - X4) / np.linalg.norm(X4) < 1e-10, j
+
+
+def test_cg1_k1_equals_scalar_cg_and_dense_lu():
+    """k = 1: textbook Hestenes-Stiefel CG residual history; converged block solve = dense LU."""
+    A = synth.make_matrix("c1s")
+    b = synth.multivector(A.n_rows, 1, 2).numpy()
+    X, rep = oracle.block_cg1(A, b, rtol=1e-30, max_iters=25)
+    x, hist = _scalar_cg(_dense(A), b[:, 0], 25)
+    assert np.allclose(X[:, 0], x, rtol=0, atol=1e-10 * np.abs(x).max())
+    h = np.array(rep.history)[:, 0] * np.linalg.norm(b)
+    assert np.allclose(h, hist, rtol=1e-8)
+    B = synth.multivector(A.n_rows, 8, 2).numpy()
+    X, rep = oracle.block_cg1(A, B, rtol=1e-10)
+    assert rep.converged
+    Xd = oracle.dense_solve(A, B)
+    assert np.linalg.norm(X - Xd) / np.linalg.norm(Xd) < 200 * 1e-10
+    assert np.all(rep.true_relres < 1e-9)
+    _, r4 = oracle.block_cg(A, B, rtol=1e-10)
+    assert abs(rep.iterations - r4.iterations) <= 1
+
+
+def test_cg1_identity_breakdown_and_one_reduction_per_iteration(monkeypatch):
+    """A = I: one iteration; duplicated RHS -> breakdown status; exactly two Gram calls
+    (R^T R, R^T W: one reduction pass) and one apply per iteration, vs O4's two passes."""
+    B = synth.multivector(50, 4, 2).numpy()
+    X, rep = oracle.block_cg1(_eye_csr(50), B, rtol=1e-12)
+    assert rep.converged and rep.iterations == 1 and np.allclose(X, B, atol=1e-14)
+    A = synth.make_matrix("c1s")
+    Bd = synth.multivector(A.n_rows, 2, 2).numpy()
+    _, rep = oracle.block_cg1(A, np.concatenate([Bd, Bd[:, :1]], axis=1), rtol=1e-10)
+    assert rep.status == "breakdown"
+    calls = {"gram": 0, "spmm": 0}
+    g0, s0 = oracle.gram, oracle.spmm
+
+    def cg(*a, **kw):
+        calls["gram"] += 1
+        return g0(*a, **kw)
+
+    def cs(*a, **kw):
+        calls["spmm"] += 1
+        return s0(*a, **kw)
+    monkeypatch.setattr(oracle, "gram", cg)
+    monkeypatch.setattr(oracle, "spmm", cs)
+    Bk = synth.multivector(A.n_rows, 4, 2).numpy()
+    _, rep = oracle.block_cg1(A, Bk, rtol=1e-30, max_iters=7)
+    # setup: R = B - A X, W = A R, R^T R, R^T W; per iteration W = A R, R^T R, R^T W;
+    # _finish: true residual (one apply, one Gram for the column norms)
+    assert calls["spmm"] == 2 + 7 + 1 and calls["gram"] == 2 + 2 * 7 + 1
