@@ -172,7 +172,12 @@ int block_update(bk_ctx *ctx, int64_t n, int kp, int k, double a, double *X, int
  * ... for all right-hand-sides"), using the method's recurrence residual;
  * rep->true_relres is recomputed from scratch at the end.
  * Returns BK_OK, BK_NOT_CONVERGED or BK_BREAKDOWN (also in rep->status).   */
-enum bk_method  { BK_CG = 0, BK_GMRES = 1, BK_BICGSTAB = 2 };
+/* BK_CG1 (the communication-avoiding form the paper's P:43
+ * motivates): single-reduction block CG -- the O'Leary iterates (in exact arithmetic) with
+ * every k x k quantity of an iteration taken from ONE reduction pass over [R, W = A R]
+ * (Q = A P by recurrence; one allreduce per iteration for nranks > 1); SPD A,
+ * unpreconditioned (R32, oracle O11).                                           */
+enum bk_method  { BK_CG = 0, BK_GMRES = 1, BK_BICGSTAB = 2, BK_CG1 = 3 };
 /* Preconditioners (CG only: M^-1 must be SPD).  CHEBYSHEV (SURVEY.md §8(f) NEXT-4,
  * the polynomial stand-in for the paper's AMG preconditioner):
  * M^-1 R = cheb_steps steps of Chebyshev acceleration (Saad Alg. 12.1) for A Z = R

@@ -30,7 +30,7 @@ BK_OK, BK_ERR_ARG, BK_NOT_CONVERGED, BK_BREAKDOWN = 0, 1, 2, 3
 BK_ERR_CUDA, BK_ERR_NCCL, BK_ERR_OOM, BK_ERR_UNSUPPORTED = 4, 5, 6, 7
 BK_MAX_K, BK_MAX_KA = 32, 4096
 BK_GRAM_ALLREDUCE = 1
-METHODS = {"cg": 0, "gmres": 1, "bicgstab": 2}
+METHODS = {"cg": 0, "gmres": 1, "bicgstab": 2, "cg1": 3}
 PRECONDS = {"none": 0, "jacobi": 1, "chebyshev": 2}
 CONV = {"all": 0, "first": 1}
 

@@ -721,7 +721,7 @@ extern "C" int block_krylov_solve(bk_ctx* ctx, const bk_csr* A, int k, const dou
     ARG_CHECK(ctx, ldb >= k && ldx >= k, "block_krylov_solve: leading dimension too small");
     ARG_CHECK(ctx, A->n_local == 0 || (B && X), "block_krylov_solve: NULL pointer");
     ARG_CHECK(ctx, (const void*)B != (const void*)X, "block_krylov_solve: X must not alias B");
-    ARG_CHECK(ctx, o->method >= BK_CG && o->method <= BK_BICGSTAB, "block_krylov_solve: unknown method");
+    ARG_CHECK(ctx, o->method >= BK_CG && o->method <= BK_CG1, "block_krylov_solve: unknown method");
     ARG_CHECK(ctx, o->max_iters >= 0 && o->check_every >= 1, "block_krylov_solve: bad max_iters/check_every");
     ARG_CHECK(ctx, o->method != BK_GMRES || (o->restart >= 1 && (int64_t)(o->restart + 1) * k <= BK_MAX_KA),
               "block_krylov_solve: GMRES needs restart >= 1 and (restart+1)*k <= 4096");
@@ -797,7 +797,7 @@ extern "C" int bk_alg1_run(bk_ctx* ctx, const bk_dr_problem* pb, int m, const do
               "bk_alg1_run: need 1 <= m <= 8, n_steps >= 0, 1 <= window <= 32, eps > 0, max_newton >= 0");
     ARG_CHECK(ctx, !is_device_ptr(A), "bk_alg1_run: A must be a host array");
     ARG_CHECK(ctx, !traj || ldt >= n_steps, "bk_alg1_run: ldt < n_steps");
-    ARG_CHECK(ctx, inner->method >= BK_CG && inner->method <= BK_BICGSTAB && inner->check_every >= 1 &&
+    ARG_CHECK(ctx, inner->method >= BK_CG && inner->method <= BK_CG1 && inner->check_every >= 1 &&
                        inner->max_iters >= 0 && inner->rtol >= 0.0 &&
                        (inner->method != BK_GMRES || (int64_t)(inner->restart + 1) * window <= BK_MAX_KA),
               "bk_alg1_run: bad inner solver options");
@@ -828,7 +828,7 @@ static int dirk_entry(bk_ctx* ctx, const bk_csr* L, const bk_csr* K, double mass
     ARG_CHECK(ctx, L->n_local == 0 || (B && B0 && Y), "bk_dirk_solve: NULL B/B0/Y");
     ARG_CHECK(ctx, (const void*)Y != (const void*)B && (const void*)Y != (const void*)B0,
               "bk_dirk_solve: Y must not alias B or B0");
-    ARG_CHECK(ctx, inner->method >= BK_CG && inner->method <= BK_BICGSTAB && inner->check_every >= 1 &&
+    ARG_CHECK(ctx, inner->method >= BK_CG && inner->method <= BK_CG1 && inner->check_every >= 1 &&
                        inner->max_iters >= 0 && inner->rtol >= 0.0,
               "bk_dirk_solve: bad inner solver options");
     ARG_CHECK(ctx, inner->method != BK_GMRES || (inner->restart >= 1 && (int64_t)(inner->restart + 1) * k <= BK_MAX_KA),

@@ -143,7 +143,8 @@ bool launch_update_wide(const UpdArgs& u, cudaStream_t st);
 // factors kept in LU/piv; 2 BiCGStab omega from ts, tt then Out = G^{-1}(sign Rhs)
 // from LU/piv; 3 convergence test on column norms g; 4 Out = G^{-1} Rhs by
 // Cholesky (block CG alpha); 5 block CG: convergence test on diag(g), then
-// Out = Rhs^{-1} g by Cholesky (beta) and Rhs <- g.
+// Out = Rhs^{-1} g by Cholesky (beta) and Rhs <- g; 6 / 7 single-reduction block CG step /
+// setup (O11; dense_dev.cuh): S state, Out = alpha, Out2 = beta.
 struct SmallEpi {
     int kind = 0;
     int k = 0;
@@ -159,7 +160,11 @@ struct SmallEpi {
     const double* g = nullptr;
     double rtol = 0.0;
     int conv_mode = 0;
+    double* S = nullptr;
+    double* Out2 = nullptr;
 };
+// run a SmallEpi as a one-warp kernel (no fused reduction pass: p > 1, or not applicable)
+void sd_small_epi(const SmallEpi& e, cudaStream_t s);
 // Fused block-BiCGStab passes (stream.cu; false = not applicable):
 // multi-operand Gram: X = [arrays[xs[0]] ..], Y = [arrays[ys[0]] ..], all kw wide
 // (kw <= 16); k x k block (i, j) of X^T Y is written to blk[i][j] (null = dropped).
@@ -173,6 +178,10 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
 bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double* P, const double* Q,
                            const double* al, double* G, const int* halt, double* part, int* ticket, int num_sms,
                            cudaStream_t st, const SmallEpi* epi = nullptr);
+// single-reduction block CG tail (O11): P = R + P be; Q = W + Q be; X += P al; R -= Q al
+// (new P, Q); k % 4 == 0, k <= 16
+bool launch_cg1_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* W, double* Q,
+                            const double* al, const double* be, const int* halt, int num_sms, cudaStream_t st);
 // X += P al + w S; R = S - w T; P = R + (P - w V) be; rr_c = ||R_c||^2 (w = *w_dev); k % 8 == 0
 bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
                             const double* V, const double* al, const double* be, const double* w_dev, double* rr,

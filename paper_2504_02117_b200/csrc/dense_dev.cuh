@@ -13,7 +13,7 @@ namespace dd {
 
 constexpr int KM = BK_MAX_K;
 constexpr int LD = KM + 1;
-constexpr int SCRATCH_DOUBLES = 2 * KM * LD + KM;   // A, B, pivots
+constexpr int SCRATCH_DOUBLES = 3 * KM * LD + KM;   // A, B, pivots, T (kind 6)
 
 __device__ __forceinline__ double wmax(double v) {
 #pragma unroll
@@ -266,6 +266,46 @@ __device__ __forceinline__ void run_small_epi(const SmallEpi& e, double* scratch
         __syncwarp();
         double* rz = const_cast<double*>(e.Rhs);   // roll R^T R for the next iteration
         for (int t = threadIdx.x & 31; t < e.k * e.k; t += 32) rz[t] = e.g[t];
+    } else if (e.kind == 6 || e.kind == 7) {
+        // single-reduction block CG (oracle O11) from the one reduction pass over [R, W = A R]:
+        // g = R^T R (new), G = R^T W, Rhs = R^T R of the previous iteration (rolled here),
+        // S = the S state (P^T A P), Out = alpha, Out2 = beta.
+        //   7 (setup): r0 from diag(g); S = G; alpha = S^{-1} g; beta = 0
+        //   6: test on diag(g); beta = Rhs^{-1} g; S = G - beta^T S beta; alpha = S^{-1} g
+        const int l = threadIdx.x & 31, k = e.k;
+        conv_check_dev(e.g, k + 1, k, e.rtol, e.conv_mode, e.kind == 7, e.st);
+        __syncwarp();
+        if (e.st->halt) return;
+        if (e.kind == 7) {
+            for (int t = l; t < k * k; t += 32) { e.S[t] = e.G[t]; e.Out2[t] = 0.0; }
+        } else {
+            chol_solve_warp(e.Rhs, e.g, e.Out2, k, k, e.tol, e.st, A, B);   // B = beta (k x k, LD)
+            __syncwarp();
+            if (e.st->halt) return;
+            double* T = B + KM * LD + KM;
+            load_rows_w(e.S, A, k, k, 1.0);
+            __syncwarp();
+            if (l < k) {   // T = S beta, lane = column
+                for (int r = 0; r < k; ++r) {
+                    double v = 0.0;
+                    for (int q = 0; q < k; ++q) v = fma(A[r * LD + q], B[q * LD + l], v);
+                    T[r * LD + l] = v;
+                }
+            }
+            __syncwarp();
+            if (l < k) {   // S = G - beta^T T
+                for (int r = 0; r < k; ++r) {
+                    double v = 0.0;
+                    for (int q = 0; q < k; ++q) v = fma(B[q * LD + r], T[q * LD + l], v);
+                    e.S[r * k + l] = e.G[r * k + l] - v;
+                }
+            }
+        }
+        __syncwarp();
+        chol_solve_warp(e.S, e.g, e.Out, k, k, e.tol, e.st, A, B);
+        __syncwarp();
+        double* rz = const_cast<double*>(e.Rhs);
+        for (int t = l; t < k * k; t += 32) rz[t] = e.g[t];
     }
 }
 

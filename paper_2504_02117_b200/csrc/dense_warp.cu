@@ -132,7 +132,15 @@ __global__ void __launch_bounds__(32) chol_qr_w(const double* __restrict__ G, do
     }
 }
 
+// a fused pass's k x k epilogue run on its own (dense_dev.cuh run_small_epi)
+__global__ void __launch_bounds__(32) small_epi_w(const SmallEpi e) {
+    __shared__ double scr[dd::SCRATCH_DOUBLES];
+    dd::run_small_epi(e, scr);
+}
+
 }  // namespace
+
+void sd_small_epi(const SmallEpi& e, cudaStream_t s) { BK_KERNEL(small_epi_w<<<1, 32, 0, s>>>(e)); }
 
 void sdw_lu_solve(const double* G, const double* Rhs, double* Out, int k, int nrhs, double sign, double tol,
                   DevStatus* st, cudaStream_t s, int defer, double* LUo, int* pivo) {

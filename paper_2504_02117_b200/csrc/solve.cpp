@@ -523,6 +523,87 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     return finish(S, B, ldb, X, ldx, e0);
 }
 
+// ---------------------------------------------------------------- O11 single-reduction block CG
+// NEXT-2 (R32): every k x k quantity of an iteration comes from ONE reduction
+// pass over [R, W = A R]; Q = A P is carried by a recurrence.  Fused pass structure:
+//   tail:  P = R + P be ; Q = W + Q be ; X += P al ; R -= Q al     (one pass, 9 N x k)
+//   W = A R with [R^T W, R^T R] in the apply's epilogue (RED 4, X = R from the staged window)
+//          -> k x k epilogue: test on diag(R^T R), be, S = R^T W - be^T S be, al
+// The first tail runs with P = Q = 0 and be = 0 (P = R, Q = W).  p > 1: the two k x k blocks
+// are adjacent, so the pass costs ONE allreduce.
+int block_cg1(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cudaEvent_t e0) {
+    const int k = S.k;
+    double* R = S.vec();
+    double* W = S.vec();
+    double* P = S.vec();
+    double* Q = S.vec();
+    double* sm = S.small(8 * 32 * 32);
+    double *D = sm, *Gn = sm + k * k, *Gold = sm + 2048, *Sst = sm + 3072, *al = sm + 4096, *be = sm + 5120;
+    TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
+    if (S.n > 0) {
+        S.ab(2 * S.vb());
+        TRY(cuda_check(S.ctx, cudaMemsetAsync(P, 0, (size_t)S.n * k * sizeof(double), S.st), "P = 0"));
+        TRY(cuda_check(S.ctx, cudaMemsetAsync(Q, 0, (size_t)S.n * k * sizeof(double), S.st), "Q = 0"));
+    }
+    const bool al16 = ((uintptr_t)X % 16) == 0 && ((uintptr_t)R % 16) == 0 && ((uintptr_t)W % 16) == 0;
+    const bool fused = fused_enabled() && use_stream_kernels() && S.n > 0 && k % 4 == 0 && k <= 16 && ldx == k && al16;
+    const bool multi = use_stream_kernels() && S.n > 0 && k <= 16 && al16;   // one Gram pass for both blocks
+    static const int epi_env = env_int("BK_EPI", 1);
+    static const int fa_env = env_int("BK_FUSED_APPLY", 1);
+    const bool epi = !S.allred && epi_env != 0;
+    SmallEpi e_init, e_it;
+    e_it.kind = 6; e_it.k = k; e_it.st = S.ds; e_it.G = D; e_it.g = Gn; e_it.Rhs = Gold; e_it.S = Sst;
+    e_it.Out = al; e_it.Out2 = be; e_it.tol = S.o->breakdown_tol; e_it.rtol = S.o->rtol;
+    e_it.conv_mode = S.o->conv_mode;
+    e_init = e_it;
+    e_init.kind = 7;
+    // W = A R and the one reduction pass [R^T W, R^T R] (+ its k x k epilogue)
+    auto reduce = [&](const SmallEpi& e) -> int {
+        int ferr = 0;
+        if (epi && fa_env != 0 && S.spmm_red(R, W, 4, nullptr, nullptr, D, Gn, nullptr, nullptr, &e, &ferr)) return ferr;
+        TRY(S.spmm(R, k, W, k));
+        bool ran_epi = false;
+        if (multi) {
+            const double* arr[2] = {R, W};
+            const int xs[1] = {0}, ys[2] = {1, 0};
+            double* const blk[3][2] = {{D, Gn}, {nullptr, nullptr}, {nullptr, nullptr}};
+            TRY(S.gram_multi(1, xs, 2, ys, 2, arr, blk, 0, nullptr, nullptr, epi ? &e : nullptr, BK_K_GRAM));
+            ran_epi = epi;
+        } else {
+            TRY(S.gram(R, k, k, W, k, D));
+            TRY(S.gram(R, k, k, R, k, Gn));
+        }
+        if (!ran_epi) {
+            sd_small_epi(e, S.st);
+            TRY(S.launched("cg1 step"));
+        }
+        return 0;
+    };
+    S.rep->n_small++;
+    TRY(reduce(e_init));
+    auto body = [&]() -> int {
+        S.rep->n_update += 4;
+        if (fused) {
+            S.ab(9 * S.vb());   // X, R, P, W, Q read; X, R, P, Q written
+            S.tb();
+            if (!launch_cg1_tail_stream(S.n, k, X, R, P, W, Q, al, be, &S.ds->halt, S.ctx->num_sms, S.st))
+                return set_error(S.ctx, BK_ERR_UNSUPPORTED, "cg1 tail not applicable");
+            S.te(BK_K_FUSED_TAIL);
+            TRY(S.launched("cg1_tail"));
+        } else {
+            S.rep->n_update -= 4;   // (upd counts its own)
+            TRY(S.upd(P, k, 1.0, R, k, 1.0, P, k, k, be));
+            TRY(S.upd(Q, k, 1.0, W, k, 1.0, Q, k, k, be));
+            TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al));
+            TRY(S.upd(R, k, 1.0, R, k, -1.0, Q, k, k, al));
+        }
+        S.rep->n_small++;
+        return reduce(e_it);
+    };
+    TRY(S.iterate(1, body));
+    return finish(S, B, ldb, X, ldx, e0);
+}
+
 // ---------------------------------------------------------------- O6 block BiCGStab
 // Fused pass structure, same steps and order of the O6 recurrences:
 //   V = A P                          (windowed apply)
@@ -798,6 +879,7 @@ int solve_impl(bk_ctx* ctx, const bk_csr* A, int k, const double* B, int64_t ldb
         switch (o->method) {
             case BK_CG: r = block_cg(S, B, ldb, X, ldx, e0); break;
             case BK_GMRES: r = block_gmres(S, B, ldb, X, ldx, e0); break;
+            case BK_CG1: r = block_cg1(S, B, ldb, X, ldx, e0); break;
             default: r = block_bicgstab(S, B, ldb, X, ldx, e0); break;
         }
     }

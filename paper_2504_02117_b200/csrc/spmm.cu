@@ -517,6 +517,7 @@ struct BandArgs {
     //   RED 1:  ro.blk[0][0] = e0^T Y, ro.blk[0][1] = e0^T e1         (Y = A X, e.g. V = A P)
     //   RED 2:  ro.blk[0][0] = e0^T Y, dots[0] = <Y_c, X_c>, dots[1] = <Y_c, Y_c>   (T = A S)
     //   RED 3:  ro.blk[0][0] = X^T Y (X from the staged window; no extra operand)   (Q = A P)
+    //   RED 4:  ro.blk[0][0] = X^T Y, ro.blk[0][1] = X^T X (X from the window)      (W = A R, O11)
     // are accumulated on the FP64 tensor cores / in FMA registers and reduced over the grid in
     // a fixed order (reduce.cuh); the CTA that writes the result runs the k x k epilogue `epi`.
     const double* e[2];
@@ -758,7 +759,8 @@ bspmm_win_kernel(const BandArgs w) {
     // kernel to 106 registers and measured 0.66 -> 0.49 of HBM; the gather kernel keeps them)
     // fused reduction (RED): Gram fragments (m8n8k4 accumulators) and per-lane column dots
     constexpr int RNA = KP / 8;
-    double g0[RED ? RNA : 1][RED ? RNA : 1][2], g1[RED == 1 ? RNA : 1][RED == 1 ? RNA : 1][2];
+    constexpr bool TWO = RED == 1 || RED == 4;   // two k x k blocks
+    double g0[RED ? RNA : 1][RED ? RNA : 1][2], g1[TWO ? RNA : 1][TWO ? RNA : 1][2];
     double dd0[RED == 2 ? 4 : 1], dd1[RED == 2 ? 4 : 1];
     if constexpr (RED > 0) {
 #pragma unroll
@@ -766,7 +768,7 @@ bspmm_win_kernel(const BandArgs w) {
 #pragma unroll
             for (int j = 0; j < RNA; ++j) {
                 g0[i][j][0] = g0[i][j][1] = 0.0;
-                if constexpr (RED == 1) g1[i][j][0] = g1[i][j][1] = 0.0;
+                if constexpr (TWO) g1[i][j][0] = g1[i][j][1] = 0.0;
             }
         if constexpr (RED == 2)
 #pragma unroll
@@ -865,7 +867,7 @@ bspmm_win_kernel(const BandArgs w) {
                             const bool rin = pass < passes && tr < nr;
                             double af[RNA], bf[RNA], cf[RED == 1 ? RNA : 1];
                             const double* erow = E0 + (int64_t)tr * k;
-                            if constexpr (RED == 3) {
+                            if constexpr (RED >= 3) {
                                 const int c = (int)(r0 + tr);
                                 int f = fo[0];
 #pragma unroll
@@ -886,6 +888,7 @@ bspmm_win_kernel(const BandArgs w) {
                                 for (int j = 0; j < RNA; ++j) {
                                     dmma(g0[i][j][0], g0[i][j][1], af[i], bf[j]);
                                     if constexpr (RED == 1) dmma(g1[i][j][0], g1[i][j][1], af[i], cf[j]);
+                                    if constexpr (RED == 4) dmma(g1[i][j][0], g1[i][j][1], af[i], af[j]);
                                 }
                         }
                     __syncwarp();
@@ -937,7 +940,7 @@ bspmm_win_kernel(const BandArgs w) {
     }
     if constexpr (RED > 0) {
         // every issued copy was waited on: once all consumers are here the ring holds the combine
-        constexpr int KBP = (RED == 1 ? 2 : 1) * KP, NOUT = KP * KBP + 64;
+        constexpr int KBP = (TWO ? 2 : 1) * KP, NOUT = KP * KBP + 64;
         asm volatile("bar.sync 1, %0;" ::"r"(NC));
         double* s_red = reinterpret_cast<double*>(smem);
         const int mg = lane32 >> 2, kq = lane32 & 3;
@@ -952,7 +955,7 @@ bspmm_win_kernel(const BandArgs w) {
                 double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + c;
                 d[0] = g0[i][j][0];
                 d[1] = g0[i][j][1];
-                if constexpr (RED == 1) {
+                if constexpr (TWO) {
                     d[k] = g1[i][j][0];
                     d[k + 1] = g1[i][j][1];
                 }
@@ -973,7 +976,7 @@ bspmm_win_kernel(const BandArgs w) {
                     s_red[warp * NOUT + NOUT - 32 + c0 + t] = dd1[t];
                 }
         }
-        const int kb_real = (RED == 1 ? 2 : 1) * k;
+        const int kb_real = (TWO ? 2 : 1) * k;
         if (grid_reduce<NC, NOUT>(w.ro, s_red, k * kb_real + (RED == 2 ? 2 * k : 0), kb_real, KBP, false) &&
             w.epi.kind && warp == 0)
             dd::run_small_epi(w.epi, reinterpret_cast<double*>(smem));
@@ -1069,7 +1072,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     if (ns < 2) return false;
     w.ns = ns;
     if constexpr (RED > 0) {   // the combine buffer (warps x NOUT doubles) reuses the drained ring
-        constexpr int KBP = (RED == 1 ? 2 : 1) * KP;
+        constexpr int KBP = (RED == 1 || RED == 4 ? 2 : 1) * KP;
         if ((size_t)(NC / 32) * (KP * KBP + 64) * 8 > (size_t)ns * w.stage_bytes) return false;
     }
     const int64_t ntiles = (a.nrows + w.TR - 1) / w.TR;
@@ -1172,23 +1175,24 @@ void launch_bspmm(const SpmmArgs& a, cudaStream_t st) {
 
 bool launch_bspmm_win_red(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int red, const double* e0,
                           const double* e1, const RedOut& ro, const SmallEpi* epi) {
-    if (!win_enabled() || red < 1 || red > 3) return false;
+    if (!win_enabled() || red < 1 || red > 4) return false;
     // 2-D 5-point lattices (3 bands), plain apply, k = 8, 12, 16, packed and 16-byte aligned operands
     if (p.nbands != 3 || p.max_row_nnz > 5 || a.C || a.rows || a.Xg || a.alpha != 1.0 || a.beta != 0.0) return false;
     if (a.row0 != p.row0 || a.nrows != p.nrows || a.nrows <= 0) return false;
     const int k = a.k;
     if (!(k == 8 || k == 12 || k == 16) || a.kout != k || a.ldx != k || a.ldy != k) return false;
     auto al16 = [](const void* q) { return q && ((uintptr_t)q & 15) == 0; };
-    if (!al16(a.X) || !al16(a.Y) || (red != 3 && !al16(e0)) || (red == 1 && !al16(e1))) return false;
+    if (!al16(a.X) || !al16(a.Y) || (red <= 2 && !al16(e0)) || (red == 1 && !al16(e1))) return false;
     RedArgs ra{e0, e1, ro, epi};
     ra.ro.mode = 2;
     ra.ro.ka = k;
-    ra.ro.kb = (red == 1 ? 2 : 1) * k;
+    ra.ro.kb = (red == 1 || red == 4 ? 2 : 1) * k;
     ra.ro.kw = k;
 #define BK_RED(KP_, KX)                                                                              \
     switch (red) {                                                                               \
         case 1: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 1>(a, p, st, 2, true, &ra);   \
         case 2: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 2>(a, p, st, 2, true, &ra);   \
+        case 4: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 4>(a, p, st, 2, true, &ra);   \
         default: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 3>(a, p, st, 2, true, &ra);  \
     }
     if (k == 8) { BK_RED(8, true) }

@@ -1045,6 +1045,139 @@ __global__ void __launch_bounds__(NC + 32, 2) cg_tail_stream_kernel(const CgTail
     if (finish_reduce<NOUT>(U.red, s_red, k * k, k, KBP, false)) small_epilogue(U.red.epi, smem);
 }
 
+// ------------------------------------------------------------------ single-reduction block-CG tail
+// O11 (oracle block_cg1), one pass:  P <- R + P be ;  Q <- W + Q be ;  X <- X + P al ;  R <- R - Q al
+// (new P, Q).  Streams: 0 X, 1 R, 2 P, 3 W, 4 Q.  al, be: k x k (B fragments in shared memory).
+// Each warp owns 8-row blocks: the new P / Q rows are written back into the consumed stage
+// tile and re-read as A fragments of the X / R updates by the same warp.  No reduction: the
+// iteration's one reduction pass is the next W = A R apply (RED 4).
+struct Cg1Tail {
+    Streams S;
+    int k;
+    const double* al;
+    const double* be;
+    double* X;
+    double* R;
+    double* P;
+    double* Q;
+    const int* halt;
+};
+
+template <int NQ, int NK>
+__global__ void __launch_bounds__(NC + 32, 2) cg1_tail_stream_kernel(const Cg1Tail U) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + NSTAGE * STAGE_BYTES);
+    uint64_t* empty = full + NSTAGE;
+    int* s_direct = reinterpret_cast<int*>(empty + NSTAGE);
+    if (U.halt && *U.halt) return;
+    stream_setup(full, empty);
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == NC / 32) {
+        if (lane == 0) stream_produce(U.S, smem, full, empty, s_direct);
+        return;
+    }
+    const int k = U.k, kq = lane & 3, mg = lane >> 2;
+    double* s_ba = reinterpret_cast<double*>(smem + NSTAGE * STAGE_BYTES + 128);
+    double* s_bb = s_ba + NQ * NK * 32;
+#pragma unroll
+    for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+        for (int nb = 0; nb < NK; ++nb) {   // (k % 8 == 4: the last block is half padding)
+            const bool oc = 8 * nb + mg < k;
+            s_ba[(ks * NK + nb) * 32 + lane] = oc ? U.al[(4 * ks + kq) * k + 8 * nb + mg] : 0.0;
+            s_bb[(ks * NK + nb) * 32 + lane] = oc ? U.be[(4 * ks + kq) * k + 8 * nb + mg] : 0.0;
+        }
+    __syncwarp();
+    int it = 0;
+    for (int tile = blockIdx.x; tile < U.S.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % NSTAGE;
+        mbar_wait(&full[s], (it / NSTAGE) & 1);
+        const int64_t r0 = (int64_t)tile * U.S.T;
+        const int nr = (int)((U.S.n - r0) < U.S.T ? (U.S.n - r0) : U.S.T);
+        unsigned char* st = smem + s * STAGE_BYTES;
+        const bool dir = s_direct[s] != 0;
+        const double* Xt = dir ? U.S.p[0] + r0 * k : reinterpret_cast<const double*>(st + U.S.off[0]);
+        const double* Rt = dir ? U.S.p[1] + r0 * k : reinterpret_cast<const double*>(st + U.S.off[1]);
+        // direct tiles: the new P / Q rows are re-read from global memory (this warp wrote them)
+        double* Pt = dir ? U.P + r0 * k : reinterpret_cast<double*>(st + U.S.off[2]);
+        const double* Wt = dir ? U.S.p[3] + r0 * k : reinterpret_cast<const double*>(st + U.S.off[3]);
+        double* Qt = dir ? U.Q + r0 * k : reinterpret_cast<double*>(st + U.S.off[4]);
+        for (int rb = 8 * warp; rb < nr; rb += 8 * (NC / 32)) {
+            const int r = rb + mg;
+            const bool rin = r < nr;
+            double ap[NQ], aq[NQ];   // A fragments of the old P, Q (row mg, col 4 ks + kq)
+#pragma unroll
+            for (int ks = 0; ks < NQ; ++ks) {
+                ap[ks] = rin ? Pt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+                aq[ks] = rin ? Qt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+            }
+            __syncwarp();   // every lane holds its old P / Q fragments before the rows are overwritten
+#pragma unroll
+            for (int nb = 0; nb < NK; ++nb) {
+                const int c = 8 * nb + 2 * kq;
+                const bool cin = rin && c < k;
+                double p0 = 0.0, p1 = 0.0, q0 = 0.0, q1 = 0.0;
+                if (cin) {
+                    const double2 rv = *reinterpret_cast<const double2*>(Rt + (int64_t)r * k + c);
+                    const double2 wv = *reinterpret_cast<const double2*>(Wt + (int64_t)r * k + c);
+                    p0 = rv.x; p1 = rv.y; q0 = wv.x; q1 = wv.y;
+                }
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) {
+                    const double b = s_bb[(ks * NK + nb) * 32 + lane];
+                    dmma(p0, p1, ap[ks], b);
+                    dmma(q0, q1, aq[ks], b);
+                }
+                if (cin) {
+                    const int64_t o = (r0 + r) * k + c;
+                    if (!dir) {
+                        *reinterpret_cast<double2*>(U.P + o) = make_double2(p0, p1);
+                        *reinterpret_cast<double2*>(U.Q + o) = make_double2(q0, q1);
+                    }
+                    *reinterpret_cast<double2*>(Pt + (int64_t)r * k + c) = make_double2(p0, p1);
+                    *reinterpret_cast<double2*>(Qt + (int64_t)r * k + c) = make_double2(q0, q1);
+                }
+            }
+            __syncwarp();   // the block's new P / Q rows are visible to the whole warp
+            double bp[NQ], bq[NQ];   // A fragments of the new P and of -(new Q)
+#pragma unroll
+            for (int ks = 0; ks < NQ; ++ks) {
+                bp[ks] = rin ? Pt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+                bq[ks] = rin ? -Qt[(int64_t)r * k + 4 * ks + kq] : 0.0;
+            }
+#pragma unroll
+            for (int nb = 0; nb < NK; ++nb) {
+                const int c = 8 * nb + 2 * kq;
+                const bool cin = rin && c < k;
+                double x0 = 0.0, x1 = 0.0, v0 = 0.0, v1 = 0.0;
+                if (cin) {
+                    const double2 xv = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
+                    const double2 rv = *reinterpret_cast<const double2*>(Rt + (int64_t)r * k + c);
+                    x0 = xv.x; x1 = xv.y; v0 = rv.x; v1 = rv.y;
+                }
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) {
+                    const double b = s_ba[(ks * NK + nb) * 32 + lane];
+                    dmma(x0, x1, bp[ks], b);
+                    dmma(v0, v1, bq[ks], b);
+                }
+                if (cin) {
+                    const int64_t o = (r0 + r) * k + c;
+                    *reinterpret_cast<double2*>(U.X + o) = make_double2(x0, x1);
+                    *reinterpret_cast<double2*>(U.R + o) = make_double2(v0, v1);
+                }
+            }
+            __syncwarp();
+        }
+        // generic stores went into the stage; the producer's next bulk copy into it is an
+        // async-proxy write: order them (PTX memory model)
+        if (!dir) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+}
+
 int panel_mode() {
     static int v = -1;
     if (v < 0) {
@@ -1346,6 +1479,33 @@ bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double*
     }
     BK_CT(1, 1) BK_CT(2, 1) BK_CT(3, 2) BK_CT(4, 2) BK_CT(6, 3) BK_CT(8, 4)
 #undef BK_CT
+    return false;
+}
+
+bool launch_cg1_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* W, double* Q,
+                            const double* al, const double* be, const int* halt, int num_sms, cudaStream_t st) {
+    if (n <= 0 || k % 4 != 0 || k > 16) return false;
+    const double* arr[5] = {X, R, P, W, Q};
+    Cg1Tail U{};
+    for (int q = 0; q < 5; ++q) {
+        if ((uintptr_t)arr[q] & 15) return false;
+        U.S.p[q] = arr[q];
+        U.S.w[q] = k;
+    }
+    stream_geom(U.S, 5, n);
+    U.k = k; U.al = al; U.be = be; U.X = X; U.R = R; U.P = P; U.Q = Q; U.halt = halt;
+    const int grid = grid_for(U.S.ntiles, num_sms);
+    const int nq = k / 4, nk = (k + 7) / 8;
+    const int smem = NSTAGE * STAGE_BYTES + 128 + 2 * nq * nk * 32 * 8;
+#define BK_C1(Q_, K_)                                                                            \
+    if (nq == Q_ && nk == K_) {                                                                  \
+        static bool at = false;                                                                  \
+        if (!at) { set_smem((const void*)cg1_tail_stream_kernel<Q_, K_>, smem); at = true; }     \
+        BK_KERNEL(cg1_tail_stream_kernel<Q_, K_><<<grid, NC + 32, smem, st>>>(U));                \
+        return true;                                                                             \
+    }
+    BK_C1(1, 1) BK_C1(2, 1) BK_C1(3, 2) BK_C1(4, 2)
+#undef BK_C1
     return false;
 }
 

@@ -124,6 +124,20 @@ def cg_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None, fused_app
             + gram_bytes(n, k, k, same=True) + update_bytes(n, k, k))
 
 
+def cg1_iter_bytes(n: int, nnz: int, k: int, fused: bool | None = None, fused_apply: bool = False) -> int:
+    """One single-reduction block CG iteration (O11) as enqueued by solve.cpp.  Fused (k % 4 == 0,
+    <= 16): tail X, R, P, W, Q -> X, R, P, Q (5 reads, 4 writes) + W = A R with [R^T W, R^T R]
+    (fused_apply: in the apply's epilogue, R read once from the staged window; else one Gram
+    pass over R, W).  Unfused: four updates + the apply + the Gram pass (k <= 16)."""
+    if fused is None:
+        fused = k % 4 == 0 and k <= 16
+    v = 8 * n * k
+    red = 0 if fused_apply else 2 * v
+    if fused:
+        return 9 * v + spmm_bytes(n, nnz, k) + red
+    return 4 * update_bytes(n, k, k) + spmm_bytes(n, nnz, k) + red
+
+
 def gmres_step_bytes(n: int, nnz: int, k: int, j: int) -> int:
     """Inner step j (0-based) of block GMRES with BCGS2 + CholQR2 (O5)."""
     ka = (j + 1) * k

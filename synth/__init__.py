@@ -471,6 +471,7 @@ CONFIGS = {
     "c1": dict(kind="convdiff2d", n=32, k=[4]),
     "c1s": dict(kind="convdiff2d", n=32, k=[4], v=(0.0, 0.0)),
     "c2": dict(kind="convdiff2d", n=1024, k=[1, 2, 4, 8, 16, 32]),
+    "c2s": dict(kind="convdiff2d", n=1024, k=[8, 16], v=(0.0, 0.0)),   # symmetric c2 (CG)
     "c3": dict(kind="diffreact3d", n=128, k=[12]),
     "c4": dict(kind="richards3d", shape=(256, 256, 256), k=[16]),
     "c5": dict(kind="richards3d", shape=(512, 512, 256), k=[8, 16, 32]),

@@ -49,6 +49,13 @@ def test_fused_solver_pass_counts():
         assert pm.cg_iter_bytes(n, nnz, k) == pm.spmm_bytes(n, nnz, k) + 11 * 8 * n * k
     assert not pm.bicgstab_fused(3) and not pm.bicgstab_fused(32)
     assert pm.cg_iter_bytes(n, nnz, 3) > pm.spmm_bytes(n, nnz, 3) + 11 * 8 * n * 3
+    # single-reduction CG (O11): tail 9 passes + apply (+ 2 for the Gram pass unless the
+    # reduction rides in the apply's epilogue)
+    for k in (4, 8, 12, 16):
+        v = 8 * n * k
+        assert pm.cg1_iter_bytes(n, nnz, k, fused_apply=True) == pm.spmm_bytes(n, nnz, k) + 9 * v
+        assert pm.cg1_iter_bytes(n, nnz, k) == pm.spmm_bytes(n, nnz, k) + 11 * v
+    assert pm.cg1_iter_bytes(n, nnz, 3) == 4 * pm.update_bytes(n, 3, 3) + pm.spmm_bytes(n, nnz, 3) + 2 * 8 * n * 3
 
 
 def test_bicgstab_solve_bytes_counts_only_enqueued_passes():

@@ -20,6 +20,13 @@ ncu --metrics gpu__time_duration.sum --clock-control none --profile-from-start o
 ncu --set full --clock-control none --import-source on --profile-from-start off -k regex:bcg_tail -c 1 \
     -o $O/r2_bcg_tail $STEP > $O/r2_bcg_tail.log 2>&1
 export_rep r2_bcg_tail
+# the fused apply + reduction kernels of the BiCGStab iteration (RED 1: Rt^T[V R]; RED 2: Rt^T T, dots)
+for red in 1 2; do
+    ncu --set full --clock-control none --import-source on --profile-from-start off --kernel-name-base demangled \
+        -k "regex:bspmm_win_kernel<16, 4, 0, 256, 3, 5, 1, $red>" -c 1 -o $O/r2_fused_red$red $STEP \
+        > $O/r2_fused_red$red.log 2>&1
+    export_rep r2_fused_red$red
+done
 for cfg in "c2 16" "c2 32" "c3 12" "c5 16" "c5 32"; do
     set -- $cfg
     tag=r2_apply_$1_k$2
