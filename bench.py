@@ -304,10 +304,12 @@ def run_ours(args):
         "fused_gram_k16": dict(ms=cls_ms["fused_gram"], n=cls_n["fused_gram"], bytes=3 * v16),
         "fused_dots_k16": dict(ms=cls_ms["fused_dots"], n=cls_n["fused_dots"], bytes=3 * v16),
         "spmm_k16": dict(ms=cls_ms["spmm"] + per["spmm_k16"]["ms"], n=cls_n["spmm"] + 1, bytes=sb16),
-        # the applies with a reduction in their epilogue: (V = A P, + Rt, R) and (T = A S, + Rt),
-        # 1.5 extra operands per launch on average
-        "fused_apply_k16": dict(ms=cls_ms.get("fused_apply", 0.0), n=cls_n.get("fused_apply", 0),
-                                bytes=sb16 + 3 * v16 // 2),
+        # the applies with a reduction in their epilogue (two kernels, bspmm_win_kernel<.., RED>):
+        # V = A P with Rt^T [V R] (+ Rt, R read) and T = A S with Rt^T T, <T,S>, <T,T> (+ Rt)
+        "fused_apply_gram_k16": dict(ms=cls_ms.get("fused_apply", 0.0), n=cls_n.get("fused_apply", 0),
+                                     bytes=sb16 + 2 * v16),
+        "fused_apply_dots_k16": dict(ms=cls_ms.get("fused_apply_dots", 0.0), n=cls_n.get("fused_apply_dots", 0),
+                                     bytes=sb16 + v16),
     }
     for kk, v in per.items():
         if not kk.startswith("solve") and kk not in kern:

@@ -221,8 +221,10 @@ int bk_precond_apply(bk_ctx *ctx, const bk_csr *A, int k, const bk_solve_opts *o
 enum bk_kclass { BK_K_SPMM = 0, BK_K_GRAM = 1, BK_K_UPDATE = 2, BK_K_FUSED_TAIL = 3,
                  BK_K_FUSED_GRAM = 4 /* Rt^T [V R] */, BK_K_COPY = 5,
                  BK_K_FUSED_DOTS = 6 /* Rt^T T, <T,S>, <T,T> */,
-                 BK_K_FUSED_APPLY = 7 /* apply with one of those reductions in its epilogue */,
-                 BK_NKCLASS = 8 };
+                 BK_K_FUSED_APPLY = 7 /* apply with k x k Gram blocks in its epilogue (Rt^T [V R],
+                                         P^T Q, [R^T W, R^T R]) */,
+                 BK_K_FUSED_APPLY_DOTS = 8 /* apply with Rt^T T, <T,S>, <T,T> in its epilogue */,
+                 BK_NKCLASS = 9 };
 
 typedef struct bk_solve_report {
     int     status;           /* BK_OK / BK_NOT_CONVERGED / BK_BREAKDOWN      */

@@ -50,7 +50,8 @@ class SolveOpts(ctypes.Structure):
                 ("cheb_lmin", ctypes.c_double), ("cheb_lmax", ctypes.c_double)]
 
 
-KCLASSES = ["spmm", "gram", "update", "fused_tail", "fused_gram", "copy", "fused_dots", "fused_apply"]
+KCLASSES = ["spmm", "gram", "update", "fused_tail", "fused_gram", "copy", "fused_dots", "fused_apply",
+            "fused_apply_dots"]
 
 
 class SolveReport(ctypes.Structure):
@@ -59,7 +60,7 @@ class SolveReport(ctypes.Structure):
                 ("true_relres", ctypes.c_double * BK_MAX_K), ("t_total_ms", ctypes.c_double),
                 ("n_spmm", ctypes.c_int64), ("n_gram", ctypes.c_int64), ("n_update", ctypes.c_int64),
                 ("n_small", ctypes.c_int64), ("n_allreduce", ctypes.c_int64),
-                ("t_class_ms", ctypes.c_double * 8), ("n_class", ctypes.c_int64 * 8), ("alg_bytes", ctypes.c_int64)]
+                ("t_class_ms", ctypes.c_double * len(KCLASSES)), ("n_class", ctypes.c_int64 * len(KCLASSES)), ("alg_bytes", ctypes.c_int64)]
 
 
 class CsrInfo(ctypes.Structure):

@@ -168,9 +168,10 @@ __global__ void __launch_bounds__(FT) upd_flat_kernel(const UpdArgs u) {
     }
 }
 
-// k = 1, 2 (ka = kb = kp = k): the operands are read as flat arrays of 32-byte vectors (4 / k
+// Gram k = 1, 2 (ka = kb = k): the operands are read as flat arrays of 32-byte vectors (4 / k
 // rows per load), so every load instruction moves 32 bytes instead of 8 / 16 and one trip over
-// c2 keeps the whole operand in flight.  Rows beyond the last full vector (n k % 4 doubles: whole
+// c2 keeps the whole operand in flight (ncu c2, cold L2: k = 1 / 2 11.0 / 12.6 -> 10.1 / 11.8 us;
+// the same for the update measured slower, 7.6 -> 9.2 us at k = 1, and is not used).  Rows beyond the last full vector (n k % 4 doubles: whole
 // rows) are done by the first warp.  Same fixed-order reduction as gram_flat_kernel.
 __device__ __forceinline__ void ld4(const double* __restrict__ p, double (&v)[4]) {
     asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];" : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3]) : "l"(p));
@@ -265,71 +266,6 @@ __global__ void __launch_bounds__(FT) gram_vec_kernel(int64_t n, const double* _
     if (threadIdx.x == 0) *ticket = 0;
 }
 
-// out = a Xin + s P C + w W with kp = k = K in {1, 2}, flat 32-byte vectors (see above)
-template <int K>
-__global__ void __launch_bounds__(FT) upd_vec_kernel(const UpdArgs u) {
-    if (u.halt && *u.halt) return;
-    double c[K][K];
-#pragma unroll
-    for (int q = 0; q < K; ++q)
-#pragma unroll
-        for (int j = 0; j < K; ++j) c[q][j] = u.C[q * K + j];
-    const double wv = u.W ? (u.w_dev ? u.w_host * *u.w_dev : u.w_host) : 0.0;
-    const bool hx = u.a != 0.0 && u.Xin;
-    const int64_t n = u.n, nv = n * K / 4, S = (int64_t)gridDim.x * FT;
-    auto row = [&](const double* p, const double* x, const double* w, double* o) {   // one row
-#pragma unroll
-        for (int j = 0; j < K; ++j) {
-            double acc = 0.0;
-#pragma unroll
-            for (int q = 0; q < K; ++q) acc = fma(p[q], c[q][j], acc);
-            double v = u.s * acc;
-            if (hx) v = fma(u.a, x[j], v);
-            if (u.W) v = fma(wv, w[j], v);
-            o[j] = v;
-        }
-    };
-    for (int64_t v0 = (int64_t)blockIdx.x * FT + threadIdx.x; v0 < nv; v0 += FU * S) {
-        double p[FU][4], x[FU][4], w[FU][4];
-#pragma unroll
-        for (int t = 0; t < FU; ++t) {
-            const int64_t v = v0 + t * S;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) p[t][j] = x[t][j] = w[t][j] = 0.0;
-            if (v < nv) {
-                ld4(u.P + 4 * v, p[t]);
-                if (hx) ld4(u.Xin + 4 * v, x[t]);
-                if (u.W) ld4(u.W + 4 * v, w[t]);
-            }
-        }
-#pragma unroll
-        for (int t = 0; t < FU; ++t) {
-            const int64_t v = v0 + t * S;
-            if (v >= nv) break;
-            double o[4];
-#pragma unroll
-            for (int r = 0; r < 4 / K; ++r) row(&p[t][r * K], &x[t][r * K], &w[t][r * K], &o[r * K]);
-            double2* op = reinterpret_cast<double2*>(u.out + 4 * v);
-            op[0] = make_double2(o[0], o[1]);
-            op[1] = make_double2(o[2], o[3]);
-        }
-    }
-    if (blockIdx.x == 0 && threadIdx.x < 32) {   // ragged rows
-        for (int64_t r = nv * 4 / K + threadIdx.x; r < n; r += 32) {
-            double pr[K], xr[K], wr[K], o[K];
-#pragma unroll
-            for (int j = 0; j < K; ++j) {
-                pr[j] = u.P[r * K + j];
-                xr[j] = hx ? u.Xin[r * K + j] : 0.0;
-                wr[j] = u.W ? u.W[r * K + j] : 0.0;
-            }
-            row(pr, xr, wr, o);
-#pragma unroll
-            for (int j = 0; j < K; ++j) u.out[r * K + j] = o[j];
-        }
-    }
-}
-
 // grid: at most 2 blocks of 512 per SM (4 rows per thread per trip keep >= 40 MB of loads in
 // flight); few blocks keep the serial tail short -- one partial row per thread of the last block
 int flat_grid(int64_t n, int num_sms) {
@@ -367,7 +303,8 @@ bool launch_update_flat(const UpdArgs& u, int num_sms, cudaStream_t st) {
     if (u.ldo != u.k || (u.kp > 0 && u.ldp != u.kp) || (u.a != 0.0 && u.Xin && u.ldxin != u.k) ||
         (u.W && u.ldw != u.k))
         return false;
-    if (u.kp > 0 && (const double*)u.out == u.P) return false;   // in-place X <- X C: rows read first elsewhere
+    // (in place, out == P, is safe: each thread reads whole rows of P before writing them)
+    if (u.kp > 0 && (const double*)u.out == u.P && u.ldo != u.kp) return false;
     if (u.kp == 0 && (u.a == 0.0 || !u.Xin) && !u.W) return false;
     auto al = [](const void* p, int w) {
         return !p || (w == 4 ? ((uintptr_t)p & 31) == 0 : (w == 2 ? ((uintptr_t)p & 15) == 0 : true));
@@ -376,13 +313,6 @@ bool launch_update_flat(const UpdArgs& u, int num_sms, cudaStream_t st) {
         !al(u.W, u.k))
         return false;
     if (u.out && u.k == 4 && ((uintptr_t)u.out & 15)) return false;
-    auto a32 = [](const void* p) { return !p || ((uintptr_t)p & 31) == 0; };
-    if (u.kp == u.k && u.k <= 2 && a32(u.out) && a32(u.P) && a32(u.a != 0.0 ? u.Xin : nullptr) && a32(u.W)) {
-        const int grid = flat_grid(u.n * u.k / 4, num_sms);   // 32-byte vectors
-        if (u.k == 1) BK_KERNEL(upd_vec_kernel<1><<<grid, FT, 0, st>>>(u));
-        else BK_KERNEL(upd_vec_kernel<2><<<grid, FT, 0, st>>>(u));
-        return true;
-    }
     const int grid = flat_grid(u.n, num_sms);
 #define BK_UF(K, KP) \
     if (u.k == K && u.kp == KP) { BK_KERNEL(upd_flat_kernel<K, KP><<<grid, FT, 0, st>>>(u)); return true; }

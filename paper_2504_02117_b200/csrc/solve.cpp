@@ -328,7 +328,7 @@ struct Solver {
                   double* blk1, double* dot0, double* dot1, const SmallEpi* epi, int* err) {
         tb();
         if (!spmm_red_dev(ctx, A, k, X, Y, red, e0, e1, blk0, blk1, dot0, dot1, epi)) return false;
-        te(BK_K_FUSED_APPLY);
+        te(red == 2 ? BK_K_FUSED_APPLY_DOTS : BK_K_FUSED_APPLY);
         rep->n_spmm++;
         rep->n_gram++;
         ab(spmm_b(false) + (red == 1 ? 2 : (red == 2 ? 1 : 0)) * vb());

@@ -159,6 +159,7 @@ __device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* P
         double af[NQ];
 #pragma unroll
         for (int ks = 0; ks < NQ; ++ks) af[ks] = rin ? Pt[(int64_t)r * kp + 4 * ks + kq] : 0.0;
+        __syncwarp();   // in place (out == P) on a direct tile: the row is read before any lane writes it
 #pragma unroll
         for (int nb = 0; nb < NK; ++nb) {
             const int c = 8 * nb + 2 * kq;
@@ -1214,7 +1215,12 @@ bool launch_update_stream(const UpdArgs& u, int num_sms, cudaStream_t st) {
     // (a strided output -- e.g. a GMRES basis block -- is written row by row from registers)
     if (u.kp < 0 || u.kp > 32 || u.k > 32 || (u.kp > 0 && u.ldp != u.kp) || u.ldo < u.k) return false;
     if (u.ldo != u.k && ((u.ldo & 1) || u.k % 2)) return false;
-    if (u.kp > 0 && (const double*)u.out == u.P) return false;   // in-place X <- X C: blas.cu reads rows first
+    // in place (out == P, e.g. block CG's P = R + P be): the DMMA kernel reads a row's P fragments
+    // (from the stage, or -- direct tiles -- from global memory before a __syncwarp) before any
+    // lane writes it; the FMA kernel does not, so it leaves in-place updates to blas.cu
+    if (u.kp > 0 && (const double*)u.out == u.P &&
+        !(u.ldo == u.kp && u.kp == u.k && u.k % 4 == 0 && (!getenv("BK_UPD") || strcmp(getenv("BK_UPD"), "fma") != 0)))
+        return false;
     if (u.a != 0.0 && (u.ldxin != u.k || !u.Xin)) return false;
     if (u.W && u.ldw != u.k) return false;
     if (u.kp == 0 && u.a == 0.0 && !u.W) return false;

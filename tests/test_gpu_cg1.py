@@ -197,6 +197,6 @@ def test_library_byte_count_matches_perfmodel(ctx, bk, method, cfg, k):
                                         check_every=it)
         assert rep["iterations"] == it
         got.append(rep["alg_bytes"])
-    fa = cfg.startswith("c2") and k in (8, 12, 16)
+    fa = cfg in ("c1", "c1s", "c2", "c2s") and k in (8, 12, 16)   # 2-D band plan: reduction in the apply
     model = {"cg1": pm.cg1_iter_bytes, "cg": pm.cg_iter_bytes, "bicgstab": pm.bicgstab_iter_bytes}[method]
     assert (got[1] - got[0]) == 5 * model(A.n_rows, A.nnz, k, fused_apply=fa), (got, model(A.n_rows, A.nnz, k))

@@ -83,7 +83,8 @@ def test_fused_solver_iterate_at_benchmark_size(ctx, bk, method, cfg, k):
     assert rep["iterations"] == 10, rep
     assert rep["n_class"]["fused_tail"] == 10, rep["n_class"]      # the fused passes ran
     if cfg in ("c2", "c2s"):                                           # 2-D: reductions in the applies
-        assert rep["n_class"]["fused_apply"] == (20 if method == "bicgstab" else 10), rep["n_class"]
+        assert rep["n_class"]["fused_apply"] == 10, rep["n_class"]
+        assert rep["n_class"]["fused_apply_dots"] == (10 if method == "bicgstab" else 0), rep["n_class"]
     Xr, rr = oracle.SOLVERS[method](Ac, B.cpu(), rtol=1e-30, max_iters=10)
     Xg = X.cpu().numpy()
     rel = np.linalg.norm(Xg - Xr) / np.linalg.norm(Xr)

@@ -53,6 +53,11 @@ def main():
         X = torch.zeros_like(B)
         bk.block_krylov_solve(ctx, M, B, X, method="bicgstab", rtol=1e-30, max_iters=3, x0_is_zero=True)
         bk.block_krylov_solve(ctx, Ms, B, X, method="cg", rtol=1e-30, max_iters=3, x0_is_zero=True)
+        bk.block_krylov_solve(ctx, Ms, B, X, method="cg1", rtol=1e-30, max_iters=3, x0_is_zero=True)
+    # in-place P update (out == P) through the streaming DMMA kernel and the flat kernel
+    for k in (2, 8, 16):
+        P = synth.multivector(n, k, 3, device="cuda")
+        bk.block_update(ctx, P, P, synth.small_dense(k, k, 6, device="cuda"), a=1.0, s=1e-3)
     B = synth.multivector(A.n_rows, 8, 2, device="cuda")
     X = torch.zeros_like(B)
     bk.block_krylov_solve(ctx, M, B, X, method="gmres", restart=6, rtol=1e-30, max_iters=4, x0_is_zero=True)
