@@ -175,18 +175,21 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
                               int num_sms, cudaStream_t st, int ndot = 0, const int (*dpair)[2] = nullptr,
                               double* const* dots = nullptr, const SmallEpi* epi = nullptr);
 // block CG tail: X += P al; R -= Q al; G = R^T R (new R); k % 8 == 0
+// (Rin: where the old R is read, default R -- the first iteration reads R0 = B in place)
 bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double* P, const double* Q,
                            const double* al, double* G, const int* halt, double* part, int* ticket, int num_sms,
-                           cudaStream_t st, const SmallEpi* epi = nullptr);
+                           cudaStream_t st, const SmallEpi* epi = nullptr, const double* Rin = nullptr);
 // single-reduction block CG tail (O11): P = R + P be; Q = W + Q be; X += P al; R -= Q al
 // (new P, Q); k % 4 == 0, k <= 16
 bool launch_cg1_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* W, double* Q,
-                            const double* al, const double* be, const int* halt, int num_sms, cudaStream_t st);
+                            const double* al, const double* be, const int* halt, int num_sms, cudaStream_t st,
+                            const double* Rin = nullptr);
 // X += P al + w S; R = S - w T; P = R + (P - w V) be; rr_c = ||R_c||^2 (w = *w_dev); k % 8 == 0
+// (Pin: where the old P is read, default P)
 bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
                             const double* V, const double* al, const double* be, const double* w_dev, double* rr,
                             const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st,
-                            const SmallEpi* epi = nullptr);
+                            const SmallEpi* epi = nullptr, const double* Pin = nullptr);
 // d[c] = sum_i X[i,c] Y[i,c] for c < k (and optionally d2 with Y2); deterministic.
 size_t coldot_ws_doubles(int64_t n, int k, int num_sms);
 void launch_coldot(int64_t n, int k, const double* X, int64_t ldx, const double* Y, int64_t ldy,

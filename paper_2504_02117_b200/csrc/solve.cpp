@@ -435,10 +435,19 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     double* Z = jac ? S.vec() : R;
     double* sm = S.small(8 * 32 * 32);
     double *PQ = sm, *RZ = sm + 1024, *RZn = sm + 2048, *al = sm + 3072, *be = sm + 4096, *nr = sm + 5120;
-    TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
-    if (jac) TRY(S.prec(R, Z));
-    TRY(S.copy(P, k, Z, k));
-    TRY(S.gram(R, k, k, Z, k, RZ));
+    // X0 = 0, no preconditioner, packed aligned B: R0 = P0 = B, read in place by the first
+    // iteration (Rin / Pin) -- no setup copies
+    const bool b_as_r0 = !jac && S.o->x0_is_zero && ldb == k && ((uintptr_t)B % 16) == 0;
+    const double* Rin = R;
+    const double* Pin = P;
+    if (b_as_r0) {
+        Rin = Pin = B;
+    } else {
+        TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
+        if (jac) TRY(S.prec(R, Z));
+        TRY(S.copy(P, k, Z, k));
+    }
+    TRY(S.gram(Rin, k, k, jac ? Z : Rin, k, RZ));
     if (jac) {
         TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
         sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
@@ -462,11 +471,11 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
     e_be.rtol = S.o->rtol; e_be.conv_mode = S.o->conv_mode;
     auto cg_fused = [&]() -> int {
         int ferr = 0;
-        if (fapply && S.spmm_red(P, Q, 3, nullptr, nullptr, PQ, nullptr, nullptr, nullptr, &e_al, &ferr)) {
+        if (fapply && S.spmm_red(Pin, Q, 3, nullptr, nullptr, PQ, nullptr, nullptr, nullptr, &e_al, &ferr)) {
             TRY(ferr);   // P^T Q in the epilogue of the apply that produces Q
         } else {
-            TRY(S.spmm(P, k, Q, k));
-            const double* arr[2] = {P, Q};
+            TRY(S.spmm(Pin, k, Q, k));
+            const double* arr[2] = {Pin, Q};
             const int xs[1] = {0}, ys[1] = {1};
             double* const blk[3][2] = {{PQ, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
             TRY(S.gram_multi(1, xs, 1, ys, 2, arr, blk, 0, nullptr, nullptr, epi ? &e_al : nullptr));
@@ -477,8 +486,8 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
         double* spart = (double*)ws_get(S.ctx, WS_GRAM_PART + 32, stream_part_doubles(S.ctx->num_sms) * sizeof(double));
         S.ab(6 * S.vb());   // X, P, R, Q read; X, R written
         S.tb();
-        if (!launch_cg_tail_stream(S.n, k, X, R, P, Q, al, RZn, &S.ds->halt, spart, S.ctx->d_tickets,
-                                   S.ctx->num_sms, S.st, epi ? &e_be : nullptr))
+        if (!launch_cg_tail_stream(S.n, k, X, R, Pin, Q, al, RZn, &S.ds->halt, spart, S.ctx->d_tickets,
+                                   S.ctx->num_sms, S.st, epi ? &e_be : nullptr, Rin))
             return set_error(S.ctx, BK_ERR_UNSUPPORTED, "fused CG tail not applicable");
         S.te(BK_K_FUSED_TAIL);
         TRY(S.launched("cg_tail"));
@@ -492,16 +501,18 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
             std::swap(RZ, RZn);
         }
         S.rep->n_small += 2;
-        TRY(S.upd(P, k, 1.0, R, k, 1.0, P, k, k, be));
+        TRY(S.upd(P, k, 1.0, R, k, 1.0, Pin, k, k, be));
+        Rin = R;
+        Pin = P;
         return 0;
     };
     auto cg_plain = [&]() -> int {
-        TRY(S.spmm(P, k, Q, k));
-        TRY(S.gram(P, k, k, Q, k, PQ));
+        TRY(S.spmm(Pin, k, Q, k));
+        TRY(S.gram(Pin, k, k, Q, k, PQ));
         sd_chol_solve(PQ, RZ, al, k, k, tol, S.ds, S.st);
         S.rep->n_small++;
-        TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al));
-        TRY(S.upd(R, k, 1.0, R, k, -1.0, Q, k, k, al));
+        TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, Pin, k, k, al));
+        TRY(S.upd(R, k, 1.0, Rin, k, -1.0, Q, k, k, al));
         if (jac) {
             TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
             sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
@@ -513,8 +524,10 @@ int block_cg(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, cu
         }
         sd_chol_solve(RZ, RZn, be, k, k, tol, S.ds, S.st);
         S.rep->n_small += 2;
-        TRY(S.upd(P, k, 1.0, Z, k, 1.0, P, k, k, be));
+        TRY(S.upd(P, k, 1.0, Z, k, 1.0, Pin, k, k, be));
         std::swap(RZ, RZn);
+        Rin = R;
+        Pin = P;
         return 0;
     };
     // (the RZ / RZn swap makes two iterations the period of the launch sequence)
@@ -539,13 +552,19 @@ int block_cg1(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, c
     double* Q = S.vec();
     double* sm = S.small(8 * 32 * 32);
     double *D = sm, *Gn = sm + k * k, *Gold = sm + 2048, *Sst = sm + 3072, *al = sm + 4096, *be = sm + 5120;
-    TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
+    // X0 = 0 with a packed aligned B: R0 = B, read in place by the setup reduction and the first
+    // tail (Rin) -- no copy
+    const bool b_as_r0 = S.o->x0_is_zero && ldb == k && ((uintptr_t)B % 16) == 0;
+    const double* Rin = R;
+    if (b_as_r0) Rin = B;
+    else TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
     if (S.n > 0) {
         S.ab(2 * S.vb());
         TRY(cuda_check(S.ctx, cudaMemsetAsync(P, 0, (size_t)S.n * k * sizeof(double), S.st), "P = 0"));
         TRY(cuda_check(S.ctx, cudaMemsetAsync(Q, 0, (size_t)S.n * k * sizeof(double), S.st), "Q = 0"));
     }
-    const bool al16 = ((uintptr_t)X % 16) == 0 && ((uintptr_t)R % 16) == 0 && ((uintptr_t)W % 16) == 0;
+    const bool al16 = ((uintptr_t)X % 16) == 0 && ((uintptr_t)R % 16) == 0 && ((uintptr_t)W % 16) == 0 &&
+                      ((uintptr_t)Rin % 16) == 0;
     const bool fused = fused_enabled() && use_stream_kernels() && S.n > 0 && k % 4 == 0 && k <= 16 && ldx == k && al16;
     const bool multi = use_stream_kernels() && S.n > 0 && k <= 16 && al16;   // one Gram pass for both blocks
     static const int epi_env = env_int("BK_EPI", 1);
@@ -560,18 +579,19 @@ int block_cg1(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, c
     // W = A R and the one reduction pass [R^T W, R^T R] (+ its k x k epilogue)
     auto reduce = [&](const SmallEpi& e) -> int {
         int ferr = 0;
-        if (epi && fa_env != 0 && S.spmm_red(R, W, 4, nullptr, nullptr, D, Gn, nullptr, nullptr, &e, &ferr)) return ferr;
-        TRY(S.spmm(R, k, W, k));
+        if (epi && fa_env != 0 && S.spmm_red(Rin, W, 4, nullptr, nullptr, D, Gn, nullptr, nullptr, &e, &ferr))
+            return ferr;
+        TRY(S.spmm(Rin, k, W, k));
         bool ran_epi = false;
         if (multi) {
-            const double* arr[2] = {R, W};
+            const double* arr[2] = {Rin, W};
             const int xs[1] = {0}, ys[2] = {1, 0};
             double* const blk[3][2] = {{D, Gn}, {nullptr, nullptr}, {nullptr, nullptr}};
             TRY(S.gram_multi(1, xs, 2, ys, 2, arr, blk, 0, nullptr, nullptr, epi ? &e : nullptr, BK_K_GRAM));
             ran_epi = epi;
         } else {
-            TRY(S.gram(R, k, k, W, k, D));
-            TRY(S.gram(R, k, k, R, k, Gn));
+            TRY(S.gram(Rin, k, k, W, k, D));
+            TRY(S.gram(Rin, k, k, Rin, k, Gn));
         }
         if (!ran_epi) {
             sd_small_epi(e, S.st);
@@ -586,18 +606,19 @@ int block_cg1(Solver& S, const double* B, int64_t ldb, double* X, int64_t ldx, c
         if (fused) {
             S.ab(9 * S.vb());   // X, R, P, W, Q read; X, R, P, Q written
             S.tb();
-            if (!launch_cg1_tail_stream(S.n, k, X, R, P, W, Q, al, be, &S.ds->halt, S.ctx->num_sms, S.st))
+            if (!launch_cg1_tail_stream(S.n, k, X, R, P, W, Q, al, be, &S.ds->halt, S.ctx->num_sms, S.st, Rin))
                 return set_error(S.ctx, BK_ERR_UNSUPPORTED, "cg1 tail not applicable");
             S.te(BK_K_FUSED_TAIL);
             TRY(S.launched("cg1_tail"));
         } else {
             S.rep->n_update -= 4;   // (upd counts its own)
-            TRY(S.upd(P, k, 1.0, R, k, 1.0, P, k, k, be));
+            TRY(S.upd(P, k, 1.0, Rin, k, 1.0, P, k, k, be));
             TRY(S.upd(Q, k, 1.0, W, k, 1.0, Q, k, k, be));
             TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al));
-            TRY(S.upd(R, k, 1.0, R, k, -1.0, Q, k, k, al));
+            TRY(S.upd(R, k, 1.0, Rin, k, -1.0, Q, k, k, al));
         }
         S.rep->n_small++;
+        Rin = R;
         return reduce(e_it);
     };
     TRY(S.iterate(1, body));
@@ -631,14 +652,21 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     double *M1 = sm, *RR = sm + k * k, *RtT = sm + 2048, *ts = RtT + k * k, *tt = ts + k, *al = sm + 3200,
            *be = sm + 4224, *nr = sm + 5248, *LUf = sm + 6144;
     int* piv = reinterpret_cast<int*>(sm + 7168);
-    TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
-    TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
-    sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
-    // Rt = R0 is never written: with X0 = 0 it is B itself (no copy)
+    // X0 = 0 with a packed, aligned B: R0 = P0 = Rt = B.  Rt is never written, and the first
+    // iteration reads B in place of R and P (Rin / Pin), so the setup copies nothing.
+    const bool b_as_r0 = S.o->x0_is_zero && ldb == k && ((uintptr_t)B % 16) == 0;
+    const double* Rin = R;
+    const double* Pin = P;
     const double* Rt = Rt_buf;
-    if (S.o->x0_is_zero && ldb == k && ((uintptr_t)B % 16) == 0) Rt = B;
-    else TRY(S.copy(Rt_buf, k, R, k));
-    TRY(S.copy(P, k, R, k));
+    if (b_as_r0) {
+        Rin = Pin = Rt = B;
+    } else {
+        TRY(S.residual(B, ldb, X, ldx, R, S.o->x0_is_zero));
+        TRY(S.copy(Rt_buf, k, R, k));
+        TRY(S.copy(P, k, R, k));
+    }
+    TRY(S.coldot(Rin, k, Rin, k, nullptr, 0, nr, nullptr));
+    sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 1, S.ds, S.st);
     const double tol = S.o->breakdown_tol;
     const double* om = &S.ds->omega;
     const double* nom = &S.ds->neg_omega;
@@ -664,9 +692,9 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
     const bool fapply = fused && epi && fa_env != 0;
     auto iteration = [&]() -> int {
         int ferr = 0;
-        if (fapply && S.spmm_red(P, V, 1, Rt, R, M1, RR, nullptr, nullptr, &e_al, &ferr)) {
+        if (fapply && S.spmm_red(Pin, V, 1, Rt, Rin, M1, RR, nullptr, nullptr, &e_al, &ferr)) {
             TRY(ferr);
-            TRY(S.upd(Sv, k, 1.0, R, k, -1.0, V, k, k, al));
+            TRY(S.upd(Sv, k, 1.0, Rin, k, -1.0, V, k, k, al));
             if (S.spmm_red(Sv, T, 2, Rt, nullptr, RtT, nullptr, ts, tt, &e_be, &ferr)) {
                 TRY(ferr);
             } else {
@@ -684,26 +712,28 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
             S.ab(8 * S.vb());   // X, P, S, T, V read; X, R, P written
             S.tb();
             if (!launch_bcg_tail_stream(S.n, k, X, R, P, Sv, T, V, al, be, om, nr, &S.ds->halt, spart,
-                                        S.ctx->d_tickets, S.ctx->num_sms, S.st, &e_cv))
+                                        S.ctx->d_tickets, S.ctx->num_sms, S.st, &e_cv, Pin))
                 return set_error(S.ctx, BK_ERR_UNSUPPORTED, "fused BiCGStab tail not applicable");
             S.te(BK_K_FUSED_TAIL);
             TRY(S.launched("bcg_tail"));
             S.rep->n_small += 4;
+            Rin = R;
+            Pin = P;
             return 0;
         }
-        TRY(S.spmm(P, k, V, k));
+        TRY(S.spmm(Pin, k, V, k));
         if (fused) {
-            const double* arr[3] = {Rt, V, R};
+            const double* arr[3] = {Rt, V, Rin};
             const int xs[1] = {0}, ys[2] = {1, 2};
             double* const blk[3][2] = {{M1, RR}, {nullptr, nullptr}, {nullptr, nullptr}};
             TRY(S.gram_multi(1, xs, 2, ys, 3, arr, blk, 0, nullptr, nullptr, epi ? &e_al : nullptr));
             if (!epi) sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st, 0, LUf, piv);   // factors kept for be
         } else {
             TRY(S.gram(Rt, k, k, V, k, M1));
-            TRY(S.gram(Rt, k, k, R, k, RR));
+            TRY(S.gram(Rt, k, k, Rin, k, RR));
             sd_lu_solve(M1, RR, al, k, k, 1.0, tol, S.ds, S.st);
         }
-        TRY(S.upd(Sv, k, 1.0, R, k, -1.0, V, k, k, al));
+        TRY(S.upd(Sv, k, 1.0, Rin, k, -1.0, V, k, k, al));
         TRY(S.spmm(Sv, k, T, k));
         if (fused) {
             const double* arr[3] = {Rt, Sv, T};
@@ -724,7 +754,7 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
             S.ab(8 * S.vb());   // X, P, S, T, V read; X, R, P written
             S.tb();
             if (!launch_bcg_tail_stream(S.n, k, X, R, P, Sv, T, V, al, be, om, nr, &S.ds->halt, spart,
-                                        S.ctx->d_tickets, S.ctx->num_sms, S.st, epi ? &e_cv : nullptr))
+                                        S.ctx->d_tickets, S.ctx->num_sms, S.st, epi ? &e_cv : nullptr, Pin))
                 return set_error(S.ctx, BK_ERR_UNSUPPORTED, "fused BiCGStab tail not applicable");
             S.te(BK_K_FUSED_TAIL);
             TRY(S.launched("bcg_tail"));
@@ -737,16 +767,18 @@ int block_bicgstab(Solver& S, const double* B, int64_t ldb, double* X, int64_t l
         } else {
             TRY(S.coldot(T, k, Sv, k, T, k, ts, tt));
             sd_omega(ts, tt, k, S.ds, S.st);
-            TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, P, k, k, al, Sv, k, 1.0, om));
+            TRY(S.upd(X, ldx, 1.0, X, ldx, 1.0, Pin, k, k, al, Sv, k, 1.0, om));
             TRY(S.upd(R, k, 1.0, Sv, k, 0.0, nullptr, k, 0, nullptr, T, k, 1.0, nom));
             TRY(S.coldot(R, k, R, k, nullptr, 0, nr, nullptr));
             sd_conv_check(nr, 1, k, S.o->rtol, S.o->conv_mode, 0, S.ds, S.st);
             TRY(S.gram(Rt, k, k, T, k, RtT));
             sd_lu_solve(M1, RtT, be, k, k, -1.0, tol, S.ds, S.st);
             S.rep->n_small += 4;
-            TRY(S.upd(Tmp, k, 1.0, P, k, 0.0, nullptr, k, 0, nullptr, V, k, 1.0, nom));
+            TRY(S.upd(Tmp, k, 1.0, Pin, k, 0.0, nullptr, k, 0, nullptr, V, k, 1.0, nom));
             TRY(S.upd(P, k, 1.0, R, k, 1.0, Tmp, k, k, be));
         }
+        Rin = R;
+        Pin = P;
         return 0;
     };
     TRY(S.iterate(1, iteration));

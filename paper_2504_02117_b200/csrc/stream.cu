@@ -1429,9 +1429,9 @@ bool launch_gram_multi_stream(int64_t n, int kw, int nxa, const int* xs, int nya
 bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* S, const double* T,
                             const double* V, const double* al, const double* be, const double* w_dev, double* rr,
                             const int* halt, double* part, int* ticket, int num_sms, cudaStream_t st,
-                            const SmallEpi* epi) {
+                            const SmallEpi* epi, const double* Pin) {
     if (n <= 0 || k % 4 != 0 || k > 32) return false;
-    const double* arr[5] = {X, P, S, T, V};
+    const double* arr[5] = {X, Pin ? Pin : P, S, T, V};
     BcgTail U{};
     for (int q = 0; q < 5; ++q) {
         if ((uintptr_t)arr[q] & 15) return false;
@@ -1460,9 +1460,9 @@ bool launch_bcg_tail_stream(int64_t n, int k, double* X, double* R, double* P, c
 
 bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double* P, const double* Q,
                            const double* al, double* G, const int* halt, double* part, int* ticket, int num_sms,
-                           cudaStream_t st, const SmallEpi* epi) {
+                           cudaStream_t st, const SmallEpi* epi, const double* Rin) {
     if (n <= 0 || k % 4 != 0 || k > 32) return false;
-    const double* arr[4] = {X, P, R, Q};
+    const double* arr[4] = {X, P, Rin ? Rin : R, Q};
     CgTail U{};
     for (int q = 0; q < 4; ++q) {
         if ((uintptr_t)arr[q] & 15) return false;
@@ -1489,9 +1489,10 @@ bool launch_cg_tail_stream(int64_t n, int k, double* X, double* R, const double*
 }
 
 bool launch_cg1_tail_stream(int64_t n, int k, double* X, double* R, double* P, const double* W, double* Q,
-                            const double* al, const double* be, const int* halt, int num_sms, cudaStream_t st) {
+                            const double* al, const double* be, const int* halt, int num_sms, cudaStream_t st,
+                            const double* Rin) {
     if (n <= 0 || k % 4 != 0 || k > 16) return false;
-    const double* arr[5] = {X, R, P, W, Q};
+    const double* arr[5] = {X, Rin ? Rin : R, P, W, Q};
     Cg1Tail U{};
     for (int q = 0; q < 5; ++q) {
         if ((uintptr_t)arr[q] & 15) return false;

@@ -150,13 +150,16 @@ def gmres_step_bytes(n: int, nnz: int, k: int, j: int) -> int:
 def bicgstab_solve_bytes(n: int, nnz: int, k: int, iters: int, x0_is_zero: bool = True, rt_is_b: bool = True,
                          fused: bool | None = None, fused_apply: bool = False) -> int:
     """A whole block_krylov_solve(method=bicgstab) call as solve.cpp enqueues it (no convergence
-    before `iters`): R = B (copy; + an apply when X0 != 0), ||R_c|| (one same-operand column-dot
-    pass), Rt = R0 (no copy when X0 = 0: Rt aliases B), P = R (copy), `iters` iterations, and the
-    final true residual (copy + apply with beta != 0 + ||.||)."""
+    before `iters`).  X0 = 0 with a packed B (rt_is_b): R0 = P0 = Rt = B are read in place -- only
+    ||R_c|| (one same-operand column-dot pass over B); otherwise R = B (copy; + an apply when
+    X0 != 0), Rt = R0 (copy), P = R (copy), ||R_c||.  Then `iters` iterations and the final true
+    residual (copy + apply with beta != 0 + ||.||)."""
     v = D * n * k
-    b = 2 * v + (0 if x0_is_zero else spmm_bytes(n, nnz, k, beta_nonzero=True))
-    b += coldot_bytes(n, k, 0)
-    b += (0 if (x0_is_zero and rt_is_b) else 2 * v) + 2 * v
+    if x0_is_zero and rt_is_b:
+        b = coldot_bytes(n, k, 0)
+    else:
+        b = 2 * v + (0 if x0_is_zero else spmm_bytes(n, nnz, k, beta_nonzero=True))
+        b += 2 * v + 2 * v + coldot_bytes(n, k, 0)
     b += iters * bicgstab_iter_bytes(n, nnz, k, fused, fused_apply)
     b += 2 * v + spmm_bytes(n, nnz, k, beta_nonzero=True) + coldot_bytes(n, k, 0)
     return b
