@@ -87,8 +87,9 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
 
 // FP64 tensor-core MMA m8n8k4 (SASS DMMA): D(8x8) += A(8x4) B(4x8); lane (g = lane/4,
 // q = lane%4) holds A[g][q], B[q][g] and D[g][2q], D[g][2q+1].
+// (not volatile: a pure register operation, so the compiler may interleave independent chains)
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }

@@ -224,12 +224,18 @@ __device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col,
             for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
             const int pq = pass0 + lr / WR;
             const int row = pq * RPP + wrow0 + lr % WR;
+            double dd[NKO][2];   // k-step outer: NKO independent accumulator chains
+#pragma unroll
+            for (int nb = 0; nb < NKO; ++nb) dd[nb][0] = dd[nb][1] = 0.0;
+#pragma unroll
+            for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+                for (int nb = 0; nb < NKO; ++nb)
+                    dmma(dd[nb][0], dd[nb][1], af[ks],
+                         KP <= 16 ? cf[(ks * NKO + nb) % NCF] : s_Cf[(ks * NKO + nb) * 32 + lane32]);
 #pragma unroll
             for (int nb = 0; nb < NKO; ++nb) {
-                double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-                for (int ks = 0; ks < NQ; ++ks)
-                    dmma(d0, d1, af[ks], KP <= 16 ? cf[(ks * NKO + nb) % NCF] : s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                const double d0 = dd[nb][0], d1 = dd[nb][1];
                 const int c = 8 * nb + 2 * kq;
                 if (rv && pq < PASSES && row < nr && c < a.kout) {
                     double* yp = a.Y + (r0 + row) * a.ldy + c;
@@ -625,9 +631,6 @@ bspmm_win_kernel(const BandArgs w) {
     // then the tile's (A X) rows (TS doubles per row) for the DMMA epilogue
     constexpr bool TCE = HAS_C && KP >= 8 && VEC == 4;
     constexpr int NQ = KP / 4, NKO = KP / 8, TS = KP + 2;
-    // fused-reduction scratch row stride: 4 rows of a DMMA k-step land on both 16-bank halves
-    // (2·TSR ≡ 16 mod 32 words) -- KP + 2 put all four on overlapping banks (4-way)
-    constexpr int TSR = KP == 16 ? 24 : KP;
     double* s_Cf = s_C;
     double* s_tT = s_Cf + NQ * NKO * 32;
 
@@ -832,8 +835,8 @@ bspmm_win_kernel(const BandArgs w) {
                 }
                 if constexpr (RED > 0) {
                     // the warp's WR rows of Y -> its scratch (columns >= k and inactive rows zero)
-                    double* w_scr = s_C + warp * WR * TSR;
-                    double* tp = w_scr + (lane32 / LANES) * TSR + c0;
+                    double* w_scr = s_C + warp * WR * TS;
+                    double* tp = w_scr + (lane32 / LANES) * TS + c0;
                     const bool keep = active && c0 < k;
                     reinterpret_cast<double2*>(tp)[0] = keep ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
                     reinterpret_cast<double2*>(tp)[1] = keep ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
@@ -877,25 +880,13 @@ bspmm_win_kernel(const BandArgs w) {
                                 for (int g = 1; g < NB; ++g) f = (c >= thr[g]) ? fo[g] : f;
                                 erow = s_win + (int64_t)(c + f) * kk;
                             }
-                            // staged / window rows are k doubles apart (128 B at k = 16: every row
-                            // starts on bank 0): odd k-lanes load the column blocks in swapped order,
-                            // so one LDS covers both 16-bank halves (2 wavefronts, not 4)
-                            const int sw = RNA == 2 ? (kq & 1) : 0;
 #pragma unroll
-                            for (int t = 0; t < RNA; ++t) {
-                                const int i = t ^ sw;
+                            for (int i = 0; i < RNA; ++i) {
                                 const int col = 8 * i + mg;
                                 const bool ok = rin && col < k;
-                                const double ea = ok ? erow[col] : 0.0;
-                                const double eb = ok ? w_scr[lr * TSR + col] : 0.0;
-                                const double ec = (RED == 1 && ok) ? E1[(int64_t)tr * k + col] : 0.0;
-#pragma unroll
-                                for (int q = 0; q < RNA; ++q)
-                                    if (q == i) {
-                                        af[q] = ea;
-                                        bf[q] = eb;
-                                        if constexpr (RED == 1) cf[q] = ec;
-                                    }
+                                af[i] = ok ? erow[col] : 0.0;
+                                bf[i] = ok ? w_scr[lr * TS + col] : 0.0;
+                                if constexpr (RED == 1) cf[i] = ok ? E1[(int64_t)tr * k + col] : 0.0;
                             }
 #pragma unroll
                             for (int i = 0; i < RNA; ++i)
@@ -903,9 +894,7 @@ bspmm_win_kernel(const BandArgs w) {
                                 for (int j = 0; j < RNA; ++j) {
                                     dmma(g0[i][j][0], g0[i][j][1], af[i], bf[j]);
                                     if constexpr (RED == 1) dmma(g1[i][j][0], g1[i][j][1], af[i], cf[j]);
-                                    // X^T X is symmetric: the blocks below the diagonal are written
-                                    // from the transposed upper blocks at the end
-                                    if constexpr (RED == 4) if (j >= i) dmma(g1[i][j][0], g1[i][j][1], af[i], af[j]);
+                                    if constexpr (RED == 4) dmma(g1[i][j][0], g1[i][j][1], af[i], af[j]);
                                 }
                         }
                     __syncwarp();
@@ -926,11 +915,19 @@ bspmm_win_kernel(const BandArgs w) {
 #pragma unroll
                     for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
                     const int row = (pass0 + lr / WR) * RPP + warp * WR + lr % WR;
+                    // k-step outer, output block inner: NKO independent accumulator chains in
+                    // flight instead of one dependent chain of NQ DMMAs per output block
+                    double dd[NKO][2];
+#pragma unroll
+                    for (int nb = 0; nb < NKO; ++nb) dd[nb][0] = dd[nb][1] = 0.0;
+#pragma unroll
+                    for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+                        for (int nb = 0; nb < NKO; ++nb)
+                            dmma(dd[nb][0], dd[nb][1], af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
 #pragma unroll
                     for (int nb = 0; nb < NKO; ++nb) {
-                        double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-                        for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                        const double d0 = dd[nb][0], d1 = dd[nb][1];
                         const int c = 8 * nb + 2 * kq;
                         if (rv && pass0 + lr / WR < passes && row < nr && c < a.kout) {
                             double* yp = a.Y + (r0 + row) * a.ldy + c;
@@ -972,20 +969,9 @@ bspmm_win_kernel(const BandArgs w) {
                 double* d = s_red + warp * NOUT + (8 * i + mg) * KBP + c;
                 d[0] = g0[i][j][0];
                 d[1] = g0[i][j][1];
-                if constexpr (RED == 1) {
+                if constexpr (TWO) {
                     d[k] = g1[i][j][0];
                     d[k + 1] = g1[i][j][1];
-                }
-                if constexpr (RED == 4) {
-                    if (j >= i) {
-                        d[k] = g1[i][j][0];
-                        d[k + 1] = g1[i][j][1];
-                    }
-                    if (j > i && 8 * i + mg < k) {   // block (j, i) = block (i, j)^T
-                        double* e = s_red + warp * NOUT + k + 8 * i + mg;
-                        e[c * KBP] = g1[i][j][0];
-                        e[(c + 1) * KBP] = g1[i][j][1];
-                    }
                 }
             }
         if constexpr (RED == 2) {
@@ -1066,7 +1052,7 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
         constexpr int scr_rows = (NC / 32) * ((32 / LANES) < 8 ? 8 : (32 / LANES));
         (void)tr;
         const int cb = TCE ? ((KP / 4) * (KP / 8) * 32 + scr_rows * (KP + 2)) * 8
-                           : (RED ? RPP * (KP == 16 ? 24 : KP) : KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
+                           : (RED ? RPP * (KP + 2) : KP * KP + (HAS_C ? RPP * (KP + 1) : 0)) * 8;
         return 16 * 8 + kMetaDepth * 8 + cb;
     };
     // two CTAs per SM: half the shared memory each (the fused-reduction kernels also hold a few
@@ -1216,14 +1202,12 @@ bool launch_bspmm_win_red(const SpmmArgs& a, const BandPlan& p, cudaStream_t st,
     ra.ro.ka = k;
     ra.ro.kb = (red == 1 || red == 4 ? 2 : 1) * k;
     ra.ro.kw = k;
-    // (BK_RED_CTAS=1: one CTA per SM with a deeper ring -- A/B)
-    static const int rc = env_int("BK_RED_CTAS", 2) == 1 ? 1 : 2;
 #define BK_RED(KP_, KX)                                                                              \
     switch (red) {                                                                               \
-        case 1: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 1>(a, p, st, rc, true, &ra);  \
-        case 2: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 2>(a, p, st, rc, true, &ra);  \
-        case 4: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 4>(a, p, st, rc, true, &ra);  \
-        default: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 3>(a, p, st, rc, true, &ra); \
+        case 1: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 1>(a, p, st, 2, true, &ra);   \
+        case 2: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 2>(a, p, st, 2, true, &ra);   \
+        case 4: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 4>(a, p, st, 2, true, &ra);   \
+        default: return launch_win_t<KP_, 4, false, 3, 5, KX, 256, 3>(a, p, st, 2, true, &ra);  \
     }
     if (k == 8) { BK_RED(8, true) }
     if (k == 16) { BK_RED(16, true) }

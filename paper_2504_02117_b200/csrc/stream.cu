@@ -160,25 +160,59 @@ __device__ __forceinline__ void upd_tile_mma(const UpdStream& U, const double* P
 #pragma unroll
         for (int ks = 0; ks < NQ; ++ks) af[ks] = rin ? Pt[(int64_t)r * kp + 4 * ks + kq] : 0.0;
         __syncwarp();   // in place (out == P) on a direct tile: the row is read before any lane writes it
+        // k <= 16: k-step outer, so the NK output blocks are independent DMMA chains in flight;
+        // k > 16 (sC already holds 2 NQ NK registers): one output block at a time
+        if constexpr (NQ * NK <= 8) {
+            double dd[NK][2];
 #pragma unroll
-        for (int nb = 0; nb < NK; ++nb) {
-            const int c = 8 * nb + 2 * kq;
-            const bool cin = rin && c < k;   // (k % 8 == 4: the last block is half outside)
-            double d0 = 0.0, d1 = 0.0;
-            if (cin && Xt) {
-                const double2 x = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
-                d0 = U.a * x.x;
-                d1 = U.a * x.y;
-            }
-            if (cin && Wt) {
-                const double2 w = *reinterpret_cast<const double2*>(Wt + (int64_t)r * k + c);
-                d0 = fma(wv, w.x, d0);
-                d1 = fma(wv, w.y, d1);
+            for (int nb = 0; nb < NK; ++nb) {
+                const int c = 8 * nb + 2 * kq;
+                const bool cin = rin && c < k;   // (k % 8 == 4: the last block is half outside)
+                double d0 = 0.0, d1 = 0.0;
+                if (cin && Xt) {
+                    const double2 x = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
+                    d0 = U.a * x.x;
+                    d1 = U.a * x.y;
+                }
+                if (cin && Wt) {
+                    const double2 w = *reinterpret_cast<const double2*>(Wt + (int64_t)r * k + c);
+                    d0 = fma(wv, w.x, d0);
+                    d1 = fma(wv, w.y, d1);
+                }
+                dd[nb][0] = d0;
+                dd[nb][1] = d1;
             }
             // D(row = mg, cols 2kq, 2kq+1): the accumulator layout of m8n8k4
 #pragma unroll
-            for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], bf[ks][nb]);
-            if (cin) *reinterpret_cast<double2*>(U.out + (r0 + r) * U.ldo + c) = make_double2(d0, d1);
+            for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+                for (int nb = 0; nb < NK; ++nb) dmma(dd[nb][0], dd[nb][1], af[ks], bf[ks][nb]);
+#pragma unroll
+            for (int nb = 0; nb < NK; ++nb) {
+                const int c = 8 * nb + 2 * kq;
+                if (rin && c < k)
+                    *reinterpret_cast<double2*>(U.out + (r0 + r) * U.ldo + c) = make_double2(dd[nb][0], dd[nb][1]);
+            }
+        } else {
+#pragma unroll
+            for (int nb = 0; nb < NK; ++nb) {
+                const int c = 8 * nb + 2 * kq;
+                const bool cin = rin && c < k;
+                double d0 = 0.0, d1 = 0.0;
+                if (cin && Xt) {
+                    const double2 x = *reinterpret_cast<const double2*>(Xt + (int64_t)r * k + c);
+                    d0 = U.a * x.x;
+                    d1 = U.a * x.y;
+                }
+                if (cin && Wt) {
+                    const double2 w = *reinterpret_cast<const double2*>(Wt + (int64_t)r * k + c);
+                    d0 = fma(wv, w.x, d0);
+                    d1 = fma(wv, w.y, d1);
+                }
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) dmma(d0, d1, af[ks], bf[ks][nb]);
+                if (cin) *reinterpret_cast<double2*>(U.out + (r0 + r) * U.ldo + c) = make_double2(d0, d1);
+            }
         }
     }
 }
