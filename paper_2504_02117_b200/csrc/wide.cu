@@ -416,8 +416,10 @@ bool launch_gram_wide(int64_t n, int ka, int kb, const double* V, int64_t ldv, c
     return true;
 }
 
-// out = a Xin + s V H (Xin, out: n x k, ld k; V: n x ka, ldv; H: ka x k device); false = not applicable
-bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
+// out = a Xin + s V H (Xin, out: n x k, ld k; V: n x ka, ldv; H: ka x k device); false = not applicable.
+// dry: plan only (a column split launches its parts only after every part has a plan, so a
+// false return never leaves a partial update behind for the caller's fallback)
+static bool update_wide_impl(const UpdArgs& u, cudaStream_t st, bool dry) {
     // (small systems: launch-bound, the generic kernel has less fixed cost for narrow V)
     const bool small_n = u.n < 65536;
     if (!wide_enabled() || u.n <= 0 || u.kp < (small_n ? 16 : 4) || u.kp > 2048 || u.k < 1 || u.k > 32 || u.W)
@@ -441,29 +443,46 @@ bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
     const int NK = (u.k + 7) / 8;
     const int red_bytes = 128 * 8 * NK * 8;
     const int64_t hf_bytes = (int64_t)((u.kp + 3) / 4) * NK * 32 * 8;
-    // the largest tile (128, 64 or 32 rows) with >= 2 stages: a tile costs two CTA barriers and
-    // a single producer thread ~1 us per tile, so small tiles are latency-bound (c3 k = 12:
-    // 32-row tiles 1.7 TB/s; measured: 16 / 8-row tiles lose to the generic kernel); H
-    // fragments in shared memory if they fit
+    // s H as shared-memory B fragments, then the largest tile (128, 64 or 32 rows) with >= 2
+    // stages: a tile costs two CTA barriers and a single producer thread ~1 us per tile (16 / 8-row
+    // tiles measured slower than the generic kernel); without the fragments every DMMA waits on
+    // an L1 load of H (c3 GMRES(64), k = 12: 64-row tiles without them 1.3 TB/s, 32-row tiles
+    // with them 3.4-3.8 TB/s), so a wider V is split instead
     int smem = 0;
     bool ok = false;
-    for (int rb = small_n ? 4 : 16; rb >= 4 && !ok; rb /= 2) {
-        if (!geometry(w, u.n, 8 * rb, &tmV, &tmW)) return false;
-        w.rb = rb;
-        for (int hf = 1; hf >= 0 && !ok; --hf) {
-            if (hf && hf_bytes > 64 * 1024) continue;
+    if (hf_bytes <= 64 * 1024) {
+        for (int rb = small_n ? 4 : 16; rb >= 4 && !ok; rb /= 2) {
+            // (the TMA encoder refuses some large boxes, e.g. 240 columns x 128 rows: next tile size)
+            if (!geometry(w, u.n, 8 * rb, &tmV, &tmW)) continue;
+            w.rb = rb;
             for (int ns = WSTAGES; ns >= 2 && !ok; --ns) {
-                const int64_t need = (int64_t)ns * w.stage_bytes + 64 + red_bytes + (hf ? hf_bytes : 0);
+                const int64_t need = (int64_t)ns * w.stage_bytes + 64 + red_bytes + hf_bytes;
                 if (need <= 227 * 1024) {
                     w.ns = ns;
-                    w.hfrag = hf;
+                    w.hfrag = 1;
                     smem = (int)need;
                     ok = true;
                 }
             }
         }
     }
-    if (!ok) return false;
+    if (!ok) {
+        // too wide for a 32-row tile with its H fragments: split the contraction over V's columns,
+        // out = a Xin + s V[:, :h] H[:h, :], then out += s V[:, h:] H[h:, :] (the second part reads
+        // out as its Xin, tile by tile before writing it: one extra N x k round trip per split)
+        if (u.kp < 32 || ((uintptr_t)u.out & 15) || (u.ldo * 8) % 16) return false;   // out must be a TMA operand
+        const int h = ((u.kp / 2) + 3) & ~3;
+        UpdArgs lo = u, hi = u;
+        lo.kp = h;
+        hi.P = u.P + h;
+        hi.C = u.C + (int64_t)h * u.k;
+        hi.kp = u.kp - h;
+        hi.a = 1.0;
+        hi.Xin = u.out;
+        hi.ldxin = u.ldo;
+        return update_wide_impl(lo, st, dry) && update_wide_impl(hi, st, dry);
+    }
+    if (dry) return true;
     static int nsm = 0;
     if (!nsm) {
         int dev = 0;
@@ -481,6 +500,10 @@ bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
     BK_UW(1) BK_UW(2) BK_UW(3) BK_UW(4)
 #undef BK_UW
     return false;
+}
+
+bool launch_update_wide(const UpdArgs& u, cudaStream_t st) {
+    return update_wide_impl(u, st, true) && update_wide_impl(u, st, false);
 }
 
 }  // namespace bk

@@ -723,3 +723,22 @@ def test_dirk_window_from_library_theta_method(ctx, bk):
     assert st == 0, rep
     Yt = oracle.theta_stepping(K, mass, theta, b, y0, tau, s)
     assert np.linalg.norm(Y.cpu().numpy() - Yt) / np.linalg.norm(Yt) <= 1e-8
+
+
+@pytest.mark.parametrize("kp", [96, 240, 288, 516, 576, 780])
+def test_update_wide_strided_basis_split(ctx, bk, kp):
+    """W = a W + s [V_0 .. V_j] H over a strided GMRES basis (ld = 65 k, k = 12) at n > 65 536
+    rows with a ragged last tile: the wide TMA update, split over V's columns once H's
+    fragments and a 32-row tile no longer fit (kp = 516, 576, 780); kp = 240 has a 240 x 128
+    box the TMA encoder refuses (next tile size)."""
+    n, k, ldv = 70001, 12, 65 * 12
+    V = synth.multivector(n, ldv, 3)
+    H = synth.small_dense(kp, k, 6)
+    W0 = synth.multivector(n, k, 4)
+    for a, s in ((1.0, -1.0), (0.0, 1.0)):
+        Wd = cu(W0)
+        bk.block_update(ctx, Wd, cu(V)[:, :kp], cu(H), a=a, s=s)
+        Vs = V[:, :kp].contiguous()
+        ref = oracle.update(W0, Vs, H, a, s)
+        scale = abs(a) * np.abs(W0.numpy()) + abs(s) * (np.abs(Vs.numpy()) @ np.abs(H.numpy()))
+        check_close(Wd.cpu().numpy(), ref, scale, what=f"wide update kp={kp} a={a}")

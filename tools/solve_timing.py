@@ -47,5 +47,5 @@ for it in [int(x) for x in a.iters.split(",")]:
             ts.append(e0.elapsed_time(e1))
     out[it] = statistics.median(ts)
 its = sorted(out)
-slope = (out[its[-1]] - out[its[0]]) / (its[-1] - its[0])
+slope = (out[its[-1]] - out[its[0]]) / (its[-1] - its[0]) if len(its) > 1 else None
 print(json.dumps({"cfg": a.cfg, "k": a.k, "method": a.method, "ms": out, "ms_per_iter_slope": slope}))
