@@ -1064,7 +1064,11 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     if (tr_env > 0) {
         TR = std::max(2, tr_env & ~1);
     } else if (ctas == 2 && big_tiles) {   // the largest multiple of 16 rows with two stages per CTA
-        for (int t = std::min(1024, 8 * RPP) & ~15; t >= 64; t -= 16) {
+        // (fused reductions: a multiple of the RPP rows of one pass, so no pass runs its DMMA
+        // epilogue on mostly empty row blocks -- c2 k = 16 RED 2 with 80-row tiles (64 + 16-row
+        // passes) 131 us, with 64-row tiles 124 us)
+        const int step = (RED > 0 && RPP >= 16) ? RPP : 16;
+        for (int t = (std::min(1024, 8 * RPP) / step) * step; t >= 64; t -= step) {
             layout(t);
             if (2 * w.stage_bytes + fixed_for(t) <= kHalf) {
                 TR = t;
