@@ -780,6 +780,60 @@ bspmm_win_kernel(const BandArgs w) {
 #pragma unroll
             for (int t = 0; t < 4; ++t) dd0[t] = dd1[t] = 0.0;
     }
+    // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA by the warp itself over its NR scratch
+    // rows (no CTA barrier, so the other warps keep gathering); rowof(lr, grow)
+    // gives scratch row lr's global row and whether it is stored
+    auto tce_epi = [&](auto&& rowof) {
+        if constexpr (TCE) {
+            constexpr int NR = PP * WR, NB8 = (NR + 7) / 8;
+            const double* w_scr = s_tT + warp * NR * TS;
+            __syncwarp();
+            const int mg = lane32 >> 2, kq = lane32 & 3;
+#pragma unroll
+            for (int b = 0; b < NB8; ++b) {
+                const int lr = 8 * b + mg;
+                int64_t grow = 0;
+                const bool rv = lr < NR && rowof(lr, grow);
+                double af[NQ];
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
+                // k-step outer, output block inner: NKO independent accumulator chains in
+                // flight instead of one dependent chain of NQ DMMAs per output block
+                double dd[NKO][2];
+#pragma unroll
+                for (int nb = 0; nb < NKO; ++nb) dd[nb][0] = dd[nb][1] = 0.0;
+#pragma unroll
+                for (int ks = 0; ks < NQ; ++ks)
+#pragma unroll
+                    for (int nb = 0; nb < NKO; ++nb)
+                        dmma(dd[nb][0], dd[nb][1], af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
+#pragma unroll
+                for (int nb = 0; nb < NKO; ++nb) {
+                    const double d0 = dd[nb][0], d1 = dd[nb][1];
+                    const int c = 8 * nb + 2 * kq;
+                    if (rv && c < a.kout) {
+                        double* yp = a.Y + grow * a.ldy + c;
+                        double v0 = a.alpha * d0, v1 = a.alpha * d1;
+                        if (a.beta != 0.0) {
+                            v0 = fma(a.beta, yp[0], v0);
+                            if (c + 1 < a.kout) v1 = fma(a.beta, yp[1], v1);
+                        }
+                        if (c + 1 < a.kout) __stcs(reinterpret_cast<double2*>(yp), make_double2(v0, v1));
+                        else __stcs(yp, v0);
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    };
+    // coupled k > 16 with one pass per tile (TR <= RPP, e.g. k = 32 on 64-row tiles): a DMMA
+    // block pairs the warp's rows of TWO consecutive tiles of this CTA (scratch halves xq = 0, 1;
+    // each stage is released right after its gathers) instead of padding every block with a
+    // second, empty pass (half the epilogue's tensor-core work was on zero rows)
+    const bool xt = TCE && PP == 2 && passes == 1;
+    int xq = 0;
+    int64_t xr0a = 0, xr0b = 0;   // (scalars: a dynamically indexed pair would live in local memory)
+    int xnra = 0, xnrb = 0;
     int s = 0;
     uint32_t ph = 0;
     for (int tile = blockIdx.x; tile < w.ntiles; tile += gridDim.x) {
@@ -799,6 +853,44 @@ bspmm_win_kernel(const BandArgs w) {
             const bool on = g < w.G;
             thr[g] = on ? (int)(r0 + w.lo[g]) : INT_MAX;
             fo[g] = on ? (int)(w.wb[g] - (r0 + w.lo[g])) : 0;
+        }
+        if constexpr (TCE && PP == 2) {
+            if (xt) {
+                const int r = grp;   // the tile's single pass
+                const bool active = r < nr;
+                double acc[VEC];
+#pragma unroll
+                for (int t = 0; t < VEC; ++t) acc[t] = 0.0;
+                if (active) {
+                    const int rs = s_rp[r], re = s_rp[r + 1];
+                    if (re > rs) {
+                        const int gr = (int)(r0 + r);
+                        const int sw = (kk <= 16) ? (((gr * kk) >> 4) & 1) : (gr & 1);
+                        band_accumulate<VEC, NB, MR, SPLIT>(s_win, scol, sval, rs, re, thr, fo, kk, c0, sw, acc);
+                    }
+                }
+                double* tp = s_tT + warp * (PP * WR) * TS + (xq * WR + lane32 / LANES) * TS;
+                reinterpret_cast<double2*>(tp + cA)[0] =
+                    (active && cA < a.k) ? make_double2(acc[0], acc[1]) : make_double2(0.0, 0.0);
+                reinterpret_cast<double2*>(tp + cB)[0] =
+                    (active && cB < a.k) ? make_double2(acc[2], acc[3]) : make_double2(0.0, 0.0);
+                if (xq) { xr0b = r0; xnrb = nr; } else { xr0a = r0; xnra = nr; }
+                __syncwarp();
+                if (lane32 == 0) mbar_arrive(&empty[s]);   // the scratch holds what the epilogue needs
+                if (xq == 1) {
+                    tce_epi([&](int lr, int64_t& grow) {
+                        const int h = lr / WR, row = warp * WR + lr % WR;
+                        grow = (h ? xr0b : xr0a) + row;
+                        return row < (h ? xnrb : xnra);
+                    });
+                }
+                xq ^= 1;
+                if (++s == w.ns) {
+                    s = 0;
+                    ph ^= 1u;
+                }
+                continue;
+            }
         }
 #pragma unroll 1
         for (int pass0 = 0; pass0 < passes; pass0 += PP) {
@@ -901,47 +993,11 @@ bspmm_win_kernel(const BandArgs w) {
                 }
             }
             if constexpr (TCE) {
-                // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA by the warp itself: no CTA
-                // barrier, so the other warps keep gathering
-                constexpr int NR = PP * WR, NB8 = (NR + 7) / 8;
-                const double* w_scr = s_tT + warp * NR * TS;
-                __syncwarp();
-                const int mg = lane32 >> 2, kq = lane32 & 3;
-#pragma unroll
-                for (int b = 0; b < NB8; ++b) {
-                    const int lr = 8 * b + mg;
-                    const bool rv = lr < NR;
-                    double af[NQ];
-#pragma unroll
-                    for (int ks = 0; ks < NQ; ++ks) af[ks] = rv ? w_scr[lr * TS + 4 * ks + kq] : 0.0;
+                tce_epi([&](int lr, int64_t& grow) {
                     const int row = (pass0 + lr / WR) * RPP + warp * WR + lr % WR;
-                    // k-step outer, output block inner: NKO independent accumulator chains in
-                    // flight instead of one dependent chain of NQ DMMAs per output block
-                    double dd[NKO][2];
-#pragma unroll
-                    for (int nb = 0; nb < NKO; ++nb) dd[nb][0] = dd[nb][1] = 0.0;
-#pragma unroll
-                    for (int ks = 0; ks < NQ; ++ks)
-#pragma unroll
-                        for (int nb = 0; nb < NKO; ++nb)
-                            dmma(dd[nb][0], dd[nb][1], af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
-#pragma unroll
-                    for (int nb = 0; nb < NKO; ++nb) {
-                        const double d0 = dd[nb][0], d1 = dd[nb][1];
-                        const int c = 8 * nb + 2 * kq;
-                        if (rv && pass0 + lr / WR < passes && row < nr && c < a.kout) {
-                            double* yp = a.Y + (r0 + row) * a.ldy + c;
-                            double v0 = a.alpha * d0, v1 = a.alpha * d1;
-                            if (a.beta != 0.0) {
-                                v0 = fma(a.beta, yp[0], v0);
-                                if (c + 1 < a.kout) v1 = fma(a.beta, yp[1], v1);
-                            }
-                            if (c + 1 < a.kout) __stcs(reinterpret_cast<double2*>(yp), make_double2(v0, v1));
-                            else __stcs(yp, v0);
-                        }
-                    }
-                }
-                __syncwarp();
+                    grow = r0 + row;
+                    return pass0 + lr / WR < passes && row < nr;
+                });
             }
         }
         __syncwarp();
@@ -950,6 +1006,15 @@ bspmm_win_kernel(const BandArgs w) {
         if (++s == w.ns) {
             s = 0;
             ph ^= 1u;
+        }
+    }
+    if constexpr (TCE && PP == 2) {
+        if (xt && xq == 1) {   // an odd number of tiles: the last half pairs with nothing
+            tce_epi([&](int lr, int64_t& grow) {
+                const int row = warp * WR + lr % WR;
+                grow = xr0a + row;
+                return lr < WR && row < xnra;
+            });
         }
     }
     if constexpr (RED > 0) {

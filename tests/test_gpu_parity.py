@@ -742,3 +742,21 @@ def test_update_wide_strided_basis_split(ctx, bk, kp):
         ref = oracle.update(W0, Vs, H, a, s)
         scale = abs(a) * np.abs(W0.numpy()) + abs(s) * (np.abs(Vs.numpy()) @ np.abs(H.numpy()))
         check_close(Wd.cpu().numpy(), ref, scale, what=f"wide update kp={kp} a={a}")
+
+
+@pytest.mark.parametrize("k", [24, 32])
+def test_coupled_apply_pairs_tiles_bitwise(ctx, bk, k):
+    """Coupled apply at k > 16 on one-pass (64-row) tiles: each DMMA block pairs the warp's rows
+    of two consecutive tiles of a CTA.  161^2 rows = 406 tiles over the 148
+    CTAs: CTAs with 2 and 3 tiles (an unpaired last half) and a ragged last tile; bitwise on
+    integer data, beta = 0 (Y not read) and beta != 0."""
+    A = synth.convdiff2d(161, integer=True)
+    M = bk.Matrix.from_csr(ctx, A)
+    X = synth.multivector(A.n_rows, k, 3, integer=True)
+    C = synth.small_dense(k, k, 6, integer=True)
+    Y0 = synth.multivector(A.n_rows, k, 4, integer=True)
+    for alpha, beta in ((1.0, 0.0), (-2.0, 3.0)):
+        Y = cu(Y0) if beta else torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
+        bk.bspmm_apply(ctx, M, cu(X), Y, C=cu(C), alpha=alpha, beta=beta)
+        torch.cuda.synchronize()
+        assert np.array_equal(Y.cpu().numpy(), oracle.spmm(A, X, C, alpha=alpha, beta=beta, Y=Y0)), (k, beta)
