@@ -530,6 +530,7 @@ struct BandArgs {
     int off_e[2];
     RedOut ro;
     SmallEpi epi;
+    int pf;             // L2 prefetch distance in tiles of this CTA (0: off)
 };
 constexpr int kMetaDepth = 8;   // tiles whose row-pointer bounds are in flight
 
@@ -676,7 +677,13 @@ bspmm_win_kernel(const BandArgs w) {
         uint32_t ph = 0;
         int i = 0;
         for (int tile = blockIdx.x; tile < w.ntiles; tile += gridDim.x, ++i) {
-            asm volatile("cp.async.wait_group %0;" ::"n"(kMetaDepth - 1) : "memory");
+            int2 pq = make_int2(0, 0);   // row-pointer bounds of the tile prefetched (w.pf == 1)
+            if (w.pf == 1) {
+                asm volatile("cp.async.wait_group %0;" ::"n"(kMetaDepth - 2) : "memory");
+                pq = s_pp[slot + 1 == kMetaDepth ? 0 : slot + 1];
+            } else {
+                asm volatile("cp.async.wait_group %0;" ::"n"(kMetaDepth - 1) : "memory");
+            }
             const int2 pp = s_pp[slot];
             fetch(tile + kMetaDepth * gridDim.x, slot);
             slot = (slot + 1 == kMetaDepth) ? 0 : slot + 1;
@@ -739,6 +746,31 @@ bspmm_win_kernel(const BandArgs w) {
 #pragma unroll
                 for (int j = 0; j < NE; ++j)
                     bulk_g2s(st + w.off_e[j], w.e[j] + r0 * k, (uint32_t)nr * kb, &full[s], pol_once);
+            }
+            // L2 prefetch of what this CTA's tile pf tiles ahead reads from DRAM first: its
+            // leading band segment (the other bands were fetched by earlier tiles), its rows of
+            // the streamed operands and (pf == 1) its CSR ranges -- the ring's stages then wait
+            // on L2, not on DRAM
+            const int t2 = tile + w.pf * (int)gridDim.x;
+            if (w.pf > 0 && t2 < w.ntiles) {
+                const int64_t q0 = a.row0 + (int64_t)t2 * w.TR;
+                const int nq = (int)((rend - q0) < w.TR ? (rend - q0) : w.TR);
+                if constexpr (NE > 0) {
+#pragma unroll
+                    for (int j = 0; j < NE; ++j) bulk_prefetch_l2(w.e[j] + q0 * k, (uint32_t)nq * kb);
+                }
+                const int g = w.G - 1;
+                const int64_t lo = q0 + w.lo[g];
+                const int64_t a0 = lo < 0 ? 0 : lo;
+                int64_t b0 = q0 + nq + w.hi[g];
+                if (b0 > w.ncols) b0 = w.ncols;
+                const uint32_t xb = b0 > a0 ? ((uint32_t)(b0 - a0) * kb) & ~15u : 0u;
+                if (xb) bulk_prefetch_l2(a.X + a0 * k, xb);
+                if (w.pf == 1 && pq.y > pq.x) {
+                    const int qc = pq.x & ~3, qv = pq.x & ~1;
+                    bulk_prefetch_l2(a.col + qc, (uint32_t)(((pq.y - qc + 3) & ~3) * 4));
+                    bulk_prefetch_l2(a.val + qv, (uint32_t)(((pq.y - qv + 1) & ~1) * 8));
+                }
             }
             if (++s == w.ns) {
                 s = 0;
@@ -1080,6 +1112,13 @@ bool launch_win_t(const SpmmArgs& a, const BandPlan& p, cudaStream_t st, int cta
     BandArgs w{};
     w.a = a;
     w.G = p.nbands;
+    // L2 prefetch one tile ahead (A/B, profiles/r02/e19_prefetch.txt, c2): RED 1 / 2 at k = 16
+    // 139 / 127 -> 132 / 119 us, k = 8 75 / 71 -> 73 / 68 us; plain apply k = 8 / 16 37.9 / 64.5 ->
+    // 35.8 / 62.5 us.  Off where it measured slower: RED 3 (111 -> 116 us), plain k = 32 (129 ->
+    // 142 us: the 8-lane rows already keep enough bytes in flight), coupled applies.
+    static const int pf_red = env_int("BK_RED_PF", -1), pf_win = env_int("BK_WIN_PF", -1);
+    const int pf_dflt = ((RED == 1 || RED == 2) || (RED == 0 && !HAS_C && (KP == 8 || KP == 16))) ? 1 : 0;
+    w.pf = RED > 0 ? (pf_red >= 0 ? pf_red : pf_dflt) : (HAS_C ? 0 : (pf_win >= 0 ? pf_win : pf_dflt));
     if constexpr (RED > 0) {
         w.e[0] = ra->e0;
         w.e[1] = ra->e1;
