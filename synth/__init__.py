@@ -462,6 +462,28 @@ def coupling_c1() -> torch.Tensor:
     return (A2 - beta * torch.eye(4, dtype=torch.float64)).T.contiguous()
 
 
+INT_TABLEAU4 = [[2, 0, 0, 0], [1, 2, 0, 0], [-3, 1, 2, 0], [2, -1, 3, 2]]   # integer stand-in (bitwise tests)
+
+
+def window_coupling(k: int, stages: int, *, tau: float = 0.12, integer: bool = False,
+                    eliminated: bool = False) -> torch.Tensor:
+    """C = (A2 - beta I)^T of a window of k / stages steps of an SDIRK
+    scheme with ``stages`` stages (2: SDIRK2, 3: Alexander's SDIRK3, 4: an integer
+    lower-triangular stand-in).  ``eliminated`` adds the a_{i1} column of an eliminated
+    explicit first stage.  The structured (mostly zero) coupling the paper's
+    windows give, next to the dense random ``small_dense`` one."""
+    assert k % stages == 0
+    tab = {2: SDIRK2, 3: SDIRK3, 4: INT_TABLEAU4}[stages]
+    if integer:
+        tab = [[float(round(4 * v)) for v in row] for row in tab] if stages != 4 else tab
+    a_elim = [float(i + 1) for i in range(stages)] if eliminated else None
+    if a_elim is not None and not integer:
+        a_elim = [v / 8.0 for v in a_elim]
+    _, A2 = window_matrices(tab, k // stages, tau, a_elim=a_elim)
+    beta = float(A2[0, 0])
+    return (A2 - beta * torch.eye(k, dtype=torch.float64)).T.contiguous()
+
+
 # ---------------------------------------------------------------------------
 # Named configurations (BASELINE.json configs, SURVEY.md §8(d))
 # ---------------------------------------------------------------------------

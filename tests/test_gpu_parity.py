@@ -760,3 +760,48 @@ def test_coupled_apply_pairs_tiles_bitwise(ctx, bk, k):
         bk.bspmm_apply(ctx, M, cu(X), Y, C=cu(C), alpha=alpha, beta=beta)
         torch.cuda.synchronize()
         assert np.array_equal(Y.cpu().numpy(), oracle.spmm(A, X, C, alpha=alpha, beta=beta, Y=Y0)), (k, beta)
+
+
+@pytest.mark.parametrize("k", [8, 12, 16, 24, 32])
+def test_coupled_apply_sparse_coupling_bitwise(ctx, bk, k):
+    """Coupled apply with the structured couplings of a time-stepping window, C = (A2 - beta I)^T
+    (A2 = I_s (x) A): the DMMA epilogues skip C's all-zero 4 x 8 fragments
+    (DESIGN.md §4.1).  Windowed 2-D kernel, 3-D gather kernel and the unstructured gather path;
+    window couplings of 2 / 4 stages with and without the eliminated-stage column, a single
+    non-zero entry, an all-zero C (Y = beta Y) and a dense C: bitwise on integer inputs."""
+    cases = [synth.convdiff2d(161, integer=True), synth.diffreact3d(20, integer=True)]
+    Cs = {"w2": synth.window_coupling(k, 2, integer=True),
+          "w4e": synth.window_coupling(k, 4, integer=True, eliminated=True),
+          "zero": torch.zeros(k, k, dtype=torch.float64),
+          "dense": synth.small_dense(k, k, 6, integer=True)}
+    one = torch.zeros(k, k, dtype=torch.float64)
+    one[k - 1, 0] = 3.0
+    Cs["one"] = one
+    for A in cases:
+        M = bk.Matrix.from_csr(ctx, A)
+        X = synth.multivector(A.n_rows, k, 3, integer=True)
+        Y0 = synth.multivector(A.n_rows, k, 4, integer=True)
+        for name, C in Cs.items():
+            for alpha, beta in ((1.0, 0.0), (-2.0, 3.0)):
+                Y = cu(Y0) if beta else torch.full((A.n_rows, k), float("nan"), dtype=torch.float64, device="cuda")
+                bk.bspmm_apply(ctx, M, cu(X), Y, C=cu(C), alpha=alpha, beta=beta)
+                torch.cuda.synchronize()
+                ref = oracle.spmm(A, X, C, alpha=alpha, beta=beta, Y=Y0)
+                assert np.array_equal(Y.cpu().numpy(), ref), (A.name, k, name, beta)
+
+
+@pytest.mark.parametrize("k,stages", [(8, 2), (12, 3), (16, 2), (30, 3), (32, 2)])
+def test_coupled_apply_window_coupling_random(ctx, bk, k, stages):
+    """The SDIRK window coupling on random data (c1s-size 2-D and a 3-D lattice), componentwise
+    1e-12 bound (R17)."""
+    for A in (synth.convdiff2d(97), synth.diffreact3d(16)):
+        M = bk.Matrix.from_csr(ctx, A)
+        X = synth.multivector(A.n_rows, k, 3)
+        C = synth.window_coupling(k, stages, eliminated=True)
+        Y0 = synth.multivector(A.n_rows, k, 4)
+        Y = cu(Y0)
+        bk.bspmm_apply(ctx, M, cu(X), Y, C=cu(C), alpha=-0.5, beta=1.0)
+        torch.cuda.synchronize()
+        ref = oracle.spmm(A, X, C, alpha=-0.5, beta=1.0, Y=Y0)
+        scale = 0.5 * oracle.spmm(abs_csr(A), X.abs(), C.abs()) + np.abs(Y0.numpy())
+        check_close(Y.cpu().numpy(), ref, scale, what=f"{A.name} k={k} window coupling")

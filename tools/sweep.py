@@ -64,8 +64,10 @@ def main():
         Y = torch.empty_like(X)
         C = synth.small_dense(k, k, 6, device=dev)
         G = torch.empty(k, k, dtype=torch.float64, device=dev)
+        Cw = synth.window_coupling(k, 2).to(dev) if k % 2 == 0 else C   # SDIRK2 window coupling (sparse)
         ops = {"spmm": (lambda: bk.bspmm_apply(ctx, M, X, Y), pm.spmm_bytes(n, nnz, k)),
                "spmm_C": (lambda: bk.bspmm_apply(ctx, M, X, Y, C=C), pm.spmm_bytes(n, nnz, k)),
+               "spmm_Cw": (lambda: bk.bspmm_apply(ctx, M, X, Y, C=Cw), pm.spmm_bytes(n, nnz, k)),
                "gram": (lambda: bk.block_gram(ctx, X, Y, G), pm.gram_bytes(n, k, k)),
                "update": (lambda: bk.block_update(ctx, Y, X, C, a=1.0, s=1e-3), pm.update_bytes(n, k, k))}
         for op in args.ops.split(","):
