@@ -181,29 +181,13 @@ __device__ __forceinline__ void tile_rows(const SpmmArgs& a, const int* col, con
 // pass (32 / LANES of them) go to a per-warp scratch (TS doubles per row), then
 // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA with C as B fragments
 // ([ks][nb][lane] in shared memory); blocks of 8 rows, rows beyond the warp's share are zero.
-// The window couplings of the paper are sparse (C = (A_2 - beta I)^T: I_s (x) A of a
-// lower-triangular Butcher tableau): bit (ks * KP/8 + nb) of the mask is
-// set iff the 4 x 8 fragment (k-step ks, output block nb) of C has a non-zero entry; the DMMA
-// epilogues skip the others (their products are exact zeros).  Called by whole warps.
-template <int KP>
-__device__ __forceinline__ uint32_t c_fragment_mask(const double* s_Cf) {
-    constexpr int NF = (KP / 4) * (KP / 8);
-    static_assert(NF <= 32, "one 32-bit mask");
-    uint32_t m = 0;
-#pragma unroll
-    for (int f = 0; f < NF; ++f)
-        if (__any_sync(0xffffffffu, s_Cf[f * 32 + (threadIdx.x & 31)] != 0.0)) m |= 1u << f;
-    return m;
-}
-
 template <int KP>
 struct CfRegs { static constexpr int N = (KP <= 16 && KP >= 8) ? (KP / 4) * (KP / 8) : 1; };
 
 template <int KP, int VEC, int NC, int TR>
 __device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col, const double* val, const int* s_rp,
                                               int nr, int64_t r0, int grp, int c0, bool lane_in,
-                                              const double* s_Cf, const double (&cf)[CfRegs<KP>::N], double* w_scr,
-                                              uint32_t cmask) {
+                                              const double* s_Cf, const double (&cf)[CfRegs<KP>::N], double* w_scr) {
     constexpr int NCF = CfRegs<KP>::N;
     constexpr int LANES = KP / VEC;
     constexpr int RPP = NC / LANES;
@@ -247,9 +231,8 @@ __device__ __forceinline__ void tile_rows_tce(const SpmmArgs& a, const int* col,
             for (int ks = 0; ks < NQ; ++ks)
 #pragma unroll
                 for (int nb = 0; nb < NKO; ++nb)
-                    if ((cmask >> (ks * NKO + nb)) & 1u)   // (warp-uniform: all-zero fragments of C skipped)
-                        dmma(dd[nb][0], dd[nb][1], af[ks],
-                             KP <= 16 ? cf[(ks * NKO + nb) % NCF] : s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                    dmma(dd[nb][0], dd[nb][1], af[ks],
+                         KP <= 16 ? cf[(ks * NKO + nb) % NCF] : s_Cf[(ks * NKO + nb) * 32 + lane32]);
 #pragma unroll
             for (int nb = 0; nb < NKO; ++nb) {
                 const double d0 = dd[nb][0], d1 = dd[nb][1];
@@ -372,8 +355,6 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
     double cf[CfRegs<KP>::N];
 #pragma unroll
     for (int q = 0; q < CfRegs<KP>::N; ++q) cf[q] = (TCE && KP <= 16) ? s_C[q * 32 + (tid & 31)] : 0.0;
-    uint32_t cmask = 0;
-    if constexpr (TCE) cmask = c_fragment_mask<KP>(s_C);
     int i = 0;
     for (int tile = tb; tile < te; tile += tstep, ++i) {
         const int s = i % NS;
@@ -391,9 +372,9 @@ bspmm_pipe_kernel(const SpmmArgs a, int ntiles) {
             if (staged) {
                 const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
                 const double* sval = reinterpret_cast<const double*>(st + L::RP_BYTES + L::COL_BYTES) + off - p0;
-                tile_rows_tce<KP, VEC, NC, TR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, cf, w_scr, cmask);
+                tile_rows_tce<KP, VEC, NC, TR>(a, scol, sval, s_rp, nr, r0, grp, c0, lane_in, s_C, cf, w_scr);
             } else {
-                tile_rows_tce<KP, VEC, NC, TR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, cf, w_scr, cmask);
+                tile_rows_tce<KP, VEC, NC, TR>(a, a.col, a.val, s_rp, nr, r0, grp, c0, lane_in, s_C, cf, w_scr);
             }
         } else if (staged) {
             const int* scol = reinterpret_cast<const int*>(st + L::RP_BYTES) + off - p0;
@@ -834,8 +815,6 @@ bspmm_win_kernel(const BandArgs w) {
     // Y(rows) = alpha (A X)(rows) C + beta Y as m8n8k4 DMMA by the warp itself over its NR scratch
     // rows (no CTA barrier, so the other warps keep gathering); rowof(lr, grow)
     // gives scratch row lr's global row and whether it is stored
-    uint32_t cmask = 0;
-    if constexpr (TCE) cmask = c_fragment_mask<KP>(s_Cf);
     auto tce_epi = [&](auto&& rowof) {
         if constexpr (TCE) {
             constexpr int NR = PP * WR, NB8 = (NR + 7) / 8;
@@ -859,8 +838,7 @@ bspmm_win_kernel(const BandArgs w) {
                 for (int ks = 0; ks < NQ; ++ks)
 #pragma unroll
                     for (int nb = 0; nb < NKO; ++nb)
-                        if ((cmask >> (ks * NKO + nb)) & 1u)   // (warp-uniform)
-                            dmma(dd[nb][0], dd[nb][1], af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
+                        dmma(dd[nb][0], dd[nb][1], af[ks], s_Cf[(ks * NKO + nb) * 32 + lane32]);
 #pragma unroll
                 for (int nb = 0; nb < NKO; ++nb) {
                     const double d0 = dd[nb][0], d1 = dd[nb][1];
