@@ -131,20 +131,33 @@ def _is_torch(t):
     return hasattr(t, "data_ptr") and hasattr(t, "is_cuda")
 
 
+_F64 = []
+
+
+def _torch_f64():
+    if not _F64:
+        import torch
+        _F64.append(torch.float64)
+    return _F64[0]
+
+
 def _mv(t, name):
     """(pointer, rows, cols, ld) of a row-major float64 2-D tensor / array."""
     if t is None:
         return None, 0, 0, 0
     if _is_torch(t):
-        import torch
-        if t.dtype != torch.float64:
+        # (hot: a few attribute reads per call -- launches of the narrow kernels are host-bound)
+        if t.dtype is not _torch_f64():
             raise TypeError(f"{name}: dtype must be float64, got {t.dtype}")
-        if t.dim() != 2:
+        sh = t.shape
+        if len(sh) != 2:
             raise ValueError(f"{name}: must be 2-D (rows x k)")
-        if t.shape[1] > 1 and t.stride(1) != 1:
+        rows, cols = sh
+        s0, s1 = t.stride()
+        if cols > 1 and s1 != 1:
             raise ValueError(f"{name}: rows must be contiguous (stride(1) == 1)")
-        ld = t.stride(0) if t.shape[0] > 1 else t.shape[1]
-        return t.data_ptr(), t.shape[0], t.shape[1], max(ld, t.shape[1])
+        ld = s0 if rows > 1 else cols
+        return t.data_ptr(), rows, cols, (ld if ld > cols else cols)
     a = t
     if not isinstance(a, np.ndarray) or a.dtype != np.float64 or a.ndim != 2:
         raise TypeError(f"{name}: expected a float64 2-D numpy array or torch tensor")

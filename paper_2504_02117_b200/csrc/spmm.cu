@@ -462,7 +462,14 @@ void launch_t(const SpmmArgs& a, cudaStream_t st) {
         // (round-1 A/B of ring depth / CTAs per SM / tile size: DESIGN.md §4.1)
         // (2 CTAs x 2 stages x 512-row tiles or 2 x 3 x 256 measured 15-45 % slower on c3 / c4:
         // the gathers need the third CTA's warps for latency hiding)
-        launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304>(a, num_sms_cached(), st);
+        // coupled k > 16: C's fragments and the per-warp DMMA scratch (25.6 KB) next to two
+        // 256-row stages leave room for only TWO CTAs per SM (ncu c4 k = 32 coupled: warps active
+        // 24 % vs 42 % plain, long-scoreboard 53 %: 4.96 ms vs 2.27 ms plain) -- 128-row tiles
+        // keep the third CTA
+        if constexpr (HAS_C && KP == 32)
+            launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 128, 1152>(a, num_sms_cached(), st);
+        else
+            launch_pipe<KP, VEC, HAS_C, 256, 2, 3, 256, 2304>(a, num_sms_cached(), st);
     }
 }
 
@@ -1333,6 +1340,13 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     // L1TEX 83 %).
     static const int wc = env_int("BK_WIN_COUPLED", 1);
     if (a.C != nullptr && !wc) return false;
+    // k = 12 (e.g. 3 stages x 4 steps): the band kernel pads it to four 4-column lanes with a
+    // run-time row stride; the gather kernel has a three-lane instantiation (launch_k) -- c2 plain
+    // 83.0 vs 58.4 us (0.49 vs 0.70 of HBM), coupled 119 vs 87 us (profiles/r02/head/e22_*).
+    static const int w12 = env_int("BK_WIN_K12", 0);
+    if (!w12 && a.k == 12 && a.kout == 12 && a.ldx % 4 == 0 && ((uintptr_t)a.X % 32) == 0 && a.ldy % 2 == 0 &&
+        ((uintptr_t)a.Y % 16) == 0)
+        return false;
     static const int w3 = env_int("BK_WIN_3D", -1);
     // Coupled applies (per-warp DMMA epilogue in both kernels) follow the same rule: c2 k = 16
     // 0.64 band vs 0.52 gather, c4 k = 8 / 16 0.71 / 0.53 gather vs 0.63 / 0.49 band.

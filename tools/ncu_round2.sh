@@ -21,10 +21,11 @@ ncu --set full --clock-control none --import-source on --profile-from-start off 
     -o $O/r2_bcg_tail $STEP > $O/r2_bcg_tail.log 2>&1
 export_rep r2_bcg_tail
 # the fused apply + reduction kernels of the BiCGStab iteration (RED 1: Rt^T[V R]; RED 2: Rt^T T, dots)
-# (the step's windowed-apply launches in order: plain k = 1, 2, 4, 8, 16, then RED 1, RED 2, ...)
+# (the step's windowed-apply launches in order: plain k = 1, 2, 4, 8, 16, then RED 1, RED 2, RED 1, ...;
+# the SECOND iteration's launches are taken: in the first one P, R and Rt all alias B)
 for red in 1 2; do
     ncu --set full --clock-control none --import-source on --profile-from-start off \
-        -k regex:bspmm_win_kernel -s $((4 + red)) -c 1 -o $O/r2_fused_red$red $STEP \
+        -k regex:bspmm_win_kernel -s $((6 + red)) -c 1 -o $O/r2_fused_red$red $STEP \
         > $O/r2_fused_red$red.log 2>&1
     export_rep r2_fused_red$red
 done
