@@ -4,7 +4,7 @@ fraction of HBM peak, vs k; block-Krylov solve time) on B200.
 
 One STEP = one pass of the whole hot path over the c2 workload (BASELINE.json
 configs[1]: 2-D convection-diffusion, 1024 x 1024 cells, 5-point CSR fp64):
-    for k in (1, 2, 4, 8, 16):  bspmm_apply (Y = A X_k), block_gram (X_k^T Y_k),
+    for k in (16, 8, 4, 2, 1):  bspmm_apply (Y = A X_k), block_gram (X_k^T Y_k),
                                 block_update (P_k += 1e-3 X_k C_k)
     + block_krylov_solve: 5 fixed block-BiCGStab iterations at k = 16
 (a1 apply, a3 Gram, a4 small dense, a5 update, a6 solver; a2 halo when N > 1).
