@@ -497,6 +497,14 @@ void launch_k(const SpmmArgs& a, cudaStream_t st, bool vec2) {
             return;
         }
     }
+    if constexpr (KP == 32) {
+        // k = 24: six 4-column lanes per row (KP = 32 leaves two lanes of eight idle); same
+        // 288-consumer / 288-row shape as k = 12 (48 rows per pass, 6 passes)
+        if (vec2 && al32 && a.k == 24 && a.kout == 24 && !a.C && !a.Xg && !a.rows && a.nrows > 0) {
+            launch_pipe<24, 4, false, 288, 2, 3, 288, 2592>(a, num_sms_cached(), st);
+            return;
+        }
+    }
     if constexpr (KP >= 4) {
         if (vec2 && al32 && a.k % 4 == 0 && a.kout % 4 == 0) return launch_kv<KP, 4>(a, st);
     }
@@ -1343,6 +1351,11 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     // k = 12 (e.g. 3 stages x 4 steps): the band kernel pads it to four 4-column lanes with a
     // run-time row stride; the gather kernel has a three-lane instantiation (launch_k) -- c2 plain
     // 83.0 vs 58.4 us (0.49 vs 0.70 of HBM), coupled 119 vs 87 us (profiles/r02/head/e22_*).
+    // (k = 24, plain: the six-lane gather instantiation, A/B knob BK_WIN_K24)
+    static const int w24 = env_int("BK_WIN_K24", 0);
+    if (!w24 && !a.C && a.k == 24 && a.kout == 24 && a.ldx % 4 == 0 && ((uintptr_t)a.X % 32) == 0 &&
+        a.ldy % 2 == 0 && ((uintptr_t)a.Y % 16) == 0)
+        return false;
     static const int w12 = env_int("BK_WIN_K12", 0);
     if (!w12 && a.k == 12 && a.kout == 12 && a.ldx % 4 == 0 && ((uintptr_t)a.X % 32) == 0 && a.ldy % 2 == 0 &&
         ((uintptr_t)a.Y % 16) == 0)

@@ -143,7 +143,7 @@ def _mixed_structure_csr(n_grid=40, bad=range(500, 540), seed=0):
                      torch.tensor(np.concatenate(ncol), dtype=torch.int32), torch.tensor(np.concatenate(nval)))
 
 
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 6, 8, 12, 16, 20, 32])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 6, 8, 12, 16, 20, 24, 32])
 def test_spmm_windowed_paths_bitwise(ctx, bk, k):
     """Windowed apply (X rows of each diagonal band staged in shared memory, DESIGN.md
     §4.1): stencils are band structured; odd n_cols (clipped last segment, odd k:
