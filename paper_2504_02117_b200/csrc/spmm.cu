@@ -504,6 +504,12 @@ void launch_k(const SpmmArgs& a, cudaStream_t st, bool vec2) {
             launch_pipe<24, 4, false, 288, 2, 3, 288, 2592>(a, num_sms_cached(), st);
             return;
         }
+        // k = 20: five lanes per row; 320 consumers = 64 rows per pass, two CTAs per SM with a
+        // three-stage ring (three 352-thread CTAs would cap the kernel at 62 registers)
+        if (vec2 && al32 && a.k == 20 && a.kout == 20 && !a.C && !a.Xg && !a.rows && a.nrows > 0) {
+            launch_pipe<20, 4, false, 320, 3, 2, 256, 2304>(a, num_sms_cached(), st);
+            return;
+        }
     }
     if constexpr (KP >= 4) {
         if (vec2 && al32 && a.k % 4 == 0 && a.kout % 4 == 0) return launch_kv<KP, 4>(a, st);
@@ -1351,9 +1357,9 @@ bool launch_bspmm_win(const SpmmArgs& a, const BandPlan& p, cudaStream_t st) {
     // k = 12 (e.g. 3 stages x 4 steps): the band kernel pads it to four 4-column lanes with a
     // run-time row stride; the gather kernel has a three-lane instantiation (launch_k) -- c2 plain
     // 83.0 vs 58.4 us (0.49 vs 0.70 of HBM), coupled 119 vs 87 us (profiles/r02/head/e22_*).
-    // (k = 24, plain: the six-lane gather instantiation, A/B knob BK_WIN_K24)
-    static const int w24 = env_int("BK_WIN_K24", 0);
-    if (!w24 && !a.C && a.k == 24 && a.kout == 24 && a.ldx % 4 == 0 && ((uintptr_t)a.X % 32) == 0 &&
+    // (k = 24 / 20, plain: the six- / five-lane gather instantiations, A/B knobs BK_WIN_K24 / K20)
+    static const int w24 = env_int("BK_WIN_K24", 0), w20 = env_int("BK_WIN_K20", 0);
+    if (((!w24 && a.k == 24 && a.kout == 24) || (!w20 && a.k == 20 && a.kout == 20)) && !a.C && a.ldx % 4 == 0 && ((uintptr_t)a.X % 32) == 0 &&
         a.ldy % 2 == 0 && ((uintptr_t)a.Y % 16) == 0)
         return false;
     static const int w12 = env_int("BK_WIN_K12", 0);

@@ -51,7 +51,7 @@ def check_close(got, ref, scale, tol=TOL, what=""):
 
 
 # ----------------------------------------------------------------------------- a1 apply
-@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 12, 16, 24, 32])
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5, 8, 12, 16, 20, 24, 32])
 def test_spmm_integer_bitwise(ctx, bk, k):
     A = synth.convdiff2d(40, integer=True)            # 1600 rows: 7 tiles incl. a ragged tail
     X = synth.multivector(A.n_rows, k, 3, integer=True)
