@@ -345,7 +345,7 @@ def run_ours(args):
     # ---- isolated k sweep (flush before every kernel; adds k = 32), outside the timed region
     sweep = {}
     if not args.no_sweep:
-        for k in (1, 2, 4, 8, 16, 32):
+        for k in (1, 2, 4, 8, 12, 16, 20, 24, 32):   # (12 / 20 / 24: the lane-exact gather instantiations)
             Xk = X[k] if k in X else synth.multivector(n, k, synth.SEEDS["X"], row_begin=r0, n_global=n_glob, device=dev)
             Yk = torch.empty(n, k, dtype=torch.float64, device=dev)
             Pk = P[k] if k in P else synth.multivector(n, k, synth.SEEDS["P"], device=dev)
